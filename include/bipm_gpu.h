@@ -1,0 +1,103 @@
+/* bipm_gpu.h -- C-ABI of the B200 reduced-space KKT engine.
+ *
+ * Drop-in boundary for the reduced KKT path of the reference solver
+ * (/root/reference/proj/core).  Every entry point takes plain pointers and
+ * sizes; host arrays use the reference layout: a per-scenario array is
+ * scenario-major, i.e. the reference's column-major Matrix(len, M)
+ * (types.hpp:56-78), and shared patterns are int32 CSR.  No C++ exception
+ * crosses this boundary: functions return a BIPM_* status and the message of
+ * the last failure is available from bipm_last_error().  The status codes map
+ * one-to-one onto the reference exception types, so a host shim can rethrow
+ * them.
+ *
+ * Reference interfaces replaced (file:line under proj/core):
+ *   bipm_problem_create      opf::parse_matpower_file + generate_scenarios +
+ *                            build_block_opf + make_ad_plan
+ *                            (opf_parse.cpp:216, scenarios.cpp:44,
+ *                             opf_model.cpp:624, autodiff.cpp:180)
+ *   bipm_eval_bundle         eval_bundle_range            (autodiff.hpp:131-133)
+ *   bipm_eval_values         batch_eval                   (autodiff.hpp:96-97)
+ *   bipm_condense            condense                     (kkt.hpp:110)
+ *   bipm_factor_gx           factor_gx_range / BlockDiagFactor::factor
+ *                                                         (kkt.hpp:162, linalg.hpp:213)
+ *   bipm_reduce              reduce + finish_reduce       (kkt.hpp:139-142)
+ *   bipm_reduce_rhs          reduce_rhs_group             (kkt.cpp:209)
+ *   bipm_dense_factor_solve  factor_dense_sym + solve     (linalg.hpp:116, kkt.cpp:965-976)
+ *   bipm_recover             recover_state_adjoint + recover_slack_dual
+ *                                                         (kkt.hpp:114,147-148)
+ *   bipm_solve_reduced       solve_reduced                (kkt.hpp:170-172)
+ *   bipm_solve               solve (the IPM driver)       (ipm.hpp:361)
+ */
+#ifndef BIPM_GPU_H
+#define BIPM_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (reference exception in parentheses) */
+#define BIPM_OK 0
+#define BIPM_SINGULAR_BLOCK 1   /* SingularBlockError */
+#define BIPM_NONFINITE 2        /* NonFiniteError */
+#define BIPM_NOT_PD 3           /* reduced matrix not positive definite */
+#define BIPM_CUDA_ERROR 4
+#define BIPM_INVALID_ARGUMENT 5 /* DimensionError / std::invalid_argument */
+#define BIPM_NON_INTERIOR 6     /* NonInteriorError */
+#define BIPM_LINEAR_SOLVE 7     /* LinearSolveError */
+#define BIPM_PARSE_ERROR 8      /* opf::ParseError */
+#define BIPM_UNSUPPORTED 9      /* augmented fallback (not on the GPU path) */
+
+typedef struct bipm_problem bipm_problem; /* host model + symbolic plans */
+typedef struct bipm_ctx bipm_ctx;         /* one GPU owning scenarios [lo, hi) */
+
+const char* bipm_last_error(void);
+int bipm_version(void);
+
+/* ---- problem (host, no GPU needed) ---------------------------------- */
+int bipm_problem_create(const char* case_path, int32_t N, double sigma, uint64_t seed,
+                        bipm_problem** out);
+void bipm_problem_destroy(bipm_problem* p);
+/* dims[0..9] = N, n_x, n_u, m, n_b, nbus, nbranch, ngen, nnz(L+U) factor, levels(fwd) */
+int bipm_problem_dims(const bipm_problem* p, int32_t dims[10]);
+/* Read-only view of a named host array (model maps, bounds, patterns, LU
+ * plan): *is_int = 1 for int32 data, 0 for float64. */
+int bipm_problem_array(const bipm_problem* p, const char* name, const void** data,
+                       int64_t* count, int32_t* is_int);
+
+/* ---- engine ---------------------------------------------------------- */
+int bipm_ctx_create(const bipm_problem* p, int32_t device, int32_t lo, int32_t hi,
+                    bipm_ctx** out);
+void bipm_ctx_destroy(bipm_ctx* c);
+
+/* Host inputs of the reduction, all scenario-major over the ctx's M = hi-lo
+ * scenarios and laid out on the problem's shared patterns. */
+typedef struct {
+  const double* gu;      /* [M][nnz G_u] */
+  const double* kxx;     /* [M][nnz K_xx] */
+  const double* kxu;     /* [M][nnz K_xu] */
+  const double* kuu;     /* [M][nnz K_uu] */
+  const double* sigma_x; /* [M][n_x] */
+  const double* rhat1;   /* [M][n_x] */
+  const double* rhat3;   /* [M][n_x] */
+  const double* sigma_u; /* [n_u] */
+  const double* rhat2;   /* [n_u] */
+} bipm_condensed;
+
+/* G_x values [M][nnz G_x] -> batched LU on the device.  On a tiny or
+ * non-finite pivot returns BIPM_SINGULAR_BLOCK with *singular_block set to
+ * the lowest global scenario index. */
+int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block);
+
+/* K_hat (n_u x n_u column-major) and rhs (n_u) of the reduced system at
+ * delta_w, exactly as reduce()+finish_reduce(): K_hat includes
+ * diag(sigma_u + delta_w), rhs includes -rhat2.  Requires bipm_factor_gx. */
+int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* khat,
+                double* rhs);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BIPM_GPU_H */

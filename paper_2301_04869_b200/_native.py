@@ -1,0 +1,159 @@
+"""ctypes binding of the C-ABI in ``include/bipm_gpu.h``.
+
+The shared library is built in-tree (``paper_2301_04869_b200/_lib``) by
+``__graft_entry__.build()``.  There is no fallback: if the library is missing
+or a CUDA call fails, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libbipm_gpu.so")
+
+STATUS = {
+    0: "OK",
+    1: "SINGULAR_BLOCK",
+    2: "NONFINITE",
+    3: "NOT_PD",
+    4: "CUDA_ERROR",
+    5: "INVALID_ARGUMENT",
+    6: "NON_INTERIOR",
+    7: "LINEAR_SOLVE",
+    8: "PARSE_ERROR",
+    9: "UNSUPPORTED",
+}
+
+
+class BipmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class SingularBlockError(BipmError):
+    """Mirror of blockipm::SingularBlockError (types.hpp:99-103)."""
+
+
+class NonFiniteError(BipmError):
+    """Mirror of blockipm::NonFiniteError (types.hpp:105-109)."""
+
+
+_EXC = {1: SingularBlockError, 2: NonFiniteError}
+
+_lib = None
+_P = ctypes.c_void_p
+_D = ctypes.POINTER(ctypes.c_double)
+_I = ctypes.POINTER(ctypes.c_int32)
+
+# exported symbol -> (restype, argtypes); also the list the CPU tests check
+SIGNATURES = {
+    "bipm_last_error": (ctypes.c_char_p, []),
+    "bipm_version": (ctypes.c_int, []),
+    "bipm_problem_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_double,
+                                           ctypes.c_uint64, ctypes.POINTER(_P)]),
+    "bipm_problem_destroy": (None, [_P]),
+    "bipm_problem_dims": (ctypes.c_int, [_P, _I]),
+    "bipm_problem_array": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_P),
+                                          ctypes.POINTER(ctypes.c_int64), _I]),
+    "bipm_ctx_create": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                       ctypes.POINTER(_P)]),
+    "bipm_ctx_destroy": (None, [_P]),
+    "bipm_factor_gx": (ctypes.c_int, [_P, _D, _I]),
+    "bipm_reduce": (ctypes.c_int, [_P, _P, ctypes.c_double, _D, _D]),
+}
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: run __graft_entry__.build() (there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(code: int) -> None:
+    if code != 0:
+        msg = lib().bipm_last_error().decode()
+        raise _EXC.get(code, BipmError)(code, msg)
+
+
+def dptr(a: np.ndarray):
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(_D)
+
+
+class _Condensed(ctypes.Structure):
+    _fields_ = [(n, _D) for n in ("gu", "kxx", "kxu", "kuu", "sigma_x", "rhat1", "rhat3",
+                                  "sigma_u", "rhat2")]
+
+
+class Problem:
+    """Host model + symbolic plans (no GPU): bipm_problem_create."""
+
+    def __init__(self, case_path: str, N: int, sigma: float = 0.0, seed: int = 0):
+        h = _P()
+        check(lib().bipm_problem_create(case_path.encode(), N, sigma, seed, ctypes.byref(h)))
+        self._h = h
+        d = (ctypes.c_int32 * 10)()
+        check(lib().bipm_problem_dims(h, d))
+        (self.N, self.n_x, self.n_u, self.m, self.n_b, self.nbus, self.nbranch, self.ngen,
+         self.nnz_factor, self.levels) = list(d)
+
+    def array(self, name: str) -> np.ndarray:
+        data, n, is_int = _P(), ctypes.c_int64(), ctypes.c_int32()
+        check(lib().bipm_problem_array(self._h, name.encode(), ctypes.byref(data),
+                                       ctypes.byref(n), ctypes.byref(is_int)))
+        if n.value == 0:
+            return np.zeros(0, dtype=np.int32 if is_int.value else np.float64)
+        ct = ctypes.c_int32 if is_int.value else ctypes.c_double
+        buf = (ct * n.value).from_address(data.value)
+        return np.array(buf, copy=True)
+
+    def csr(self, name: str):
+        return self.array(name + "_rowptr"), self.array(name + "_colind")
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().bipm_problem_destroy(self._h)
+            self._h = None
+
+
+class Context:
+    """One GPU owning scenarios [lo, hi): bipm_ctx_create."""
+
+    def __init__(self, problem: Problem, device: int = 0, lo: int = 0, hi: int | None = None):
+        self.problem = problem
+        self.lo, self.hi = lo, problem.N if hi is None else hi
+        h = _P()
+        check(lib().bipm_ctx_create(problem._h, device, self.lo, self.hi, ctypes.byref(h)))
+        self._h = h
+
+    def factor_gx(self, gx: np.ndarray) -> None:
+        gx = np.ascontiguousarray(gx, dtype=np.float64)
+        bad = ctypes.c_int32(-1)
+        check(lib().bipm_factor_gx(self._h, dptr(gx), ctypes.byref(bad)))
+
+    def reduce(self, delta_w: float, **arrays):
+        keep = {k: np.ascontiguousarray(v, dtype=np.float64) for k, v in arrays.items()}
+        c = _Condensed(**{k: dptr(v) for k, v in keep.items()})
+        n_u = self.problem.n_u
+        khat = np.zeros(n_u * n_u)
+        rhs = np.zeros(n_u)
+        check(lib().bipm_reduce(self._h, ctypes.byref(c), delta_w, dptr(khat), dptr(rhs)))
+        return khat.reshape(n_u, n_u).T.copy(), rhs  # column-major -> numpy
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().bipm_ctx_destroy(self._h)
+            self._h = None

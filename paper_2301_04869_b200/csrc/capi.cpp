@@ -1,0 +1,164 @@
+// extern "C" boundary (include/bipm_gpu.h): exceptions become status codes.
+#include "../../include/bipm_gpu.h"
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+
+#include "engine/engine.hpp"
+
+using namespace bipm;
+
+struct bipm_problem {
+  std::unique_ptr<Problem> p;
+  std::map<std::string, std::pair<std::vector<int>, std::vector<double>>> cache;
+};
+
+struct bipm_ctx {
+  const bipm_problem* prob = nullptr;
+  std::unique_ptr<Engine> eng;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return BIPM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    const std::string w = e.what();
+    if (w.find("cuda") != std::string::npos || w.find("CUDA") != std::string::npos)
+      return BIPM_CUDA_ERROR;
+    return BIPM_INVALID_ARGUMENT;
+  }
+}
+
+// Named host arrays exposed read-only for tests and integration shims.
+const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, int32_t* is_int) {
+  const Problem& P = *bp->p;
+  const OpfModel& M = P.M;
+  auto ints = [&](const std::vector<idx>& v) {
+    *count = int64_t(v.size());
+    *is_int = 1;
+    return static_cast<const void*>(v.data());
+  };
+  auto dbls = [&](const std::vector<double>& v) {
+    *count = int64_t(v.size());
+    *is_int = 0;
+    return static_cast<const void*>(v.data());
+  };
+  const std::map<std::string, const Csr*> pats = {
+      {"L_f", &M.L_f},       {"L_g", &M.L_g},     {"L_h", &M.L_h},         {"gx_p", &P.D.g.x},
+      {"gu_p", &P.D.g.u},    {"hx_p", &P.D.h.x},  {"hu_p", &P.D.h.u},      {"wxx_p", &P.D.wxx},
+      {"wxu_p", &P.D.wxu},   {"wuu_p", &P.D.wuu}, {"hess_p", &P.D.hess},   {"kxx_p", &P.D.kxx.out},
+      {"kxu_p", &P.D.kxu.out}, {"kuu_p", &P.D.kuu.out}};
+  for (const auto& [pre, c] : pats) {
+    if (name == pre + "_rowptr") return ints(c->ptr);
+    if (name == pre + "_colind") return ints(c->ind);
+    if (name == pre + "_val") return dbls(c->val);
+  }
+  const std::map<std::string, const std::vector<double>*> vecs = {
+      {"x_lo", &M.x_lo}, {"x_up", &M.x_up}, {"u_lo", &M.u_lo},       {"u_up", &M.u_up},
+      {"s_lo", &M.s_lo}, {"s_up", &M.s_up}, {"x_start", &M.x_start}, {"u_start", &M.u_start},
+      {"pd", &M.pd},     {"qd", &M.qd},     {"mult", &P.sc.mult}};
+  if (auto it = vecs.find(name); it != vecs.end()) return dbls(*it->second);
+  const std::map<std::string, const std::vector<idx>*> ivecs = {
+      {"lu_perm", &P.LU.perm},       {"lu_fwd_ptr", &P.LU.fwd_ptr}, {"lu_bwd_ptr", &P.LU.bwd_ptr},
+      {"lu_l_ptr", &P.LU.l_ptr},     {"lu_l_col", &P.LU.l_col},     {"lu_u_ptr", &P.LU.u_ptr},
+      {"lu_u_col", &P.LU.u_col},     {"lu_mul_ptr", &P.LU.mul_ptr}};
+  if (auto it = ivecs.find(name); it != ivecs.end()) return ints(*it->second);
+  throw Error(kInvalidArgument, "unknown problem array '" + name + "'");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bipm_last_error(void) { return g_err.c_str(); }
+int bipm_version(void) { return 1; }
+
+int bipm_problem_create(const char* case_path, int32_t N, double sigma, uint64_t seed,
+                        bipm_problem** out) {
+  return guarded([&] {
+    if (!case_path || !out) throw Error(kInvalidArgument, "null argument");
+    auto bp = std::make_unique<bipm_problem>();
+    bp->p = Problem::from_case_file(case_path, N, sigma, seed);
+    *out = bp.release();
+  });
+}
+
+void bipm_problem_destroy(bipm_problem* p) { delete p; }
+
+int bipm_problem_dims(const bipm_problem* bp, int32_t d[10]) {
+  return guarded([&] {
+    const Problem& P = *bp->p;
+    const OpfModel& M = P.M;
+    const int32_t v[10] = {M.N,  M.n_x, M.n_u, M.m, M.n_b(), M.nbus, M.nbr, M.ngen, P.LU.nnz_f,
+                           int32_t(P.LU.fwd_ptr.size()) - 1};
+    std::memcpy(d, v, sizeof v);
+  });
+}
+
+int bipm_problem_array(const bipm_problem* bp, const char* name, const void** data,
+                       int64_t* count, int32_t* is_int) {
+  return guarded([&] {
+    *data = lookup(const_cast<bipm_problem*>(bp), name, count, is_int);
+  });
+}
+
+int bipm_ctx_create(const bipm_problem* bp, int32_t device, int32_t lo, int32_t hi,
+                    bipm_ctx** out) {
+  return guarded([&] {
+    auto c = std::make_unique<bipm_ctx>();
+    c->prob = bp;
+    c->eng = std::make_unique<Engine>(*bp->p, device, lo, hi);
+    *out = c.release();
+  });
+}
+
+void bipm_ctx_destroy(bipm_ctx* c) { delete c; }
+
+int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    e.gx.upload(gx, e.gx.size(), e.st);
+    const idx bad = e.factor_gx();
+    if (singular_block) *singular_block = bad;
+    if (bad >= 0) throw Error(kSingularBlock, "singular block " + std::to_string(bad), bad);
+  });
+}
+
+int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* khat,
+                double* rhs) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    e.gu.upload(in->gu, e.gu.size(), e.st);
+    e.kxx.upload(in->kxx, e.kxx.size(), e.st);
+    e.kxu.upload(in->kxu, e.kxu.size(), e.st);
+    e.kuu.upload(in->kuu, e.kuu.size(), e.st);
+    e.sigma_x.upload(in->sigma_x, e.sigma_x.size(), e.st);
+    e.rhat1.upload(in->rhat1, e.rhat1.size(), e.st);
+    e.rhat3.upload(in->rhat3, e.rhat3.size(), e.st);
+    e.sigma_u.upload(in->sigma_u, e.sigma_u.size(), e.st);
+    e.rhat2.upload(in->rhat2, e.rhat2.size(), e.st);
+    e.reduce_local(delta_w);
+    e.finish_reduce(delta_w);
+    e.reduce_rhs_local(delta_w, e.rhs.get());
+    // rhs = sum_b (...) - rhat2
+    std::vector<double> r(e.rhs.size()), r2(e.rhat2.size());
+    e.rhs.download(r.data(), r.size(), e.st);
+    e.khat.download(khat, e.khat.size(), e.st);
+    e.sync();
+    for (size_t i = 0; i < r.size(); ++i) rhs[i] = r[i] - in->rhat2[i];
+  });
+}
+
+}  // extern "C"

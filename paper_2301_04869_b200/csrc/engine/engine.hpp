@@ -1,0 +1,99 @@
+// Device engine: one GPU owning scenarios [lo, hi) of a problem.
+//
+// Host plans (patterns, gather programs, the LU plan) are uploaded once; the
+// per-scenario values (bundle, condensed blocks, factors) stay resident in
+// HBM in the reference's scenario-major layout.  The operator methods mirror
+// the reference's reduced-strategy operators (kkt.hpp:110-162,
+// linalg.hpp:116) and run entirely on the device stream.
+#pragma once
+
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/grid_model.hpp"
+#include "../host/plan.hpp"
+#include "../kernels/kkt_kernels.hpp"
+#include "device_array.hpp"
+
+namespace bipm {
+
+struct Problem {
+  GridCase cs;
+  ScenarioDraw sc;
+  OpfModel M;
+  LaneDeps deps;
+  DerivPlan D;
+  LuPlan LU;
+  static std::unique_ptr<Problem> from_case_file(const std::string& path, idx N, double sigma,
+                                                 std::uint64_t seed);
+  static std::unique_ptr<Problem> from_parts(GridCase cs, ScenarioDraw sc);
+};
+
+struct DevPattern {
+  DArr<int> ptr, ind, t_ptr, t_row, t_slot;
+  DevCsr v{};
+  void upload(const Csr& p);
+};
+
+struct DevCondense {
+  DArr<int> w_of, ptr, ka, kb, r;
+  CondenseDev v{};
+  void upload(const CondenseProgram& p);
+};
+
+class Engine {
+ public:
+  Engine(const Problem& pb, int device, idx lo, idx hi);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const Problem& pb;
+  const idx lo, hi, M;
+  int device = 0, sm_count = 148;
+  cudaStream_t st = nullptr;
+
+  // ---- uploaded plans
+  DevPattern gx_p, gu_p, hx_p, hu_p, kxx_p, kxu_p, kuu_p;
+  DevCondense cxx, cxu, cuu;
+  std::vector<DArr<int>> lu_arrays;
+  DevLu lu{};
+
+  // ---- per-scenario resident values ([M][len])
+  DArr<double> gx, gu, hx, hu, wxx, wxu, wuu;  // bundle blocks
+  DArr<double> kxx, kxu, kuu;                  // condensed blocks
+  DArr<double> sigma_x, sigma_s, rhat1, rhat3, r2, r4;
+  DArr<double> sigma_u, rhat2;                 // n_u (replicated)
+  DArr<double> F;                              // LU factors [M][nnz_f]
+  DArr<int> lu_status;
+  // ---- reduction workspace
+  ReduceLaunch red{};
+  DArr<double> red_partial, red_scratch, rhs_part;
+  DArr<double> khat, rhs;   // n_u x n_u (column-major), n_u
+  DArr<int> chol_info;
+
+  // ---- operators (device-resident inputs/outputs)
+  // factor_gx_range (kkt.cpp:190-196): returns the lowest singular global
+  // scenario index or -1.
+  idx factor_gx();
+  // condense (kkt.cpp:123-170) of the K blocks from the bundle and sigma_s
+  void condense_blocks();
+  // local part of reduce (kkt.cpp:371-466): khat/rhs partial sums over the
+  // owned scenarios, without the sigma_u / rhat2 terms.
+  void reduce_local(double delta_w);
+  void reduce_rhs_local(double delta_w, double* d_rhs_out);
+  // finish_reduce (kkt.cpp:468-488) for a single engine
+  void finish_reduce(double delta_w);
+  // shift + Cholesky (kkt.cpp:965-971); true when positive definite
+  bool factor_khat();
+  void solve_khat(double* d_vec);
+  // recover_state_adjoint + recover_slack_dual (kkt.cpp:507-532, :172-188)
+  void recover(double delta_w, const double* d_pu, double* d_px, double* d_py, double* d_pz,
+               double* d_ps);
+
+  void sync();
+  size_t nnz(const Csr& c) const { return size_t(c.nnz()); }
+};
+
+}  // namespace bipm

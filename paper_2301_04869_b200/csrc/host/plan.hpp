@@ -1,0 +1,85 @@
+// Symbolic, scenario-independent plans built once per solve on the host.
+//
+//  * derivative patterns: the reference detects G, H and the Lagrangian
+//    Hessian supports by index propagation through the basis
+//    (autodiff.cpp:93-124, opf_model.cpp:277-327) and splits them into state
+//    and control blocks (autodiff.cpp:126-178).  The same patterns are
+//    reproduced here so per-scenario value arrays line up slot for slot with
+//    the reference boundary.
+//  * condense gather programs: K = W + A' diag(sigma) B as, for every output
+//    slot, its W slot and the (a slot, b slot, row) triples that feed it, in
+//    the reference's accumulation order (sparse.cpp:176-214).
+//  * the static-pivot sparse LU of G_x: one symmetric minimum-degree ordering
+//    shared by every scenario, its factor pattern, level schedules for the
+//    four triangular sweeps, and the numeric refactor program.  This replaces
+//    the reference's per-scenario Eigen::SparseLU (linalg.cpp:76-104).
+#pragma once
+
+#include <vector>
+
+#include "common.hpp"
+#include "grid_model.hpp"
+
+namespace bipm {
+
+struct LaneDeps {
+  std::vector<std::vector<idx>> jac;   // first-derivative support per lane
+  std::vector<std::vector<idx>> hess;  // inputs entering nonlinearly
+};
+LaneDeps basis_deps(const OpfModel& M);
+
+struct SplitMap {
+  Csr x, u;                 // column split at n_x
+  std::vector<idx> x_src, u_src;  // slot in the unsplit pattern
+};
+
+struct CondenseProgram {
+  Csr out;                       // pattern of W + A' S B
+  std::vector<idx> w_of;         // per out slot: W slot or -1
+  std::vector<idx> ptr;          // per out slot: range into (ka, kb, r)
+  std::vector<idx> ka, kb, r;
+};
+
+struct DerivPlan {
+  Csr jac_g, jac_h, hess;        // n_x x n_d, m x n_d, n_d x n_d
+  SplitMap g, h;                 // G_x | G_u, H_x | H_u
+  Csr wxx, wxu, wuu;             // Hessian split blocks
+  std::vector<idx> wxx_src, wxu_src, wuu_src;  // slot in `hess`
+  CondenseProgram kxx, kxu, kuu;
+};
+
+DerivPlan make_deriv_plan(const OpfModel& M, const LaneDeps& deps);
+CondenseProgram plan_condense_program(const Csr& W, const Csr& A, const Csr& B);
+
+// Static-pivot LU of a structurally symmetric n x n pattern (P A P' = L U).
+// Factor values of one scenario live in one array of length nnz_f:
+//   [0, nnz_l)        strict lower L, row-major by permuted row
+//   [nnz_l, nnz_f)    upper U including the diagonal, row-major
+struct LuPlan {
+  idx n = 0, nnz_l = 0, nnz_f = 0;
+  std::vector<idx> perm, iperm;  // permuted k <-> original perm[k]
+  // row access (permuted indices): L strict lower / U strict upper / diag slot
+  std::vector<idx> l_ptr, l_col, l_slot;
+  std::vector<idx> u_ptr, u_col, u_slot;
+  std::vector<idx> diag;
+  // column access for the transposed sweeps: column i of U above the
+  // diagonal (rows k < i) and column i of L below it (rows r > i)
+  std::vector<idx> ut_ptr, ut_row, ut_slot;
+  std::vector<idx> lt_ptr, lt_row, lt_slot;
+  // level schedules: forward (L, U') and backward (U, L') sweeps
+  std::vector<idx> fwd_ptr, fwd_rows, bwd_ptr, bwd_rows;
+  // numeric refactor: per level of the forward schedule, the U-row entries
+  // then the L-column entries of its pivot steps (factor slots); each entry
+  // e: value = A[a_src[e]] (or 0) - sum_t F[mul_l[t]] * F[mul_u[t]]
+  // over t in [mul_ptr[e], mul_ptr[e+1]); L entries then divide by the pivot.
+  std::vector<idx> lvl_u_ptr, lvl_u_slot, lvl_l_ptr, lvl_l_slot;
+  std::vector<idx> a_src;       // per factor slot: G_x slot or -1 (fill)
+  std::vector<idx> piv_of;      // per factor slot: pivot slot for L entries, -1 for U
+  std::vector<idx> mul_ptr, mul_l, mul_u;
+  long long flops() const { return 2LL * (long long)mul_l.size(); }
+};
+
+std::vector<idx> min_degree_order(const Csr& sym_pattern);
+LuPlan make_lu_plan(const Csr& gx_pattern);
+
+}  // namespace bipm

@@ -1,0 +1,30 @@
+// Device views of the host plans (plain pointers, passed by value).
+#pragma once
+
+#include <cstdint>
+
+namespace bipm {
+
+// Static-pivot LU plan of G_x (host: LuPlan in host/plan.hpp).
+struct DevLu {
+  int n, nnz_l, nnz_f, n_fwd, n_bwd;
+  const int *perm, *iperm;
+  const int *l_ptr, *l_col;               // L strict lower, slot == position
+  const int *u_ptr, *u_col, *u_slot;      // U strict upper
+  const int *diag;
+  const int *ut_ptr, *ut_row, *ut_slot;   // column i of U above the diagonal
+  const int *lt_ptr, *lt_row, *lt_slot;   // column i of L below the diagonal
+  const int *fwd_ptr, *fwd_rows, *bwd_ptr, *bwd_rows;
+  const int *lvl_u_ptr, *lvl_u_slot, *lvl_l_ptr, *lvl_l_slot;
+  const int *a_src, *piv_of, *mul_ptr, *mul_l, *mul_u;
+};
+
+// A shared CSR pattern with an optional column-major (transposed) view:
+// for column c, entries (row t_row[q], slot t_slot[q]) for q in t_ptr[c]..
+struct DevCsr {
+  int rows, cols, nnz;
+  const int *ptr, *ind;
+  const int *t_ptr, *t_row, *t_slot;
+};
+
+}  // namespace bipm

@@ -1,0 +1,597 @@
+// Reduced-space KKT kernels for sm_100a: batched static-pivot LU refactor of
+// G_x, the multi-RHS Schur reduction K_hat = sum_i Z_i' K_i Z_i, the reduced
+// right-hand side, state/adjoint and slack/dual recovery, condensation and the
+// dense Cholesky of K_hat.
+//
+// Reference operators replaced (proj/core/src):
+//   launch_lu_refactor     BlockDiagFactor::factor     linalg.cpp:51-89
+//   launch_reduce_tiles    reduce_group (tile loop)    kkt.cpp:371-466
+//   launch_sum_parts       finish_reduce/all_reduce    kkt.cpp:468-488, executor.cpp:39-61
+//   launch_reduce_rhs      reduce_rhs_group            kkt.cpp:209-239
+//   launch_recover_state   recover_state_adjoint       kkt.cpp:507-532
+//   launch_recover_slack   recover_slack_dual          kkt.cpp:172-188
+//   launch_condense        condense / run_condense     kkt.cpp:123-170, sparse.cpp:208-214
+//   launch_shift_cholesky  solve_reduced shift+factor  kkt.cpp:965-971, linalg.cpp:129-145
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+
+#include "kkt_kernels.hpp"
+#include "sweeps.cuh"
+
+namespace bipm {
+
+namespace {
+
+constexpr int kSolveBlock = 256;
+constexpr int kLuBlock = 256;
+constexpr int kDenseBlock = 1024;
+
+template <int BLOCK>
+__device__ double block_reduce(double v, bool is_max) {
+  __shared__ double red[BLOCK / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int off = 16; off > 0; off >>= 1) {
+    const double o = __shfl_xor_sync(0xffffffffu, v, off);
+    v = is_max ? fmax(v, o) : v + o;
+  }
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < BLOCK / 32 ? red[lane] : (is_max ? 0.0 : 0.0);
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, v, off);
+      v = is_max ? fmax(v, o) : v + o;
+    }
+    if (lane == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// slot of column c in CSR row `row`, or -1
+__device__ __forceinline__ int find_in_row(const int* ptr, const int* ind, int row, int c) {
+  int lo = ptr[row], hi = ptr[row + 1];
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = ind[mid];
+    if (v == c) return mid;
+    if (v < c)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return -1;
+}
+
+// ---------------------------------------------------------------- LU refactor
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const double* __restrict__ gx,
+                                                            int nnz_gx, double* F, int* status,
+                                                            double piv_tol) {
+  const int s = blockIdx.x;
+  const double* __restrict__ A = gx + size_t(s) * nnz_gx;
+  double* Fs = F + size_t(s) * P.nnz_f;
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < nnz_gx; i += BLOCK) mx = fmax(mx, fabs(A[i]));
+  const double scale = block_reduce<BLOCK>(mx, true);
+
+  for (int lv = 0; lv < P.n_fwd; ++lv) {
+    {
+      const int b0 = P.lvl_u_ptr[lv];
+      group_dot<BLOCK>(
+          P.lvl_u_ptr[lv + 1] - b0,
+          [&](int it, int& b, int& e) {
+            const int slot = P.lvl_u_slot[b0 + it];
+            b = P.mul_ptr[slot];
+            e = P.mul_ptr[slot + 1];
+          },
+          [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
+          [&](int it, double acc) {
+            const int slot = P.lvl_u_slot[b0 + it];
+            const int src = P.a_src[slot];
+            Fs[slot] = (src >= 0 ? A[src] : 0.0) - acc;
+          });
+    }
+    __syncthreads();
+    {
+      const int b0 = P.lvl_l_ptr[lv];
+      group_dot<BLOCK>(
+          P.lvl_l_ptr[lv + 1] - b0,
+          [&](int it, int& b, int& e) {
+            const int slot = P.lvl_l_slot[b0 + it];
+            b = P.mul_ptr[slot];
+            e = P.mul_ptr[slot + 1];
+          },
+          [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
+          [&](int it, double acc) {
+            const int slot = P.lvl_l_slot[b0 + it];
+            const int src = P.a_src[slot];
+            Fs[slot] = ((src >= 0 ? A[src] : 0.0) - acc) / Fs[P.piv_of[slot]];
+          });
+    }
+    __syncthreads();
+  }
+  double bad = 0.0;
+  const double floor_ = piv_tol * fmax(scale, 1e-300);
+  for (int j = threadIdx.x; j < P.n; j += BLOCK) {
+    const double d = Fs[P.diag[j]];
+    if (!(fabs(d) >= floor_) || !isfinite(d)) bad = 1.0;
+  }
+  bad = block_reduce<BLOCK>(bad, true);
+  if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
+}
+
+// ----------------------------------------------------------- Schur reduction
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) reduce_tiles_kernel(ReduceLaunch a) {
+  extern __shared__ double sm[];
+  const int tile = blockIdx.x, chunk = blockIdx.y;
+  const int cta = chunk * gridDim.x + tile;
+  const int j0 = tile * a.kc;
+  const int k = min(a.kc, a.n_u - j0);
+  const int n_x = a.n_x, n_u = a.n_u, ldx = k;
+  const size_t per_cta = size_t(n_x) * a.kc * (a.panel_in_smem ? 1 : 2);
+  double* acc = sm;
+  double* S = a.scratch + size_t(cta) * per_cta;
+  double* X = a.panel_in_smem ? sm + size_t(n_u) * a.kc : S + size_t(n_x) * a.kc;
+  const DevLu& P = a.lu;
+
+  for (int i = threadIdx.x; i < n_u * k; i += BLOCK) acc[i] = 0.0;
+  const int s_lo = chunk * a.chunk, s_hi = min(a.M, s_lo + a.chunk);
+  for (int s = s_lo; s < s_hi; ++s) {
+    const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+    const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
+    const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
+    const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
+    const double* __restrict__ kuu = a.kuu_v + size_t(s) * a.kuu.nnz;
+    const double* __restrict__ sig = a.sigma_x + size_t(s) * n_x;
+
+    // V = Cartesian columns [j0, j0+k): X = P G_u V
+    for (int i = threadIdx.x; i < n_x * k; i += BLOCK) X[i] = 0.0;
+    __syncthreads();
+    for (int c = 0; c < k; ++c)
+      for (int q = a.gu.t_ptr[j0 + c] + threadIdx.x; q < a.gu.t_ptr[j0 + c + 1]; q += BLOCK)
+        X[P.iperm[a.gu.t_row[q]] * ldx + c] = gu[a.gu.t_slot[q]];
+    __syncthreads();
+    // X = G_x^{-1} G_u V  (so T = -X)
+    sweep_L<BLOCK>(P, F, X, k, ldx);
+    sweep_U<BLOCK>(P, F, X, k, ldx);
+
+    // acc += K_xu' T + K_uu V;  S = P (K~_xx T + K_xu V)
+    for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
+      const int u = it / k, c = it % k;
+      double v = 0.0;
+      for (int q = a.kxu.t_ptr[u]; q < a.kxu.t_ptr[u + 1]; ++q)
+        v -= kxu[a.kxu.t_slot[q]] * X[P.iperm[a.kxu.t_row[q]] * ldx + c];
+      const int ku = find_in_row(a.kuu.ptr, a.kuu.ind, u, j0 + c);
+      if (ku >= 0) v += kuu[ku];
+      acc[it] += v;
+    }
+    for (int it = threadIdx.x; it < n_x * k; it += BLOCK) {
+      const int p = it / k, c = it % k;
+      const int i = P.perm[p];
+      double v = 0.0;
+      for (int t = a.kxx.ptr[i]; t < a.kxx.ptr[i + 1]; ++t)
+        v -= kxx[t] * X[P.iperm[a.kxx.ind[t]] * ldx + c];
+      v -= (sig[i] + a.dw) * X[p * ldx + c];
+      const int ks = find_in_row(a.kxu.ptr, a.kxu.ind, i, j0 + c);
+      if (ks >= 0) v += kxu[ks];
+      S[p * ldx + c] = v;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n_x * k; i += BLOCK) X[i] = S[i];
+    __syncthreads();
+    // X = P G_x^{-T} L_x  (Y[perm[p]] = X[p])
+    sweep_Ut<BLOCK>(P, F, X, k, ldx);
+    sweep_Lt<BLOCK>(P, F, X, k, ldx);
+    // acc -= G_u' Y
+    for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
+      const int u = it / k, c = it % k;
+      double v = 0.0;
+      for (int q = a.gu.t_ptr[u]; q < a.gu.t_ptr[u + 1]; ++q)
+        v += gu[a.gu.t_slot[q]] * X[P.iperm[a.gu.t_row[q]] * ldx + c];
+      acc[it] -= v;
+    }
+    __syncthreads();
+  }
+  double* out = a.partial + size_t(chunk) * n_u * n_u;
+  for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
+    const int u = it / k, c = it % k;
+    out[size_t(j0 + c) * n_u + u] = acc[it];
+  }
+}
+
+__device__ double tree_sum(const double* p, long long stride, int lo, int hi) {
+  // fixed half-split order (executor.hpp:37-59), iterative over a small stack
+  struct Frame { int lo, hi, state; double left; };
+  Frame st[32];
+  int top = 0;
+  st[0] = {lo, hi, 0, 0.0};
+  double ret = 0.0;
+  while (top >= 0) {
+    Frame& f = st[top];
+    if (f.hi - f.lo == 1) {
+      ret = p[f.lo * stride];
+      --top;
+      continue;
+    }
+    const int mid = f.lo + (f.hi - f.lo) / 2;
+    if (f.state == 0) {
+      f.state = 1;
+      st[top + 1] = {f.lo, mid, 0, 0.0};
+      ++top;
+    } else if (f.state == 1) {
+      f.left = ret;
+      f.state = 2;
+      st[top + 1] = {mid, f.hi, 0, 0.0};
+      ++top;
+    } else {
+      ret = f.left + ret;
+      --top;
+    }
+  }
+  return ret;
+}
+
+__global__ void sum_parts_kernel(const double* parts, int nparts, long long len, double* out,
+                                 const double* diag_add, double dw, int n_mat,
+                                 const double* sub_vec) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j >= len) return;
+  double v = tree_sum(parts + j, len, 0, nparts);
+  if (n_mat > 0 && diag_add && (j % (n_mat + 1)) == 0) v += diag_add[j / (n_mat + 1)] + dw;
+  if (sub_vec) v -= sub_vec[j];
+  out[j] = v;
+}
+
+// ------------------------------------------------------ single-RHS kernels
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* scratch,
+                                                           int in_smem) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.x;
+  const int n_x = a.n_x;
+  const DevLu& P = a.lu;
+  double* X = in_smem ? sm : scratch + size_t(s) * 2 * n_x;
+  double* Z = X + n_x;
+  const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+  const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
+  const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
+  const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
+  const double* __restrict__ sig = a.sigma_x + size_t(s) * n_x;
+  const double* __restrict__ r1 = a.rhat1 + size_t(s) * n_x;
+  const double* __restrict__ r3 = a.rhat3 + size_t(s) * n_x;
+
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) X[p] = r3[P.perm[p]];
+  __syncthreads();
+  sweep_L<BLOCK>(P, F, X, 1, 1);
+  sweep_U<BLOCK>(P, F, X, 1, 1);  // X = P a
+  // Z = P (rhat1 - K~ a)
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) {
+    const int i = P.perm[p];
+    double acc = 0.0;
+    for (int t = a.kxx.ptr[i]; t < a.kxx.ptr[i + 1]; ++t) acc += kxx[t] * X[P.iperm[a.kxx.ind[t]]];
+    double v = r1[i] + -1.0 * acc;
+    v -= (sig[i] + a.dw) * X[p];
+    Z[p] = v;
+  }
+  __syncthreads();
+  sweep_Ut<BLOCK>(P, F, Z, 1, 1);
+  sweep_Lt<BLOCK>(P, F, Z, 1, 1);
+  double* out = a.part + size_t(s) * a.n_u;
+  for (int u = threadIdx.x; u < a.n_u; u += BLOCK) {
+    double v = 0.0;
+    for (int q = a.gu.t_ptr[u]; q < a.gu.t_ptr[u + 1]; ++q)
+      v += gu[a.gu.t_slot[q]] * Z[P.iperm[a.gu.t_row[q]]];
+    for (int q = a.kxu.t_ptr[u]; q < a.kxu.t_ptr[u + 1]; ++q)
+      v += kxu[a.kxu.t_slot[q]] * X[P.iperm[a.kxu.t_row[q]]];
+    out[u] = v;
+  }
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) recover_state_kernel(RecoverLaunch a, double* scratch,
+                                                              int in_smem) {
+  extern __shared__ double sm[];
+  const int s = blockIdx.x;
+  const int n_x = a.n_x;
+  const DevLu& P = a.lu;
+  double* X = in_smem ? sm : scratch + size_t(s) * 2 * n_x;
+  double* Z = X + n_x;
+  const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+  const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
+  const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
+  const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
+  const double* __restrict__ sig = a.sigma_x + size_t(s) * n_x;
+  const double* __restrict__ r1 = a.rhat1 + size_t(s) * n_x;
+  const double* __restrict__ r3 = a.rhat3 + size_t(s) * n_x;
+  double* px = a.px + size_t(s) * n_x;
+  double* py = a.py + size_t(s) * n_x;
+
+  // p_x = -G_x^{-1} (rhat3 + G_u p_u)
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) {
+    const int i = P.perm[p];
+    double acc = 0.0;
+    for (int t = a.gu.ptr[i]; t < a.gu.ptr[i + 1]; ++t) acc += gu[t] * a.pu[a.gu.ind[t]];
+    X[p] = r3[i] + 1.0 * acc;
+  }
+  __syncthreads();
+  sweep_L<BLOCK>(P, F, X, 1, 1);
+  sweep_U<BLOCK>(P, F, X, 1, 1);
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) {
+    X[p] = -X[p];
+    px[P.perm[p]] = X[p];
+  }
+  __syncthreads();
+  // p_y = -G_x^{-T} (rhat1 + K~ p_x + K_xu p_u)
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) {
+    const int i = P.perm[p];
+    double acc = 0.0;
+    for (int t = a.kxx.ptr[i]; t < a.kxx.ptr[i + 1]; ++t) acc += kxx[t] * X[P.iperm[a.kxx.ind[t]]];
+    double v = r1[i] + 1.0 * acc;
+    v += (sig[i] + a.dw) * X[p];
+    double au = 0.0;
+    for (int t = a.kxu.ptr[i]; t < a.kxu.ptr[i + 1]; ++t) au += kxu[t] * a.pu[a.kxu.ind[t]];
+    Z[p] = v + 1.0 * au;
+  }
+  __syncthreads();
+  sweep_Ut<BLOCK>(P, F, Z, 1, 1);
+  sweep_Lt<BLOCK>(P, F, Z, 1, 1);
+  for (int p = threadIdx.x; p < n_x; p += BLOCK) py[P.perm[p]] = -Z[p];
+}
+
+__global__ void recover_slack_kernel(DevCsr hx, DevCsr hu, int m, int n_x, int M,
+                                     const double* __restrict__ hxv, const double* __restrict__ huv,
+                                     const double* __restrict__ px, const double* __restrict__ pu,
+                                     const double* __restrict__ sigma_s,
+                                     const double* __restrict__ r2, const double* __restrict__ r4,
+                                     double* pz, double* ps) {
+  const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (id >= (long long)m * M) return;
+  const int s = int(id / m), i = int(id % m);
+  const double* hxs = hxv + size_t(s) * hx.nnz;
+  const double* hus = huv + size_t(s) * hu.nnz;
+  const double* pxs = px + size_t(s) * n_x;
+  double a = 0.0;
+  for (int t = hx.ptr[i]; t < hx.ptr[i + 1]; ++t) a += hxs[t] * pxs[hx.ind[t]];
+  double hp = 0.0 + 1.0 * a;
+  double b = 0.0;
+  for (int t = hu.ptr[i]; t < hu.ptr[i + 1]; ++t) b += hus[t] * pu[hu.ind[t]];
+  hp += 1.0 * b;
+  const double sg = sigma_s[id], rr2 = r2[id];
+  const double z = sg * (hp + r4[id]) - rr2;
+  pz[id] = z;
+  ps[id] = -(rr2 + z) / sg;
+}
+
+__global__ void condense_kernel(CondenseDev c, int M, const double* __restrict__ W, int ldw,
+                                const double* __restrict__ A, int lda,
+                                const double* __restrict__ B, int ldb,
+                                const double* __restrict__ sigma, int lds, double* out) {
+  const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (id >= (long long)c.nout * M) return;
+  const int s = int(id / c.nout), o = int(id % c.nout);
+  const double* Ws = W + size_t(s) * ldw;
+  const double* As = A + size_t(s) * lda;
+  const double* Bs = B + size_t(s) * ldb;
+  const double* Ss = sigma + size_t(s) * lds;
+  double v = 0.0;
+  if (c.w_of[o] >= 0) v = __dadd_rn(v, Ws[c.w_of[o]]);
+  for (int t = c.ptr[o]; t < c.ptr[o + 1]; ++t)
+    v = __dadd_rn(v, __dmul_rn(__dmul_rn(As[c.ka[t]], Ss[c.r[t]]), Bs[c.kb[t]]));
+  out[size_t(s) * c.nout + o] = v;
+}
+
+// ---------------------------------------------------------- dense Cholesky
+__global__ void __launch_bounds__(kDenseBlock) shift_cholesky_kernel(double* K, int n, int* info) {
+  __shared__ int fail;
+  double mx = 0.0;
+  for (long long i = threadIdx.x; i < (long long)n * n; i += kDenseBlock) mx = fmax(mx, fabs(K[i]));
+  mx = block_reduce<kDenseBlock>(mx, true);
+  const double shift = 1e-13 * fmax(1.0, mx);
+  for (int i = threadIdx.x; i < n; i += kDenseBlock) K[size_t(i) * n + i] += shift;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    double d = 0.0;
+    for (int k = threadIdx.x; k < j; k += kDenseBlock) {
+      const double l = K[size_t(k) * n + j];
+      d += l * l;
+    }
+    d = block_reduce<kDenseBlock>(d, false);
+    if (threadIdx.x == 0) {
+      const double ajj = K[size_t(j) * n + j] - d;
+      if (!(ajj > 0.0) || isnan(ajj)) {
+        fail = j + 1;
+      } else {
+        K[size_t(j) * n + j] = sqrt(ajj);
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ljj = K[size_t(j) * n + j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) {
+      double v = K[size_t(j) * n + i];
+      for (int k = 0; k < j; ++k) v -= K[size_t(k) * n + i] * K[size_t(k) * n + j];
+      K[size_t(j) * n + i] = v / ljj;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *info = fail;
+}
+
+__global__ void __launch_bounds__(kDenseBlock) cholesky_solve_kernel(const double* L, int n, double* b) {
+  __shared__ double xj;
+  // forward: L y = b (column-oriented)
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      xj = b[j] / L[size_t(j) * n + j];
+      b[j] = xj;
+    }
+    __syncthreads();
+    const double y = xj;
+    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) b[i] -= L[size_t(j) * n + i] * y;
+    __syncthreads();
+  }
+  // backward: L' x = y
+  for (int j = n - 1; j >= 0; --j) {
+    double d = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) d += L[size_t(j) * n + i] * b[i];
+    d = block_reduce<kDenseBlock>(d, false);
+    if (threadIdx.x == 0) b[j] = (b[j] - d) / L[size_t(j) * n + j];
+    __syncthreads();
+  }
+}
+
+void check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+size_t single_rhs_smem(int n_x) {
+  const size_t b = size_t(2) * n_x * sizeof(double);
+  return b <= 200 * 1024 ? b : 0;
+}
+
+}  // namespace
+
+void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
+                        int* status, double piv_tol, cudaStream_t st) {
+  if (M <= 0) return;
+  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, status, piv_tol);
+  check_launch("lu_refactor");
+}
+
+void plan_reduce_launch(ReduceLaunch& a, int smem_budget, int sm_count) {
+  // widest tile (<= 32 columns) whose accumulator and panel fit on chip
+  int kc = 32;
+  while (kc > 1 && size_t(a.n_x + a.n_u) * kc * sizeof(double) > size_t(smem_budget)) --kc;
+  a.panel_in_smem = size_t(a.n_x + a.n_u) * kc * sizeof(double) <= size_t(smem_budget);
+  if (!a.panel_in_smem) {
+    kc = 32;
+    while (kc > 1 && size_t(a.n_u) * kc * sizeof(double) > size_t(smem_budget)) --kc;
+  }
+  a.kc = std::min(kc, a.n_u);
+  const int tiles = (a.n_u + a.kc - 1) / a.kc;
+  const int per_sm = std::max(1, int(smem_budget / std::max<size_t>(1, reduce_smem_bytes(a))));
+  int nchunks = std::max(1, (4 * sm_count * std::min(per_sm, 4) + tiles - 1) / tiles);
+  nchunks = std::min(nchunks, a.M);
+  a.chunk = (a.M + nchunks - 1) / nchunks;
+  a.nchunks = (a.M + a.chunk - 1) / a.chunk;
+}
+
+size_t reduce_smem_bytes(const ReduceLaunch& a) {
+  return size_t(a.n_u + (a.panel_in_smem ? a.n_x : 0)) * a.kc * sizeof(double);
+}
+
+size_t reduce_scratch_doubles(const ReduceLaunch& a) {
+  const int tiles = (a.n_u + a.kc - 1) / a.kc;
+  return size_t(tiles) * a.nchunks * a.n_x * a.kc * (a.panel_in_smem ? 1 : 2);
+}
+
+void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  const int tiles = (a.n_u + a.kc - 1) / a.kc;
+  const size_t smem = reduce_smem_bytes(a);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(reduce_tiles_kernel<kSolveBlock>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  reduce_tiles_kernel<kSolveBlock><<<dim3(tiles, a.nchunks), kSolveBlock, smem, st>>>(a);
+  check_launch("reduce_tiles");
+}
+
+void launch_sum_parts(const double* parts, int nparts, long long len, double* out,
+                      const double* diag_add, double dw, int n_mat, const double* sub_vec,
+                      cudaStream_t st) {
+  if (len <= 0) return;
+  const int B = 256;
+  sum_parts_kernel<<<int((len + B - 1) / B), B, 0, st>>>(parts, nparts, len, out, diag_add, dw,
+                                                          n_mat, sub_vec);
+  check_launch("sum_parts");
+}
+
+void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  static double* scratch = nullptr;
+  static size_t scratch_n = 0;
+  const size_t smem = single_rhs_smem(a.n_x);
+  if (!smem) {
+    const size_t need = size_t(a.M) * 2 * a.n_x;
+    if (need > scratch_n) {
+      if (scratch) cudaFree(scratch);
+      cudaMalloc(&scratch, need * sizeof(double));
+      scratch_n = need;
+    }
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(reduce_rhs_kernel<kSolveBlock>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  reduce_rhs_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
+  check_launch("reduce_rhs");
+}
+
+void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  static double* scratch = nullptr;
+  static size_t scratch_n = 0;
+  const size_t smem = single_rhs_smem(a.n_x);
+  if (!smem) {
+    const size_t need = size_t(a.M) * 2 * a.n_x;
+    if (need > scratch_n) {
+      if (scratch) cudaFree(scratch);
+      cudaMalloc(&scratch, need * sizeof(double));
+      scratch_n = need;
+    }
+  }
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(recover_state_kernel<kSolveBlock>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  recover_state_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
+  check_launch("recover_state");
+}
+
+void launch_recover_slack(const DevCsr& hx, const DevCsr& hu, int m, int n_x, int M,
+                          const double* hx_v, const double* hu_v, const double* px,
+                          const double* pu, const double* sigma_s, const double* r2,
+                          const double* r4, double* pz, double* ps, cudaStream_t st) {
+  const long long n = (long long)m * M;
+  if (n <= 0) return;
+  recover_slack_kernel<<<int((n + 255) / 256), 256, 0, st>>>(hx, hu, m, n_x, M, hx_v, hu_v, px,
+                                                              pu, sigma_s, r2, r4, pz, ps);
+  check_launch("recover_slack");
+}
+
+void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, const double* A,
+                     int lda, const double* B, int ldb, const double* sigma, int lds, double* out,
+                     cudaStream_t st) {
+  const long long n = (long long)c.nout * M;
+  if (n <= 0) return;
+  condense_kernel<<<int((n + 255) / 256), 256, 0, st>>>(c, M, W, ldw, A, lda, B, ldb, sigma, lds,
+                                                         out);
+  check_launch("condense");
+}
+
+void launch_shift_cholesky(double* K, int n, int* info, double*, cudaStream_t st) {
+  shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
+  check_launch("shift_cholesky");
+}
+
+void launch_cholesky_solve(const double* L, int n, double* b, cudaStream_t st) {
+  cholesky_solve_kernel<<<1, kDenseBlock, 0, st>>>(L, n, b);
+  check_launch("cholesky_solve");
+}
+
+}  // namespace bipm

@@ -1,0 +1,88 @@
+"""Host side of the product (no GPU): the C-ABI library loads, exports every
+symbol include/bipm_gpu.h declares, and builds exactly the reference's
+problem (model maps, bounds, start point, derivative and condensed patterns)
+from the same case file, scenario count, sigma and seed."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, case_path
+from paper_2301_04869_b200 import _native as nat
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "bipm_gpu.h")).read()
+    return sorted(set(re.findall(r"\b(bipm_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = nat.lib()
+    declared = header_symbols()
+    assert declared, "no symbols parsed from the header"
+    for sym in declared:
+        assert hasattr(lib, sym), f"{sym} declared in bipm_gpu.h but not exported"
+    for sym in nat.SIGNATURES:
+        assert sym in declared, f"{sym} bound in _native.py but not declared in the header"
+
+
+@pytest.mark.parametrize("name", ["case9_N8_s005_it3", "case118_N4_s005_it5"])
+def test_problem_matches_reference_model(goldens, name):
+    fx = goldens[name]
+    m = fx.meta
+    p = nat.Problem(case_path(m["case"]), m["N"], m["sigma"], m["seed"])
+    N, n_x, n_u, mm, n_b = m["dims"]
+    assert (p.N, p.n_x, p.n_u, p.m, p.n_b) == (N, n_x, n_u, mm, n_b)
+    for L in ("L_f", "L_g", "L_h"):
+        assert np.array_equal(p.array(L + "_rowptr"), fx[L + "_rowptr"])
+        assert np.array_equal(p.array(L + "_colind"), fx[L + "_colind"])
+        assert np.array_equal(p.array(L + "_val"), fx[L + "_val"])  # bitwise
+    for v in ("x_lo", "x_up", "u_lo", "u_up", "s_lo", "s_up", "x_start", "u_start"):
+        assert np.array_equal(p.array(v), fx[v]), v
+    for pat in ("gx_p", "gu_p", "hx_p", "hu_p", "wxx_p", "wxu_p", "wuu_p", "hess_p", "kxx_p",
+                "kxu_p", "kuu_p"):
+        assert np.array_equal(p.array(pat + "_rowptr"), fx[pat + "_rowptr"]), pat
+        assert np.array_equal(p.array(pat + "_colind"), fx[pat + "_colind"]), pat
+
+
+def test_scenario_draws_match_reference_rng(goldens):
+    # N(1, 0.05^2) clamped draws from std::mt19937_64(seed) (scenarios.cpp:44-80):
+    # identical doubles reach L_g-independent per-scenario loads; check via
+    # the objective-free model data: loads are Pd/base * multiplier.
+    p = nat.Problem(case_path("case9"), 8, 0.05, 0)
+    mult = p.array("mult").reshape(8, p.nbus)
+    assert np.all(mult >= 0.5) and np.all(mult <= 1.5)
+    assert abs(mult.mean() - 1.0) < 0.05
+    p0 = nat.Problem(case_path("case9"), 8, 0.0, 0)
+    assert np.all(p0.array("mult") == 1.0)
+
+
+def test_lu_plan_is_a_valid_symmetric_factor_pattern():
+    p = nat.Problem(case_path("case118"), 2, 0.05, 0)
+    perm = p.array("lu_perm")
+    assert sorted(perm.tolist()) == list(range(p.n_x))
+    lp, lc = p.array("lu_l_ptr"), p.array("lu_l_col")
+    up, uc = p.array("lu_u_ptr"), p.array("lu_u_col")
+    # strict lower / strict upper, sorted, and U pattern = L pattern transposed
+    rows_l = np.repeat(np.arange(p.n_x), np.diff(lp))
+    rows_u = np.repeat(np.arange(p.n_x), np.diff(up))
+    assert np.all(lc < rows_l) and np.all(uc > rows_u)
+    assert sorted(zip(lc.tolist(), rows_l.tolist())) == sorted(zip(rows_u.tolist(), uc.tolist()))
+    # the symmetric minimum-degree ordering keeps fill well below COLAMD's
+    # (nnz L = 1,685 with COLAMD + partial pivoting)
+    assert len(lc) < 1685
+
+
+def test_bad_inputs_raise_reference_error_kinds(tmp_path):
+    with pytest.raises(nat.BipmError) as e:
+        nat.Problem(str(tmp_path / "missing.m"), 2)
+    assert e.value.code == 8  # ParseError
+    bad = tmp_path / "bad.m"
+    bad.write_text("function mpc = bad\nmpc.baseMVA = 100;\nmpc.bus = [1 3 0 0 0 0 1 1 0 1 1 1.1];\n")
+    with pytest.raises(nat.BipmError) as e:
+        nat.Problem(str(bad), 2)
+    assert e.value.code == 8
+    with pytest.raises(nat.BipmError) as e:
+        nat.Problem(case_path("case9"), 0)
+    assert e.value.code == 5
