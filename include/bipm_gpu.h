@@ -96,6 +96,32 @@ int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block);
 int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* khat,
                 double* rhs);
 
+/* Derivative bundle outputs (host, scenario-major over M; any may be NULL):
+ * DerivativeBundle (autodiff.hpp:117-127). */
+typedef struct {
+  double* f;        /* [M] */
+  double* g;        /* [M][n_x] */
+  double* h;        /* [M][m] */
+  double* gx;       /* [M][nnz G_x] */
+  double* gu;       /* [M][nnz G_u] */
+  double* hx;       /* [M][nnz H_x] */
+  double* hu;       /* [M][nnz H_u] */
+  double* wxx;      /* [M][nnz W_xx] */
+  double* wxu;      /* [M][nnz W_xu] */
+  double* wuu;      /* [M][nnz W_uu] */
+  double* grad_lag; /* [M][n_x + n_u] */
+} bipm_bundle;
+
+/* eval_bundle_range: X, y [M][n_x], u [n_u], z [M][m].  Returns
+ * BIPM_NONFINITE (with *bad_block the lowest scenario) when a basis value or
+ * derivative is not finite (autodiff.cpp:11-22). */
+int bipm_eval_bundle(bipm_ctx* c, const double* X, const double* u, const double* y,
+                     const double* z, double obj_weight, const bipm_bundle* out,
+                     int32_t* bad_block);
+/* batch_eval: values only (line-search trials). */
+int bipm_eval_values(bipm_ctx* c, const double* X, const double* u, double* f, double* g,
+                     double* h, int32_t* bad_block);
+
 #ifdef __cplusplus
 }
 #endif

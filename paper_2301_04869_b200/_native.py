@@ -64,7 +64,11 @@ SIGNATURES = {
     "bipm_ctx_destroy": (None, [_P]),
     "bipm_factor_gx": (ctypes.c_int, [_P, _D, _I]),
     "bipm_reduce": (ctypes.c_int, [_P, _P, ctypes.c_double, _D, _D]),
+    "bipm_eval_bundle": (ctypes.c_int, [_P, _D, _D, _D, _D, ctypes.c_double, _P, _I]),
+    "bipm_eval_values": (ctypes.c_int, [_P, _D, _D, _D, _D, _D, _I]),
 }
+
+BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
 
 
 def lib():
@@ -96,6 +100,10 @@ def dptr(a: np.ndarray):
 class _Condensed(ctypes.Structure):
     _fields_ = [(n, _D) for n in ("gu", "kxx", "kxu", "kuu", "sigma_x", "rhat1", "rhat3",
                                   "sigma_u", "rhat2")]
+
+
+class _Bundle(ctypes.Structure):
+    _fields_ = [(n, _D) for n in BUNDLE_FIELDS]
 
 
 class Problem:
@@ -152,6 +160,35 @@ class Context:
         rhs = np.zeros(n_u)
         check(lib().bipm_reduce(self._h, ctypes.byref(c), delta_w, dptr(khat), dptr(rhs)))
         return khat.reshape(n_u, n_u).T.copy(), rhs  # column-major -> numpy
+
+    def bundle_shapes(self):
+        p, M = self.problem, self.hi - self.lo
+        nnz = {k: len(p.array(k + "_p_colind")) for k in ("gx", "gu", "hx", "hu", "wxx", "wxu",
+                                                           "wuu")}
+        shapes = {"f": (M,), "g": (M, p.n_x), "h": (M, p.m), "grad_lag": (M, p.n_x + p.n_u)}
+        shapes.update({k: (M, v) for k, v in nnz.items()})
+        return shapes
+
+    def eval_bundle(self, X, u, y, z, obj_weight=1.0):
+        """eval_bundle_range (autodiff.cpp:484-516) through bipm_eval_bundle."""
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (X, u, y, z)]
+        out = {k: np.zeros(s) for k, s in self.bundle_shapes().items()}
+        b = _Bundle(**{k: dptr(v) for k, v in out.items()})
+        bad = ctypes.c_int32(-1)
+        check(lib().bipm_eval_bundle(self._h, *[dptr(a) for a in arrs], obj_weight,
+                                     ctypes.byref(b), ctypes.byref(bad)))
+        return out
+
+    def eval_values(self, X, u):
+        """batch_eval (autodiff.cpp:256-281) through bipm_eval_values."""
+        p, M = self.problem, self.hi - self.lo
+        X = np.ascontiguousarray(X, dtype=np.float64)
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        f, g, h = np.zeros(M), np.zeros((M, p.n_x)), np.zeros((M, p.m))
+        bad = ctypes.c_int32(-1)
+        check(lib().bipm_eval_values(self._h, dptr(X), dptr(u), dptr(f), dptr(g), dptr(h),
+                                     ctypes.byref(bad)))
+        return f, g, h
 
     def __del__(self):
         if getattr(self, "_h", None):

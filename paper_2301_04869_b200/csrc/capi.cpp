@@ -129,7 +129,7 @@ void bipm_ctx_destroy(bipm_ctx* c) { delete c; }
 int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block) {
   return guarded([&] {
     Engine& e = *c->eng;
-    e.gx.upload(gx, e.gx.size(), e.st);
+    e.bd().gx.upload(gx, e.bd().gx.size(), e.st);
     const idx bad = e.factor_gx();
     if (singular_block) *singular_block = bad;
     if (bad >= 0) throw Error(kSingularBlock, "singular block " + std::to_string(bad), bad);
@@ -140,7 +140,7 @@ int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* k
                 double* rhs) {
   return guarded([&] {
     Engine& e = *c->eng;
-    e.gu.upload(in->gu, e.gu.size(), e.st);
+    e.bd().gu.upload(in->gu, e.bd().gu.size(), e.st);
     e.kxx.upload(in->kxx, e.kxx.size(), e.st);
     e.kxu.upload(in->kxu, e.kxu.size(), e.st);
     e.kuu.upload(in->kuu, e.kuu.size(), e.st);
@@ -158,6 +158,59 @@ int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* k
     e.khat.download(khat, e.khat.size(), e.st);
     e.sync();
     for (size_t i = 0; i < r.size(); ++i) rhs[i] = r[i] - in->rhat2[i];
+  });
+}
+
+int bipm_eval_bundle(bipm_ctx* c, const double* X, const double* u, const double* y,
+                     const double* z, double obj_weight, const bipm_bundle* out,
+                     int32_t* bad_block) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    const OpfModel& M = e.pb.M;
+    const size_t Ms = size_t(e.M);
+    DArr<double> dX, du, dY, dZ;
+    dX.upload(X, Ms * M.n_x, e.st);
+    du.upload(u, size_t(M.n_u), e.st);
+    dY.upload(y, Ms * M.n_x, e.st);
+    dZ.upload(z, Ms * M.m, e.st);
+    Engine::Bundle& b = e.bd();
+    const idx badb = e.eval_bundle(b, dX.get(), du.get(), dY.get(), dZ.get(), obj_weight);
+    if (bad_block) *bad_block = badb;
+    auto dl = [&](const DArr<double>& a, double* dst) {
+      if (dst) a.download(dst, a.size(), e.st);
+    };
+    dl(b.f, out->f);
+    dl(b.g, out->g);
+    dl(b.h, out->h);
+    dl(b.gx, out->gx);
+    dl(b.gu, out->gu);
+    dl(b.hx, out->hx);
+    dl(b.hu, out->hu);
+    dl(b.wxx, out->wxx);
+    dl(b.wxu, out->wxu);
+    dl(b.wuu, out->wuu);
+    dl(b.grad, out->grad_lag);
+    e.sync();
+    if (badb >= 0) throw Error(kNonFinite, "non-finite basis output (block " + std::to_string(badb) + ")", badb);
+  });
+}
+
+int bipm_eval_values(bipm_ctx* c, const double* X, const double* u, double* f, double* g,
+                     double* h, int32_t* bad_block) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    const OpfModel& M = e.pb.M;
+    const size_t Ms = size_t(e.M);
+    DArr<double> dX, du, df(Ms), dg(Ms * M.n_x), dh(Ms * M.m);
+    dX.upload(X, Ms * M.n_x, e.st);
+    du.upload(u, size_t(M.n_u), e.st);
+    const idx badb = e.eval_values(dX.get(), du.get(), df.get(), dg.get(), dh.get());
+    if (bad_block) *bad_block = badb;
+    df.download(f, df.size(), e.st);
+    dg.download(g, dg.size(), e.st);
+    dh.download(h, dh.size(), e.st);
+    e.sync();
+    if (badb >= 0) throw Error(kNonFinite, "non-finite basis output (block " + std::to_string(badb) + ")", badb);
   });
 }
 

@@ -12,6 +12,7 @@ std::unique_ptr<Problem> Problem::from_parts(GridCase cs, ScenarioDraw sc) {
   p->deps = basis_deps(p->M);
   p->D = make_deriv_plan(p->M, p->deps);
   p->LU = make_lu_plan(p->D.g.x);
+  p->AD = make_ad_program(p->M, p->deps, p->D);
   return p;
 }
 
@@ -104,13 +105,20 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   lu.mul_u = up(L.mul_u);
 
   const size_t Ms = size_t(M);
-  gx.resize(Ms * nnz(D.g.x));
-  gu.resize(Ms * nnz(D.g.u));
-  hx.resize(Ms * nnz(D.h.x));
-  hu.resize(Ms * nnz(D.h.u));
-  wxx.resize(Ms * nnz(D.wxx));
-  wxu.resize(Ms * nnz(D.wxu));
-  wuu.resize(Ms * nnz(D.wuu));
+  for (Bundle& b : bundles) {
+    b.f.resize(Ms);
+    b.g.resize(Ms * size_t(Mo.n_x));
+    b.h.resize(Ms * size_t(Mo.m));
+    b.gx.resize(Ms * nnz(D.g.x));
+    b.gu.resize(Ms * nnz(D.g.u));
+    b.hx.resize(Ms * nnz(D.h.x));
+    b.hu.resize(Ms * nnz(D.h.u));
+    b.wxx.resize(Ms * nnz(D.wxx));
+    b.wxu.resize(Ms * nnz(D.wxu));
+    b.wuu.resize(Ms * nnz(D.wuu));
+    b.grad.resize(Ms * size_t(Mo.n_d()));
+  }
+  upload_ad();
   kxx.resize(Ms * nnz(D.kxx.out));
   kxu.resize(Ms * nnz(D.kxu.out));
   kuu.resize(Ms * nnz(D.kuu.out));
@@ -152,7 +160,7 @@ Engine::~Engine() {
 void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 
 idx Engine::factor_gx() {
-  launch_lu_refactor(lu, M, gx.get(), pb.D.g.x.nnz(), F.get(), lu_status.get(), 1e-12, st);
+  launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), lu_status.get(), 1e-12, st);
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
   sync();
@@ -164,17 +172,17 @@ idx Engine::factor_gx() {
 void Engine::condense_blocks() {
   const DerivPlan& D = pb.D;
   const int m = pb.M.m;
-  launch_condense(cxx.v, M, wxx.get(), D.wxx.nnz(), hx.get(), D.h.x.nnz(), hx.get(), D.h.x.nnz(),
+  launch_condense(cxx.v, M, bd().wxx.get(), D.wxx.nnz(), bd().hx.get(), D.h.x.nnz(), bd().hx.get(), D.h.x.nnz(),
                   sigma_s.get(), m, kxx.get(), st);
-  launch_condense(cxu.v, M, wxu.get(), D.wxu.nnz(), hx.get(), D.h.x.nnz(), hu.get(), D.h.u.nnz(),
+  launch_condense(cxu.v, M, bd().wxu.get(), D.wxu.nnz(), bd().hx.get(), D.h.x.nnz(), bd().hu.get(), D.h.u.nnz(),
                   sigma_s.get(), m, kxu.get(), st);
-  launch_condense(cuu.v, M, wuu.get(), D.wuu.nnz(), hu.get(), D.h.u.nnz(), hu.get(), D.h.u.nnz(),
+  launch_condense(cuu.v, M, bd().wuu.get(), D.wuu.nnz(), bd().hu.get(), D.h.u.nnz(), bd().hu.get(), D.h.u.nnz(),
                   sigma_s.get(), m, kuu.get(), st);
 }
 
 void Engine::reduce_local(double dw) {
   red.F = F.get();
-  red.gu_v = gu.get();
+  red.gu_v = bd().gu.get();
   red.kxx_v = kxx.get();
   red.kxu_v = kxu.get();
   red.kuu_v = kuu.get();
@@ -195,7 +203,7 @@ void Engine::reduce_rhs_local(double dw, double* d_out) {
   a.n_u = pb.M.n_u;
   a.M = M;
   a.F = F.get();
-  a.gu_v = gu.get();
+  a.gu_v = bd().gu.get();
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();
   a.sigma_x = sigma_x.get();
@@ -234,7 +242,7 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.n_u = pb.M.n_u;
   a.M = M;
   a.F = F.get();
-  a.gu_v = gu.get();
+  a.gu_v = bd().gu.get();
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();
   a.sigma_x = sigma_x.get();
@@ -245,8 +253,172 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.px = d_px;
   a.py = d_py;
   launch_recover_state(a, st);
-  launch_recover_slack(hx_p.v, hu_p.v, pb.M.m, pb.M.n_x, M, hx.get(), hu.get(), d_px, d_pu,
+  launch_recover_slack(hx_p.v, hu_p.v, pb.M.m, pb.M.n_x, M, bd().hx.get(), bd().hu.get(), d_px, d_pu,
                        sigma_s.get(), r2.get(), r4.get(), d_pz, d_ps, st);
+}
+
+}  // namespace bipm
+
+namespace bipm {
+
+namespace {
+
+template <typename T>
+const T* keep(std::vector<DArr<T>>& store, const std::vector<T>& v) {
+  store.emplace_back();
+  store.back().upload(v);
+  return store.back().get();
+}
+
+}  // namespace
+
+void Engine::upload_ad() {
+  const OpfModel& Mo = pb.M;
+  const AdProgram& P = pb.AD;
+  ad_i.reserve(64);
+  ad_d.reserve(32);
+  DevAd& A = ad;
+  A.M = M;
+  A.nbus = Mo.nbus;
+  A.nbr = Mo.nbr;
+  A.ngen = Mo.ngen;
+  A.n_x = Mo.n_x;
+  A.n_u = Mo.n_u;
+  A.m = Mo.m;
+  A.n_b = Mo.n_b();
+  A.n_d = Mo.n_d();
+  A.ref_bus = Mo.ref_bus;
+  A.slack_gen = Mo.slack_gen;
+  A.vv = Mo.lay.vv;
+  A.br = Mo.lay.br;
+  A.sq = Mo.lay.sq;
+  A.pd = Mo.lay.pd;
+  A.qd = Mo.lay.qd;
+  A.pg = Mo.lay.pg;
+  A.pg2 = Mo.lay.pg2;
+  A.vmag_in = keep(ad_i, Mo.vmag_in);
+  A.pgen_in = keep(ad_i, Mo.pgen_in);
+  std::vector<idx> th(2 * size_t(Mo.nbr)), vm(2 * size_t(Mo.nbr));
+  std::vector<double> brc(8 * size_t(Mo.nbr));
+  for (idx l = 0; l < Mo.nbr; ++l) {
+    const auto& c = Mo.br[size_t(l)];
+    th[2 * size_t(l)] = Mo.theta_in[size_t(c.from)];
+    th[2 * size_t(l) + 1] = Mo.theta_in[size_t(c.to)];
+    vm[2 * size_t(l)] = Mo.vmag_in[size_t(c.from)];
+    vm[2 * size_t(l) + 1] = Mo.vmag_in[size_t(c.to)];
+    const double v[8] = {c.gff, c.bff, c.gft, c.bft, c.gtf, c.btf, c.gtt, c.btt};
+    std::copy(v, v + 8, brc.begin() + 8 * long(l));
+  }
+  A.br_th = keep(ad_i, th);
+  A.br_v = keep(ad_i, vm);
+  A.brc = keep(ad_d, brc);
+  A.gs_ref = Mo.gs_ref;
+  A.br_ref = keep(ad_i, P.branch_ref);
+  A.gen_ref_other = keep(ad_i, P.gen_ref_other);
+  auto slice = [&](const std::vector<double>& all, idx width) {
+    return std::vector<double>(all.begin() + long(lo) * width, all.begin() + long(hi) * width);
+  };
+  pd_v.upload(slice(Mo.pd, Mo.nbus));
+  qd_v.upload(slice(Mo.qd, Mo.nbus));
+  status_v.upload(slice(Mo.status, Mo.nbr));
+  A.pd_v = pd_v.get();
+  A.qd_v = qd_v.get();
+  A.status = status_v.get();
+  A.Lf_ptr = keep(ad_i, Mo.L_f.ptr);
+  A.Lf_ind = keep(ad_i, Mo.L_f.ind);
+  A.Lf_val = keep(ad_d, Mo.L_f.val);
+  A.Lg_ptr = keep(ad_i, Mo.L_g.ptr);
+  A.Lg_ind = keep(ad_i, Mo.L_g.ind);
+  A.Lg_val = keep(ad_d, Mo.L_g.val);
+  A.Lh_ptr = keep(ad_i, Mo.L_h.ptr);
+  A.Lh_ind = keep(ad_i, Mo.L_h.ind);
+  A.Lh_val = keep(ad_d, Mo.L_h.val);
+  A.n_dp = P.n_dp;
+  A.n_c = P.n_c;
+  A.c_bus = P.c_bus;
+  A.c_gen = P.c_gen;
+  A.c_slack = P.c_slack;
+  A.nsd = idx(P.sd.size());
+  A.dp_off = keep(ad_i, P.dp_off);
+  A.sd = keep(ad_i, P.sd);
+  auto gat = [&](const Gather& G) {
+    DevGather d{};
+    d.n = G.outputs();
+    d.ptr = keep(ad_i, G.ptr);
+    d.src = keep(ad_i, G.src);
+    d.coef = G.coef.empty() ? nullptr : keep(ad_d, G.coef);
+    return d;
+  };
+  A.slack_val = gat(P.slack_val);
+  A.slack_grad = gat(P.slack_grad);
+  A.w = gat(P.w);
+  A.gx = gat(P.gx);
+  A.gu = gat(P.gu);
+  A.hx = gat(P.hx);
+  A.hu = gat(P.hu);
+  A.grad = gat(P.grad);
+  A.wxx = gat(P.wxx);
+  A.wxu = gat(P.wxu);
+  A.wuu = gat(P.wuu);
+  psi.resize(size_t(M) * size_t(A.n_b));
+  dpart.resize(size_t(M) * size_t(std::max(1, A.n_dp)));
+  wlane.resize(size_t(M) * size_t(A.n_b));
+  contrib.resize(size_t(M) * size_t(std::max(1, A.n_c)));
+  bad.resize(size_t(M));
+}
+
+idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const double* dY,
+                        const double* dZ, double obj_w) {
+  AdBuffers b{};
+  b.X = dX;
+  b.u = du;
+  b.Y = dY;
+  b.Z = dZ;
+  b.obj_w = obj_w;
+  b.psi = psi.get();
+  b.dp = dpart.get();
+  b.w = wlane.get();
+  b.c = contrib.get();
+  b.f = out.f.get();
+  b.g = out.g.get();
+  b.h = out.h.get();
+  b.gx = out.gx.get();
+  b.gu = out.gu.get();
+  b.hx = out.hx.get();
+  b.hu = out.hu.get();
+  b.wxx = out.wxx.get();
+  b.wxu = out.wxu.get();
+  b.wuu = out.wuu.get();
+  b.grad = out.grad.get();
+  b.bad = bad.get();
+  bad.zero(st);
+  launch_ad_bundle(ad, b, st);
+  return first_bad();
+}
+
+idx Engine::eval_values(const double* dX, const double* du, double* df, double* dg,
+                        double* dh) {
+  AdBuffers b{};
+  b.X = dX;
+  b.u = du;
+  b.psi = psi.get();
+  b.dp = dpart.get();
+  b.f = df;
+  b.g = dg;
+  b.h = dh;
+  b.bad = bad.get();
+  bad.zero(st);
+  launch_ad_values(ad, b, st);
+  return first_bad();
+}
+
+idx Engine::first_bad() {
+  std::vector<int> flags(static_cast<size_t>(M));
+  bad.download(flags.data(), flags.size(), st);
+  sync();
+  for (idx s = 0; s < M; ++s)
+    if (flags[size_t(s)]) return lo + s;
+  return -1;
 }
 
 }  // namespace bipm

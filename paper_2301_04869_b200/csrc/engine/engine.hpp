@@ -11,8 +11,10 @@
 #include <string>
 #include <vector>
 
+#include "../host/ad_plan.hpp"
 #include "../host/grid_model.hpp"
 #include "../host/plan.hpp"
+#include "../kernels/ad_launch.hpp"
 #include "../kernels/kkt_kernels.hpp"
 #include "device_array.hpp"
 
@@ -25,6 +27,7 @@ struct Problem {
   LaneDeps deps;
   DerivPlan D;
   LuPlan LU;
+  AdProgram AD;
   static std::unique_ptr<Problem> from_case_file(const std::string& path, idx N, double sigma,
                                                  std::uint64_t seed);
   static std::unique_ptr<Problem> from_parts(GridCase cs, ScenarioDraw sc);
@@ -60,8 +63,23 @@ class Engine {
   std::vector<DArr<int>> lu_arrays;
   DevLu lu{};
 
-  // ---- per-scenario resident values ([M][len])
-  DArr<double> gx, gu, hx, hu, wxx, wxu, wuu;  // bundle blocks
+  // ---- derivative bundles ([M][len]); the IPM keeps the iterate's and a
+  // trial point's and swaps them on acceptance (ipm.cpp:204-205, 545)
+  struct Bundle {
+    DArr<double> f, g, h, gx, gu, hx, hu, wxx, wxu, wuu, grad;
+  };
+  Bundle bundles[2];
+  int cur = 0;
+  Bundle& bd() { return bundles[cur]; }
+  Bundle& trial() { return bundles[1 - cur]; }
+  void swap_bundles() { cur = 1 - cur; }
+  // AD program + scratch
+  std::vector<DArr<int>> ad_i;
+  std::vector<DArr<double>> ad_d;
+  DevAd ad{};
+  DArr<double> psi, dpart, wlane, contrib;
+  DArr<int> bad;
+  DArr<double> pd_v, qd_v, status_v;
   DArr<double> kxx, kxu, kuu;                  // condensed blocks
   DArr<double> sigma_x, sigma_s, rhat1, rhat3, r2, r4;
   DArr<double> sigma_u, rhat2;                 // n_u (replicated)
@@ -74,6 +92,12 @@ class Engine {
   DArr<int> chol_info;
 
   // ---- operators (device-resident inputs/outputs)
+  // eval_bundle_range (autodiff.cpp:484-516) into `out`; returns the lowest
+  // global scenario index with a non-finite basis / derivative, or -1.
+  idx eval_bundle(Bundle& out, const double* dX, const double* du, const double* dY,
+                  const double* dZ, double obj_w);
+  // batch_eval (autodiff.cpp:256-281): f, g, h only
+  idx eval_values(const double* dX, const double* du, double* df, double* dg, double* dh);
   // factor_gx_range (kkt.cpp:190-196): returns the lowest singular global
   // scenario index or -1.
   idx factor_gx();
@@ -93,6 +117,8 @@ class Engine {
                double* d_ps);
 
   void sync();
+  void upload_ad();
+  idx first_bad();
   size_t nnz(const Csr& c) const { return size_t(c.nnz()); }
 };
 
