@@ -122,6 +122,43 @@ int bipm_eval_bundle(bipm_ctx* c, const double* X, const double* u, const double
 int bipm_eval_values(bipm_ctx* c, const double* X, const double* u, double* f, double* g,
                      double* h, int32_t* bad_block);
 
+/* ---- interior-point driver (ipm.cpp:435-664 on the reduced strategy) ---- */
+typedef struct bipm_solver bipm_solver;
+
+typedef struct { /* IpmOptions (ipm.hpp:7-25); zero fields take the default */
+  double tol;      /* 1e-6 */
+  double mu0;      /* 0.1 */
+  int32_t max_iter; /* 300 */
+} bipm_solve_options;
+
+#define BIPM_STATUS_RUNNING -1
+#define BIPM_STATUS_OPTIMAL 0
+#define BIPM_STATUS_MAX_ITER 1
+#define BIPM_STATUS_INFEASIBLE 2 /* step too small (no restoration, as the reference) */
+
+typedef struct {
+  int32_t status;     /* BIPM_STATUS_* */
+  int32_t iterations;
+  double objective;
+  double t_total, t_ad, t_kkt; /* seconds, host clock around device phases */
+  int64_t reductions;         /* K_hat assemblies (inertia attempts) */
+} bipm_solve_result;
+
+int bipm_solver_create(bipm_ctx* c, const bipm_solve_options* opts, bipm_solver** out);
+void bipm_solver_destroy(bipm_solver* s);
+/* initial_iterate (ipm.cpp:59-105) */
+int bipm_solver_start(bipm_solver* s);
+/* one IPM iteration; *status receives BIPM_STATUS_* */
+int bipm_solver_step(bipm_solver* s, int32_t* status);
+/* result so far; u (n_u, may be NULL) receives the current controls */
+int bipm_solver_result(bipm_solver* s, bipm_solve_result* r, double* u);
+/* IterationLog k: rec[15] = iter, objective, inf_pr, inf_du, complementarity,
+ * mu, alpha_primal, alpha_dual, t_ad, t_kkt, t_total, corrections,
+ * refinements, delta_w, full_step */
+int bipm_solver_log(bipm_solver* s, int32_t k, double rec[15]);
+/* whole solve: start + steps until a terminal status */
+int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,13 @@ SIGNATURES = {
     "bipm_reduce": (ctypes.c_int, [_P, _P, ctypes.c_double, _D, _D]),
     "bipm_eval_bundle": (ctypes.c_int, [_P, _D, _D, _D, _D, ctypes.c_double, _P, _I]),
     "bipm_eval_values": (ctypes.c_int, [_P, _D, _D, _D, _D, _D, _I]),
+    "bipm_solver_create": (ctypes.c_int, [_P, _P, ctypes.POINTER(_P)]),
+    "bipm_solver_destroy": (None, [_P]),
+    "bipm_solver_start": (ctypes.c_int, [_P]),
+    "bipm_solver_step": (ctypes.c_int, [_P, _I]),
+    "bipm_solver_result": (ctypes.c_int, [_P, _P, _D]),
+    "bipm_solver_log": (ctypes.c_int, [_P, ctypes.c_int32, _D]),
+    "bipm_solve": (ctypes.c_int, [_P, _P, _P, _D]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -104,6 +111,23 @@ class _Condensed(ctypes.Structure):
 
 class _Bundle(ctypes.Structure):
     _fields_ = [(n, _D) for n in BUNDLE_FIELDS]
+
+
+class _SolveOptions(ctypes.Structure):
+    _fields_ = [("tol", ctypes.c_double), ("mu0", ctypes.c_double), ("max_iter", ctypes.c_int32)]
+
+
+class _SolveResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32),
+                ("objective", ctypes.c_double), ("t_total", ctypes.c_double),
+                ("t_ad", ctypes.c_double), ("t_kkt", ctypes.c_double),
+                ("reductions", ctypes.c_int64)]
+
+
+SOLVE_STATUS = {-1: "Running", 0: "Optimal", 1: "MaxIter", 2: "Infeasible"}
+LOG_FIELDS = ("iter", "objective", "inf_pr", "inf_du", "complementarity", "mu", "alpha_p",
+              "alpha_d", "t_ad", "t_kkt", "t_total", "corr", "refinements", "delta_w",
+              "full_step")
 
 
 class Problem:
@@ -193,4 +217,50 @@ class Context:
     def __del__(self):
         if getattr(self, "_h", None):
             lib().bipm_ctx_destroy(self._h)
+            self._h = None
+
+
+class Solver:
+    """The GPU interior-point driver (ipm.cpp:435-664) through bipm_solver_*."""
+
+    def __init__(self, ctx: Context, tol: float = 1e-6, mu0: float = 0.1, max_iter: int = 300):
+        self.ctx = ctx
+        self._opts = _SolveOptions(tol, mu0, max_iter)
+        h = _P()
+        check(lib().bipm_solver_create(ctx._h, ctypes.byref(self._opts), ctypes.byref(h)))
+        self._h = h
+
+    def start(self):
+        check(lib().bipm_solver_start(self._h))
+
+    def step(self) -> int:
+        st = ctypes.c_int32(-1)
+        check(lib().bipm_solver_step(self._h, ctypes.byref(st)))
+        return st.value
+
+    def result(self):
+        r = _SolveResult()
+        u = np.zeros(self.ctx.problem.n_u)
+        check(lib().bipm_solver_result(self._h, ctypes.byref(r), dptr(u)))
+        out = {k: getattr(r, k) for k, _ in _SolveResult._fields_}
+        out["status_name"] = SOLVE_STATUS.get(r.status, str(r.status))
+        out["u"] = u
+        out["logs"] = [self.log(k) for k in range(r.iterations)]
+        return out
+
+    def log(self, k: int) -> dict:
+        rec = np.zeros(15)
+        check(lib().bipm_solver_log(self._h, k, dptr(rec)))
+        return dict(zip(LOG_FIELDS, rec.tolist()))
+
+    def solve(self):
+        self.start()
+        st = -1
+        while st == -1:
+            st = self.step()
+        return self.result()
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().bipm_solver_destroy(self._h)
             self._h = None

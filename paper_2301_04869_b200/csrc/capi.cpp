@@ -7,6 +7,7 @@
 #include <string>
 
 #include "engine/engine.hpp"
+#include "engine/solver.hpp"
 
 using namespace bipm;
 
@@ -18,6 +19,11 @@ struct bipm_problem {
 struct bipm_ctx {
   const bipm_problem* prob = nullptr;
   std::unique_ptr<Engine> eng;
+};
+
+struct bipm_solver {
+  bipm_ctx* ctx = nullptr;
+  std::unique_ptr<Solver> s;
 };
 
 namespace {
@@ -211,6 +217,80 @@ int bipm_eval_values(bipm_ctx* c, const double* X, const double* u, double* f, d
     dh.download(h, dh.size(), e.st);
     e.sync();
     if (badb >= 0) throw Error(kNonFinite, "non-finite basis output (block " + std::to_string(badb) + ")", badb);
+  });
+}
+
+namespace {
+SolverOptions to_options(const bipm_solve_options* o) {
+  SolverOptions so;
+  if (o) {
+    if (o->tol > 0) so.tol = o->tol;
+    if (o->mu0 > 0) so.mu0 = o->mu0;
+    if (o->max_iter > 0) so.max_iter = o->max_iter;
+  }
+  return so;
+}
+void fill_result(Solver& s, bipm_solve_result* r, double* u) {
+  if (r) {
+    r->status = s.status;
+    r->iterations = int32_t(s.logs.size());
+    r->objective = s.logs.empty() ? 0.0 : s.logs.back().objective;
+    r->t_total = s.t_total;
+    r->t_ad = s.t_ad;
+    r->t_kkt = s.t_kkt;
+    r->reductions = s.reductions;
+  }
+  if (u) {
+    const auto h = s.host_u();
+    std::copy(h.begin(), h.end(), u);
+  }
+}
+}  // namespace
+
+int bipm_solver_create(bipm_ctx* c, const bipm_solve_options* opts, bipm_solver** out) {
+  return guarded([&] {
+    auto sv = std::make_unique<bipm_solver>();
+    sv->ctx = c;
+    sv->s = std::make_unique<Solver>(*c->eng, to_options(opts));
+    *out = sv.release();
+  });
+}
+
+void bipm_solver_destroy(bipm_solver* s) { delete s; }
+
+int bipm_solver_start(bipm_solver* s) {
+  return guarded([&] { s->s->start(); });
+}
+
+int bipm_solver_step(bipm_solver* s, int32_t* status) {
+  return guarded([&] {
+    const int st = s->s->step();
+    if (status) *status = st;
+  });
+}
+
+int bipm_solver_result(bipm_solver* s, bipm_solve_result* r, double* u) {
+  return guarded([&] { fill_result(*s->s, r, u); });
+}
+
+int bipm_solver_log(bipm_solver* s, int32_t k, double rec[15]) {
+  return guarded([&] {
+    const auto& L = s->s->logs;
+    if (k < 0 || size_t(k) >= L.size()) throw Error(kInvalidArgument, "log index out of range");
+    const IterRecord& l = L[size_t(k)];
+    const double v[15] = {double(l.iter), l.objective,    l.inf_pr,         l.inf_du,
+                          l.complementarity, l.mu,         l.alpha_primal,   l.alpha_dual,
+                          l.t_ad,            l.t_kkt,      l.t_total,        double(l.corrections),
+                          double(l.refinements), l.delta_w, l.full_step ? 1.0 : 0.0};
+    std::copy(v, v + 15, rec);
+  });
+}
+
+int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u) {
+  return guarded([&] {
+    Solver s(*c->eng, to_options(opts));
+    s.solve();
+    fill_result(s, r, u);
   });
 }
 

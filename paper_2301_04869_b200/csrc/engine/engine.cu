@@ -61,6 +61,9 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   kxx_p.upload(D.kxx.out);
   kxu_p.upload(D.kxu.out);
   kuu_p.upload(D.kuu.out);
+  wxx_p.upload(D.wxx);
+  wxu_p.upload(D.wxu);
+  wuu_p.upload(D.wuu);
   cxx.upload(D.kxx);
   cxu.upload(D.kxu);
   cuu.upload(D.kuu);
@@ -193,7 +196,8 @@ void Engine::reduce_local(double dw) {
   launch_reduce_tiles(red, st);
 }
 
-void Engine::reduce_rhs_local(double dw, double* d_out) {
+void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
+                              const double* d_rhat3) {
   RhsLaunch a{};
   a.lu = lu;
   a.gu = gu_p.v;
@@ -207,8 +211,8 @@ void Engine::reduce_rhs_local(double dw, double* d_out) {
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();
   a.sigma_x = sigma_x.get();
-  a.rhat1 = rhat1.get();
-  a.rhat3 = rhat3.get();
+  a.rhat1 = d_rhat1 ? d_rhat1 : rhat1.get();
+  a.rhat3 = d_rhat3 ? d_rhat3 : rhat3.get();
   a.dw = dw;
   a.part = rhs_part.get();
   launch_reduce_rhs(a, st);
@@ -232,7 +236,8 @@ bool Engine::factor_khat() {
 void Engine::solve_khat(double* d_vec) { launch_cholesky_solve(khat.get(), pb.M.n_u, d_vec, st); }
 
 void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, double* d_pz,
-                     double* d_ps) {
+                     double* d_ps, const double* d_rhat1, const double* d_rhat3,
+                     const double* d_r2, const double* d_r4) {
   RecoverLaunch a{};
   a.lu = lu;
   a.gu = gu_p.v;
@@ -246,15 +251,15 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();
   a.sigma_x = sigma_x.get();
-  a.rhat1 = rhat1.get();
-  a.rhat3 = rhat3.get();
+  a.rhat1 = d_rhat1 ? d_rhat1 : rhat1.get();
+  a.rhat3 = d_rhat3 ? d_rhat3 : rhat3.get();
   a.pu = d_pu;
   a.dw = dw;
   a.px = d_px;
   a.py = d_py;
   launch_recover_state(a, st);
   launch_recover_slack(hx_p.v, hu_p.v, pb.M.m, pb.M.n_x, M, bd().hx.get(), bd().hu.get(), d_px, d_pu,
-                       sigma_s.get(), r2.get(), r4.get(), d_pz, d_ps, st);
+                       sigma_s.get(), d_r2 ? d_r2 : r2.get(), d_r4 ? d_r4 : r4.get(), d_pz, d_ps, st);
 }
 
 }  // namespace bipm

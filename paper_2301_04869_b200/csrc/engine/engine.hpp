@@ -58,7 +58,7 @@ class Engine {
   cudaStream_t st = nullptr;
 
   // ---- uploaded plans
-  DevPattern gx_p, gu_p, hx_p, hu_p, kxx_p, kxu_p, kuu_p;
+  DevPattern gx_p, gu_p, hx_p, hu_p, kxx_p, kxu_p, kuu_p, wxx_p, wxu_p, wuu_p;
   DevCondense cxx, cxu, cuu;
   std::vector<DArr<int>> lu_arrays;
   DevLu lu{};
@@ -106,7 +106,9 @@ class Engine {
   // local part of reduce (kkt.cpp:371-466): khat/rhs partial sums over the
   // owned scenarios, without the sigma_u / rhat2 terms.
   void reduce_local(double delta_w);
-  void reduce_rhs_local(double delta_w, double* d_rhs_out);
+  // rhs of the reduced system from (rhat1, rhat3) (defaults: the engine's)
+  void reduce_rhs_local(double delta_w, double* d_rhs_out, const double* d_rhat1 = nullptr,
+                        const double* d_rhat3 = nullptr);
   // finish_reduce (kkt.cpp:468-488) for a single engine
   void finish_reduce(double delta_w);
   // shift + Cholesky (kkt.cpp:965-971); true when positive definite
@@ -114,7 +116,8 @@ class Engine {
   void solve_khat(double* d_vec);
   // recover_state_adjoint + recover_slack_dual (kkt.cpp:507-532, :172-188)
   void recover(double delta_w, const double* d_pu, double* d_px, double* d_py, double* d_pz,
-               double* d_ps);
+               double* d_ps, const double* d_rhat1 = nullptr, const double* d_rhat3 = nullptr,
+               const double* d_r2 = nullptr, const double* d_r4 = nullptr);
 
   void sync();
   void upload_ad();

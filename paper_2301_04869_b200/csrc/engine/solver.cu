@@ -1,0 +1,428 @@
+#include "solver.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace bipm {
+
+namespace {
+
+double project_start(double start, double lo, double up) {  // ipm.cpp:28-36
+  if (std::isfinite(lo) && std::isfinite(up)) {
+    const double span = up - lo;
+    return std::max(lo + 0.1 * span, std::min(up - 0.1 * span, start));
+  }
+  if (std::isfinite(lo)) return std::max(start, lo + 0.1 * std::max(1.0, std::abs(lo)));
+  if (std::isfinite(up)) return std::min(start, up - 0.1 * std::max(1.0, std::abs(up)));
+  return start;
+}
+
+double update_mu(double mu, const SolverOptions& o) {  // ipm.cpp:21-24
+  return std::max(o.tol / 10.0, std::min(o.kappa_mu * mu, std::pow(mu, o.theta_mu)));
+}
+
+}  // namespace
+
+DevIter Solver::IterStore::view() {
+  return DevIter{x.get(),   u.get(),   s.get(),   y.get(),   z.get(),  klo.get(),
+                 kup.get(), nlo.get(), nup.get(), llo.get(), lup.get()};
+}
+
+Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
+  const OpfModel& M = e.pb.M;
+  d = IpmDims{e.M, M.n_x, M.n_u, M.m, M.n_d()};
+  xlo.upload(M.x_lo);
+  xup.upload(M.x_up);
+  ulo.upload(M.u_lo);
+  uup.upload(M.u_up);
+  slo.upload(M.s_lo);
+  sup.upload(M.s_up);
+  b = DevBounds{xlo.get(), xup.get(), ulo.get(), uup.get(), slo.get(), sup.get()};
+  const size_t nx = size_t(d.M) * d.n_x, nm = size_t(d.M) * d.m, nu = size_t(d.n_u);
+  for (IterStore& s : its) {
+    for (DArr<double>* a : {&s.x, &s.y, &s.klo, &s.kup}) a->resize(nx);
+    for (DArr<double>* a : {&s.s, &s.z, &s.nlo, &s.nup}) a->resize(nm);
+    for (DArr<double>* a : {&s.u, &s.llo, &s.lup}) a->resize(nu);
+  }
+  for (DArr<double>* s : {p, q}) {
+    s[0].resize(nx);
+    s[1].resize(nu);
+    s[2].resize(nm);
+    s[3].resize(nm);
+    s[4].resize(nx);
+  }
+  bsv[0].resize(nx);
+  bsv[1].resize(nx);
+  bsv[2].resize(nm);
+  bsv[3].resize(nm);
+  bsv[4].resize(nu);
+  bsv[5].resize(nu);
+  r1x.resize(nx);
+  r1u.resize(nu);
+  gsum_u.resize(nu);
+  rhat2_part.resize(size_t(d.M) * nu);
+  o1x.resize(nx);
+  o1u.resize(nu);
+  o2.resize(nm);
+  o3.resize(nx);
+  o4.resize(nm);
+  o1u_part.resize(size_t(d.M) * nu * 2);
+  c_rhat1.resize(nx);
+  c_rhat2.resize(nu);
+  rhs_sum.resize(nu);
+  pu_rhs.resize(nu);
+  ft.resize(size_t(d.M));
+  gt.resize(nx);
+  ht.resize(nm);
+  partial.resize(600 * 8);
+  scal.resize(32);
+  flag.resize(1);
+  cuda_check(cudaMallocHost(&pinned, 64 * sizeof(double)), "cudaMallocHost");
+  // multiplier count of the scaled error (ipm.cpp:345-379): structural
+  double fin_x = 0, fin_s = 0, fin_u = 0;
+  for (idx i = 0; i < M.n_x; ++i) fin_x += std::isfinite(M.x_lo[size_t(i)]) + std::isfinite(M.x_up[size_t(i)]);
+  for (idx i = 0; i < M.m; ++i) fin_s += std::isfinite(M.s_lo[size_t(i)]) + std::isfinite(M.s_up[size_t(i)]);
+  for (idx i = 0; i < M.n_u; ++i) fin_u += std::isfinite(M.u_lo[size_t(i)]) + std::isfinite(M.u_up[size_t(i)]);
+  const double N = M.N;
+  mult_count = N * (M.n_x + fin_x) + N * (M.m + fin_s) + fin_u;
+}
+
+double Solver::now() const {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+template <int K>
+std::array<double, K> Solver::fetch(const double* dptr) {
+  cuda_check(cudaMemcpyAsync(pinned, dptr, K * sizeof(double), cudaMemcpyDeviceToHost, e.st),
+             "fetch");
+  e.sync();
+  std::array<double, K> r;
+  std::copy(pinned, pinned + K, r.begin());
+  return r;
+}
+
+double Solver::fetch1(const double* dptr) { return fetch<1>(dptr)[0]; }
+
+DevStep Solver::step_view(DArr<double>* s) {
+  return DevStep{s[0].get(), s[1].get(), s[2].get(), s[3].get(), s[4].get()};
+}
+
+Solver::Scaled Solver::scaled_error(const DevIter& it, Engine::Bundle& bd, double mu_) {
+  double* sc = scal.get();
+  launch_kkt_error_xs(d, it, b, bd.grad.get(), bd.g.get(), bd.h.get(), mu_, partial.get(), sc,
+                      e.st);
+  launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
+  launch_kkt_error_u(d, it, b, gsum_u.get(), mu_, sc + 8, e.st);
+  launch_scenario_sum(d.M, 1, bd.f.get(), nullptr, sc + 11, e.st);
+  const auto v = fetch<12>(sc);
+  objective = v[11];
+  const double stat = std::max({v[0], v[1], v[8]});
+  const double primal = std::max(v[2], v[3]);
+  const double comp = std::max(v[4], v[9]);
+  const double avg = mult_count > 0 ? (v[5] + v[10]) / mult_count : 0.0;
+  const double s_d = std::max(100.0, avg) / 100.0;
+  Scaled r;
+  r.stationarity = stat / s_d;
+  r.primal = primal;
+  r.comp = comp / s_d;
+  r.comp_raw = comp;
+  r.total = std::max({r.stationarity, r.primal, r.comp});
+  return r;
+}
+
+void Solver::start() {
+  const OpfModel& M = e.pb.M;
+  std::vector<double> x0(size_t(M.n_x)), u0(size_t(M.n_u)), llo(size_t(M.n_u)), lup(size_t(M.n_u));
+  for (idx i = 0; i < M.n_x; ++i)
+    x0[size_t(i)] = project_start(M.x_start.empty() ? 0.0 : M.x_start[size_t(i)],
+                                  M.x_lo[size_t(i)], M.x_up[size_t(i)]);
+  for (idx i = 0; i < M.n_u; ++i) {
+    const double lo = M.u_lo[size_t(i)], up = M.u_up[size_t(i)];
+    const double u = project_start(M.u_start.empty() ? 0.0 : M.u_start[size_t(i)], lo, up);
+    u0[size_t(i)] = u;
+    llo[size_t(i)] = std::isfinite(lo) ? o.mu0 / (u - lo) : 0.0;
+    lup[size_t(i)] = std::isfinite(up) ? o.mu0 / (up - u) : 0.0;
+  }
+  icur = 0;
+  IterStore& s = its[0];
+  DArr<double> dx0;
+  dx0.upload(x0);
+  s.u.upload(u0);
+  s.llo.upload(llo);
+  s.lup.upload(lup);
+  launch_init_x(d, cur(), b, dx0.get(), o.mu0, e.st);
+  if (d.m > 0) {
+    const idx bad = e.eval_values(s.x.get(), s.u.get(), ft.get(), gt.get(), ht.get());
+    if (bad >= 0) throw Error(kNonFinite, "non-finite basis output at the start point", bad);
+    launch_init_slacks(d, cur(), b, ht.get(), o.mu0, e.st);
+  }
+  e.sync();
+  mu = o.mu0;
+  delta_w_last = 0;
+  iter = 0;
+  bundle_fresh = false;
+  status = kRunning;
+  logs.clear();
+  t_ad = t_kkt = 0;
+  t0_ = std::chrono::steady_clock::now();
+}
+
+bool Solver::attempt(double dw, const DevIter& it) {
+  (void)it;
+  Engine::Bundle& bd = e.bd();
+  ++reductions;
+  e.reduce_local(dw);
+  e.finish_reduce(dw);
+  e.reduce_rhs_local(dw, rhs_sum.get());
+  if (!e.factor_khat()) return false;
+  // solve_with(c, first_sum): p_u, then state/adjoint and slack/dual recovery
+  launch_pu_rhs(d.n_u, rhs_sum.get(), e.rhat2.get(), p[1].get(), true, e.st);
+  e.solve_khat(p[1].get());
+  e.recover(dw, p[1].get(), p[0].get(), p[4].get(), p[3].get(), p[2].get());
+  // refinement against the unreduced augmented system (kkt.cpp:988-999)
+  launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
+                   scal.get() + 20, e.st);
+  const double scale = fetch1(scal.get() + 20);
+  const DerivPlan& D = e.pb.D;
+  (void)D;
+  for (int round = 0; round < o.refine_rounds; ++round) {
+    AugResidualArgs a{};
+    a.d = d;
+    a.gx = e.gx_p.v;
+    a.gu = e.gu_p.v;
+    a.hx = e.hx_p.v;
+    a.hu = e.hu_p.v;
+    a.wxx = e.wxx_p.v;
+    a.wxu = e.wxu_p.v;
+    a.wuu = e.wuu_p.v;
+    a.gx_v = bd.gx.get();
+    a.gu_v = bd.gu.get();
+    a.hx_v = bd.hx.get();
+    a.hu_v = bd.hu.get();
+    a.wxx_v = bd.wxx.get();
+    a.wxu_v = bd.wxu.get();
+    a.wuu_v = bd.wuu.get();
+    a.sigma_x = e.sigma_x.get();
+    a.sigma_s = e.sigma_s.get();
+    a.sigma_u = e.sigma_u.get();
+    a.r1x = r1x.get();
+    a.r1u = r1u.get();
+    a.r2 = e.r2.get();
+    a.r3 = bd.g.get();
+    a.r4 = e.r4.get();
+    a.p = step_view(p);
+    a.dw = dw;
+    a.o1x = o1x.get();
+    a.o2 = o2.get();
+    a.o3 = o3.get();
+    a.o4 = o4.get();
+    a.o1u_part = o1u_part.get();
+    launch_aug_residual(a, partial.get(), scal.get() + 21, e.st);
+    launch_aug_residual_u(a, o1u.get(), scal.get() + 22, e.st);
+    const auto v = fetch<2>(scal.get() + 21);
+    const double rel = std::max(v[0], v[1]) / scale;
+    if (rel <= 1e-12) break;
+    ++refinements;
+    // substitute_rhs (kkt.cpp:342-358): re-condense only the rhs from rho
+    launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
+                         o4.get(), o2.get(), o1x.get(), c_rhat1.get(), rhat2_part.get(), e.st);
+    launch_scenario_sum(d.M, d.n_u, rhat2_part.get(), o1u.get(), c_rhat2.get(), e.st);
+    e.reduce_rhs_local(dw, rhs_sum.get(), c_rhat1.get(), o3.get());
+    launch_pu_rhs(d.n_u, rhs_sum.get(), c_rhat2.get(), q[1].get(), false, e.st);
+    e.solve_khat(q[1].get());
+    e.recover(dw, q[1].get(), q[0].get(), q[4].get(), q[3].get(), q[2].get(), c_rhat1.get(),
+              o3.get(), o2.get(), o4.get());
+    launch_axpy_step(d, step_view(p), step_view(q), e.st);
+  }
+  return true;
+}
+
+void Solver::compute_step(const DevIter& it) {
+  Engine::Bundle& bd = e.bd();
+  flag.zero(e.st);
+  launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
+  launch_assemble_xs(d, it, b, bd.grad.get(), bd.h.get(), mu, e.sigma_x.get(), r1x.get(),
+                     e.sigma_s.get(), e.r2.get(), e.r4.get(), flag.get(), e.st);
+  launch_assemble_u(d, it, b, gsum_u.get(), mu, e.sigma_u.get(), r1u.get(), flag.get(), e.st);
+  cuda_check(cudaMemcpyAsync(e.rhat3.get(), bd.g.get(), e.rhat3.size() * sizeof(double),
+                             cudaMemcpyDeviceToDevice, e.st),
+             "rhat3");
+  e.condense_blocks();
+  launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
+                       e.r4.get(), e.r2.get(), r1x.get(), e.rhat1.get(), rhat2_part.get(), e.st);
+  launch_scenario_sum(d.M, d.n_u, rhat2_part.get(), r1u.get(), e.rhat2.get(), e.st);
+  int fl = 0;
+  flag.download(&fl, 1, e.st);
+  e.sync();
+  if (fl) throw Error(kNonInterior, "iterate not strictly interior");
+  const idx sing = e.factor_gx();
+  if (sing >= 0)
+    throw Error(kSingularBlock,
+                "singular block " + std::to_string(sing) +
+                    " (the reference falls back to the augmented strategy, which is not on the "
+                    "GPU path)",
+                sing);
+  corrections = 0;
+  refinements = 0;
+  double dw = 0.0;
+  if (!attempt(0.0, it)) {
+    dw = delta_w_last == 0 ? o.reg.delta_w0
+                           : std::max(o.reg.delta_w_min, delta_w_last * o.reg.kappa_minus);
+    for (;;) {
+      ++corrections;
+      if (attempt(dw, it)) {
+        delta_w_last = dw;
+        break;
+      }
+      dw *= delta_w_last == 0 ? o.reg.kappa_plus_emergency : o.reg.kappa_plus;
+      if (dw > o.reg.delta_w_max)
+        throw Error(kLinearSolve, "inertia correction: regularization budget exhausted");
+    }
+  }
+  last_dw = dw;
+}
+
+int Solver::step() {
+  if (status != kRunning) return status;
+  IterRecord log;
+  log.iter = iter;
+  const double t_iter = now();
+  DevIter it = cur();
+  if (!bundle_fresh) {
+    const double ta = now();
+    const idx bad = e.eval_bundle(e.bd(), it.x, it.u, it.y, it.z, 1.0);
+    if (bad >= 0) throw Error(kNonFinite, "non-finite basis output", bad);
+    log.t_ad += now() - ta;
+  }
+  bundle_fresh = false;
+  const Scaled e0 = scaled_error(it, e.bd(), 0.0);
+  log.objective = objective;
+  log.inf_pr = e0.primal;
+  log.inf_du = e0.stationarity;
+  log.complementarity = e0.comp_raw;
+  auto finish = [&](int st_code) {
+    log.t_total = now() - t_iter;
+    t_ad += log.t_ad;
+    t_kkt += log.t_kkt;
+    logs.push_back(log);
+    t_total = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+    if (st_code == kRunning && iter == o.max_iter - 1) st_code = kMaxIter;
+    ++iter;
+    status = st_code;
+    return status;
+  };
+  if (e0.total <= o.tol) {
+    log.mu = mu;
+    return finish(kOptimal);
+  }
+  for (;;) {
+    const Scaled emu = scaled_error(it, e.bd(), mu);
+    if (emu.total <= o.kappa_eps * mu && mu > o.tol / 10.0) {
+      mu = update_mu(mu, o);
+      continue;
+    }
+    break;
+  }
+  log.mu = mu;
+  const double tk = now();
+  compute_step(it);
+  log.t_kkt = now() - tk;
+  log.corrections = corrections;
+  log.refinements = refinements;
+  log.delta_w = last_dw;
+
+  DevBoundStep bs{bsv[0].get(), bsv[1].get(), bsv[2].get(), bsv[3].get(), bsv[4].get(), bsv[5].get()};
+  const DevStep ps = step_view(p);
+  launch_bound_steps(d, it, b, ps, mu, o.tau, bs, partial.get(), scal.get(), e.st);
+  const auto caps = fetch<2>(scal.get());
+  const double ap = std::min(1.0, caps[0]), ad = std::min(1.0, caps[1]);
+
+  // full-step primal-dual acceptance (ipm.cpp:518-563)
+  {
+    const double theta0 = scaled_error(it, e.bd(), mu).total;
+    const double obj_it = objective;
+    DevIter tr = alt();
+    launch_apply_step(d, it, tr, b, ps, bs, ap, ad, mu, e.st);
+    const double ta = now();
+    const idx bad = e.eval_bundle(e.trial(), tr.x, tr.u, tr.y, tr.z, 1.0);
+    double theta1 = kInf;
+    const bool ok = bad < 0;
+    if (ok) theta1 = scaled_error(tr, e.trial(), mu).total;
+    objective = obj_it;
+    log.t_ad += now() - ta;
+    if (ok && theta1 <= 0.99 * theta0) {
+      icur = 1 - icur;
+      e.swap_bundles();
+      bundle_fresh = true;
+      log.alpha_primal = ap;
+      log.alpha_dual = ad;
+      log.full_step = true;
+      return finish(kRunning);
+    }
+  }
+
+  // l1-merit Armijo backtracking (ipm.cpp:566-627)
+  Engine::Bundle& bd = e.bd();
+  launch_merit(d, it, b, ps, bd.grad.get(), bd.f.get(), bd.g.get(), bd.h.get(), e.gx_p.v,
+               e.gu_p.v, e.hx_p.v, e.hu_p.v, bd.gx.get(), bd.gu.get(), bd.hx.get(), bd.hu.get(),
+               mu, partial.get(), scal.get(), e.st);
+  launch_merit_u(d, it, b, p[1].get(), mu, scal.get() + 8, e.st);
+  const auto mv = fetch<10>(scal.get());
+  const double viol0 = mv[0];
+  const double penalty = 1.2 * std::max(mv[1], mv[2]) + 0.1;
+  const double bar0 = mu * (mv[3] + mv[8]);
+  const double phi0 = mv[6] + bar0 + penalty * viol0;
+  const double dird = mv[5] + (mv[4] + mv[9]) - penalty * viol0;
+  const double phi_scale = 1.0 + std::abs(bar0) + penalty * viol0 + mv[7];
+  const double relax = 1e-13 * phi_scale;
+  const double c1 = 1e-4;
+  double alpha = ap;
+  bool accepted = false;
+  DevIter tr = alt();
+  for (int ls = 0; ls < 60; ++ls) {
+    launch_primal_trial(d, it, tr, ps, alpha, e.st);
+    const double ta = now();
+    const idx bad = e.eval_values(tr.x, tr.u, ft.get(), gt.get(), ht.get());
+    if (bad < 0) {
+      launch_ls_values(d, tr, b, ft.get(), gt.get(), ht.get(), partial.get(), scal.get() + 12,
+                       e.st);
+      launch_merit_u(d, tr, b, nullptr, mu, scal.get() + 15, e.st);
+      const auto w = fetch<5>(scal.get() + 12);
+      log.t_ad += now() - ta;
+      const double phi = w[0] + mu * (w[1] + w[3]) + penalty * w[2];
+      if (phi <= phi0 + c1 * alpha * std::min(dird, 0.0) + relax) {
+        accepted = true;
+        break;
+      }
+    } else {
+      log.t_ad += now() - ta;
+    }
+    alpha *= 0.5;
+    if (alpha < 1e-12) break;
+  }
+  if (!accepted) {
+    message = "step too small (restoration not implemented, as in the reference)";
+    return finish(kInfeasible);
+  }
+  launch_apply_step(d, it, tr, b, ps, bs, alpha, ad, mu, e.st);
+  icur = 1 - icur;
+  log.alpha_primal = alpha;
+  log.alpha_dual = ad;
+  return finish(kRunning);
+}
+
+int Solver::solve() {
+  start();
+  while (status == kRunning) step();
+  return status;
+}
+
+std::vector<double> Solver::host_u() const {
+  return const_cast<Solver*>(this)->its[icur].u.to_host();
+}
+
+std::vector<double> Solver::host_x() const {
+  return const_cast<Solver*>(this)->its[icur].x.to_host();
+}
+
+}  // namespace bipm

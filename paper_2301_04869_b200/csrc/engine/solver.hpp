@@ -1,0 +1,107 @@
+// Device-resident interior-point solver on the reduced KKT path.
+//
+// Control flow restates the reference driver (proj/core/src/ipm.cpp:435-664)
+// and the reduced strategy (kkt.cpp:742-772 inertia loop, kkt.cpp:945-1006
+// solve_reduced with up to three refinement rounds).  Every N-sized vector
+// lives in HBM; the host only sees the scalars that steer control flow
+// (norms, step sizes, merit values, factorisation status).
+#pragma once
+
+#include <array>
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "../kernels/ipm_kernels.hpp"
+#include "engine.hpp"
+
+namespace bipm {
+
+struct RegOptions {  // RegSchedule (kkt.hpp:20-29)
+  double delta_w0 = 1e-4, delta_w_min = 1e-20, delta_w_max = 1e40;
+  double kappa_minus = 1.0 / 3.0, kappa_plus = 8.0, kappa_plus_emergency = 100.0;
+};
+
+struct SolverOptions {  // IpmOptions (ipm.hpp:7-25)
+  double tol = 1e-6, mu0 = 1e-1, kappa_mu = 0.2, theta_mu = 1.5, tau = 0.995, kappa_eps = 10.0;
+  int max_iter = 300;
+  RegOptions reg;
+  int refine_rounds = 3;
+};
+
+struct IterRecord {  // IterationLog (ipm.hpp:27-36)
+  int iter = 0;
+  double objective = 0, inf_pr = 0, inf_du = 0, complementarity = 0, mu = 0;
+  double alpha_primal = 0, alpha_dual = 0;
+  double t_ad = 0, t_kkt = 0, t_total = 0;
+  int corrections = 0, refinements = 0;
+  double delta_w = 0;
+  bool full_step = false;
+};
+
+enum SolveStatusCode : int { kRunning = -1, kOptimal = 0, kMaxIter = 1, kInfeasible = 2, kLinFail = 3 };
+
+class Solver {
+ public:
+  Solver(Engine& e, const SolverOptions& o);
+
+  void start();      // initial_iterate (ipm.cpp:59-105)
+  int step();        // one IPM iteration; returns a SolveStatusCode
+  int solve();       // start + steps until done
+
+  int status = kRunning;
+  int iter = 0;
+  double mu = 0, delta_w_last = 0, objective = 0;
+  std::vector<IterRecord> logs;
+  double t_ad = 0, t_kkt = 0, t_total = 0;
+  long long reductions = 0;  // K_hat assemblies (every inertia attempt)
+  std::string message;
+
+  // host copies of the final iterate
+  std::vector<double> host_u() const;
+  std::vector<double> host_x() const;
+
+ private:
+  struct Scaled {
+    double total, stationarity, primal, comp, comp_raw;
+  };
+  struct IterStore {
+    DArr<double> x, u, s, y, z, klo, kup, nlo, nup, llo, lup;
+    DevIter view();
+  };
+  Scaled scaled_error(const DevIter& it, Engine::Bundle& bd, double mu);
+  bool attempt(double dw, const DevIter& it);  // one inertia-loop attempt (kkt.cpp:954-1001)
+  void compute_step(const DevIter& it);         // solve_reduced (kkt.cpp:945-1006)
+  double fetch1(const double* d);
+  template <int K>
+  std::array<double, K> fetch(const double* d);
+  DevStep step_view(DArr<double>* s);
+  double now() const;
+
+  Engine& e;
+  SolverOptions o;
+  IpmDims d{};
+  DevBounds b{};
+  DArr<double> xlo, xup, ulo, uup, slo, sup;
+  IterStore its[2];
+  int icur = 0;
+  DevIter cur() { return its[icur].view(); }
+  DevIter alt() { return its[1 - icur].view(); }
+  bool bundle_fresh = false;
+  double mult_count = 0;
+  // augmented / refinement storage
+  DArr<double> r1x, r1u, gsum_u, rhat2_part;
+  DArr<double> p[5], q[5];  // px, pu, ps, pz, py
+  DArr<double> bsv[6];
+  DArr<double> o1x, o1u, o2, o3, o4, o1u_part;
+  DArr<double> c_rhat1, c_rhat2, rhs_sum, pu_rhs;
+  DArr<double> ft, gt, ht;  // line-search trial values
+  DArr<double> partial, scal;
+  DArr<int> flag;
+  double* pinned = nullptr;
+  int corrections = 0, refinements = 0;
+  double last_dw = 0;
+  std::chrono::steady_clock::time_point t0_;
+};
+
+}  // namespace bipm
