@@ -156,6 +156,18 @@ int bipm_solver_result(bipm_solver* s, bipm_solve_result* r, double* u);
  * mu, alpha_primal, alpha_dual, t_ad, t_kkt, t_total, corrections,
  * refinements, delta_w, full_step */
 int bipm_solver_log(bipm_solver* s, int32_t k, double rec[15]);
+/* one iteration bracketed by CUDA events on the engine stream; restarts the
+ * solve when the previous one terminated (bench harness) */
+int bipm_solver_step_timed(bipm_solver* s, int32_t* status, double* device_ms);
+/* instrumentation: out = kernels launched by this library, H2D bytes, D2H bytes */
+int bipm_counters(int64_t out[3]);
+/* CUDA-event timing of the named kernel groups (lu_refactor, reduce_tiles,
+ * reduce_rhs, cholesky, recover_state, condense, ad_bundle, ad_values) */
+int bipm_ctx_profile(bipm_ctx* c, int32_t enable);
+int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* count);
+/* out = reduce tile width, scenarios per CTA, chunks, panel-in-smem, nnz(L),
+ * nnz(L+U), LU multiply-adds, SM count */
+int bipm_ctx_info(bipm_ctx* c, int64_t out[8]);
 /* whole solve: start + steps until a terminal status */
 int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u);
 

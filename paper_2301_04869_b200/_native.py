@@ -73,6 +73,12 @@ SIGNATURES = {
     "bipm_solver_result": (ctypes.c_int, [_P, _P, _D]),
     "bipm_solver_log": (ctypes.c_int, [_P, ctypes.c_int32, _D]),
     "bipm_solve": (ctypes.c_int, [_P, _P, _P, _D]),
+    "bipm_solver_step_timed": (ctypes.c_int, [_P, _I, _D]),
+    "bipm_counters": (ctypes.c_int, [ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_ctx_profile": (ctypes.c_int, [_P, ctypes.c_int32]),
+    "bipm_ctx_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, _D,
+                                            ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_ctx_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -214,6 +220,22 @@ class Context:
                                      ctypes.byref(bad)))
         return f, g, h
 
+    def profile(self, enable: bool = True):
+        check(lib().bipm_ctx_profile(self._h, 1 if enable else 0))
+
+    def kernel_time(self, name: str):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        check(lib().bipm_ctx_kernel_time(self._h, name.encode(), ctypes.byref(ms),
+                                         ctypes.byref(n)))
+        return ms.value, n.value
+
+    def info(self) -> dict:
+        out = (ctypes.c_int64 * 8)()
+        check(lib().bipm_ctx_info(self._h, out))
+        keys = ("tile_cols", "chunk", "nchunks", "panel_in_smem", "nnz_l", "nnz_f", "lu_madds",
+                "sm_count")
+        return dict(zip(keys, list(out)))
+
     def __del__(self):
         if getattr(self, "_h", None):
             lib().bipm_ctx_destroy(self._h)
@@ -253,6 +275,11 @@ class Solver:
         check(lib().bipm_solver_log(self._h, k, dptr(rec)))
         return dict(zip(LOG_FIELDS, rec.tolist()))
 
+    def step_timed(self):
+        st, ms = ctypes.c_int32(-1), ctypes.c_double()
+        check(lib().bipm_solver_step_timed(self._h, ctypes.byref(st), ctypes.byref(ms)))
+        return st.value, ms.value
+
     def solve(self):
         self.start()
         st = -1
@@ -264,3 +291,9 @@ class Solver:
         if getattr(self, "_h", None):
             lib().bipm_solver_destroy(self._h)
             self._h = None
+
+
+def counters() -> dict:
+    out = (ctypes.c_int64 * 3)()
+    check(lib().bipm_counters(out))
+    return {"launches": out[0], "h2d_bytes": out[1], "d2h_bytes": out[2]}

@@ -286,6 +286,52 @@ int bipm_solver_log(bipm_solver* s, int32_t k, double rec[15]) {
   });
 }
 
+int bipm_solver_step_timed(bipm_solver* s, int32_t* status, double* device_ms) {
+  return guarded([&] {
+    int st = 0;
+    const double ms = s->s->step_timed(&st);
+    if (status) *status = st;
+    if (device_ms) *device_ms = ms;
+  });
+}
+
+int bipm_counters(int64_t out[3]) {
+  return guarded([&] {
+    out[0] = stats().launches.load();
+    out[1] = stats().h2d_bytes.load();
+    out[2] = stats().d2h_bytes.load();
+  });
+}
+
+int bipm_ctx_profile(bipm_ctx* c, int32_t enable) {
+  return guarded([&] {
+    c->eng->profiling = enable != 0;
+    c->eng->ktimers.clear();
+  });
+}
+
+int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* count) {
+  return guarded([&] {
+    auto it = c->eng->ktimers.find(name);
+    *ms = it == c->eng->ktimers.end() ? 0.0 : it->second.ms;
+    *count = it == c->eng->ktimers.end() ? 0 : it->second.n;
+  });
+}
+
+int bipm_ctx_info(bipm_ctx* c, int64_t out[8]) {
+  return guarded([&] {
+    const Engine& e = *c->eng;
+    out[0] = e.red.kc;
+    out[1] = e.red.chunk;
+    out[2] = e.red.nchunks;
+    out[3] = e.red.panel_in_smem ? 1 : 0;
+    out[4] = e.pb.LU.nnz_l;
+    out[5] = e.pb.LU.nnz_f;
+    out[6] = (int64_t)e.pb.LU.mul_l.size();
+    out[7] = e.sm_count;
+  });
+}
+
 int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u) {
   return guarded([&] {
     Solver s(*c->eng, to_options(opts));

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include "../kernels/stats.hpp"
+
 namespace bipm {
 
 inline void cuda_check(cudaError_t e, const char* what) {
@@ -42,17 +44,21 @@ class DArr {
   void upload(const std::vector<T>& v) {
     resize(v.size());
     if (n_) cuda_check(cudaMemcpy(p_, v.data(), n_ * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    stats().h2d_bytes += (long long)(n_ * sizeof(T));
   }
   void upload(const T* src, size_t n, cudaStream_t st) {
     resize(n);
     if (n_) cuda_check(cudaMemcpyAsync(p_, src, n_ * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+    stats().h2d_bytes += (long long)(n_ * sizeof(T));
   }
   void download(T* dst, size_t n, cudaStream_t st) const {
     if (n) cuda_check(cudaMemcpyAsync(dst, p_, n * sizeof(T), cudaMemcpyDeviceToHost, st), "download");
+    stats().d2h_bytes += (long long)(n * sizeof(T));
   }
   std::vector<T> to_host() const {
     std::vector<T> v(n_);
     if (n_) cuda_check(cudaMemcpy(v.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "to_host");
+    stats().d2h_bytes += (long long)(n_ * sizeof(T));
     return v;
   }
   void zero(cudaStream_t st) {

@@ -50,6 +50,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   cuda_check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
+  cuda_check(cudaEventCreate(&ev_a), "event");
+  cuda_check(cudaEventCreate(&ev_b), "event");
   const DerivPlan& D = pb.D;
   const LuPlan& L = pb.LU;
   const OpfModel& Mo = pb.M;
@@ -154,6 +156,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
 }
 
 Engine::~Engine() {
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
   if (st) {
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -163,7 +167,9 @@ Engine::~Engine() {
 void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 
 idx Engine::factor_gx() {
-  launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), lu_status.get(), 1e-12, st);
+  timed("lu_refactor", [&] {
+    launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), lu_status.get(), 1e-12, st);
+  });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
   sync();
@@ -173,6 +179,10 @@ idx Engine::factor_gx() {
 }
 
 void Engine::condense_blocks() {
+  timed("condense", [&] { condense_launch(); });
+}
+
+void Engine::condense_launch() {
   const DerivPlan& D = pb.D;
   const int m = pb.M.m;
   launch_condense(cxx.v, M, bd().wxx.get(), D.wxx.nnz(), bd().hx.get(), D.h.x.nnz(), bd().hx.get(), D.h.x.nnz(),
@@ -193,7 +203,7 @@ void Engine::reduce_local(double dw) {
   red.dw = dw;
   red.partial = red_partial.get();
   red.scratch = red_scratch.get();
-  launch_reduce_tiles(red, st);
+  timed("reduce_tiles", [&] { launch_reduce_tiles(red, st); });
 }
 
 void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
@@ -215,7 +225,7 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   a.rhat3 = d_rhat3 ? d_rhat3 : rhat3.get();
   a.dw = dw;
   a.part = rhs_part.get();
-  launch_reduce_rhs(a, st);
+  timed("reduce_rhs", [&] { launch_reduce_rhs(a, st); });
   launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st);
 }
 
@@ -226,7 +236,7 @@ void Engine::finish_reduce(double dw) {
 }
 
 bool Engine::factor_khat() {
-  launch_shift_cholesky(khat.get(), pb.M.n_u, chol_info.get(), nullptr, st);
+  timed("cholesky", [&] { launch_shift_cholesky(khat.get(), pb.M.n_u, chol_info.get(), nullptr, st); });
   int info = 0;
   chol_info.download(&info, 1, st);
   sync();
@@ -257,7 +267,7 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.dw = dw;
   a.px = d_px;
   a.py = d_py;
-  launch_recover_state(a, st);
+  timed("recover_state", [&] { launch_recover_state(a, st); });
   launch_recover_slack(hx_p.v, hu_p.v, pb.M.m, pb.M.n_x, M, bd().hx.get(), bd().hu.get(), d_px, d_pu,
                        sigma_s.get(), d_r2 ? d_r2 : r2.get(), d_r4 ? d_r4 : r4.get(), d_pz, d_ps, st);
 }
@@ -397,7 +407,7 @@ idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const d
   b.grad = out.grad.get();
   b.bad = bad.get();
   bad.zero(st);
-  launch_ad_bundle(ad, b, st);
+  timed("ad_bundle", [&] { launch_ad_bundle(ad, b, st); });
   return first_bad();
 }
 
@@ -413,7 +423,7 @@ idx Engine::eval_values(const double* dX, const double* du, double* df, double* 
   b.h = dh;
   b.bad = bad.get();
   bad.zero(st);
-  launch_ad_values(ad, b, st);
+  timed("ad_values", [&] { launch_ad_values(ad, b, st); });
   return first_bad();
 }
 

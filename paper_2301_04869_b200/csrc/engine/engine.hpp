@@ -7,6 +7,7 @@
 // linalg.hpp:116) and run entirely on the device stream.
 #pragma once
 
+#include <map>
 #include <memory>
 #include <string>
 #include <vector>
@@ -103,6 +104,7 @@ class Engine {
   idx factor_gx();
   // condense (kkt.cpp:123-170) of the K blocks from the bundle and sigma_s
   void condense_blocks();
+  void condense_launch();
   // local part of reduce (kkt.cpp:371-466): khat/rhs partial sums over the
   // owned scenarios, without the sigma_u / rhat2 terms.
   void reduce_local(double delta_w);
@@ -121,6 +123,31 @@ class Engine {
 
   void sync();
   void upload_ad();
+
+  // optional CUDA-event timing of named kernel groups on the engine stream
+  struct KTimer {
+    double ms = 0;
+    long long n = 0;
+  };
+  bool profiling = false;
+  std::map<std::string, KTimer> ktimers;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  template <typename F>
+  void timed(const char* name, F&& launch) {
+    if (!profiling) {
+      launch();
+      return;
+    }
+    cudaEventRecord(ev_a, st);
+    launch();
+    cudaEventRecord(ev_b, st);
+    cudaEventSynchronize(ev_b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev_a, ev_b);
+    KTimer& t = ktimers[name];
+    t.ms += ms;
+    ++t.n;
+  }
   idx first_bad();
   size_t nnz(const Csr& c) const { return size_t(c.nnz()); }
 };

@@ -95,6 +95,7 @@ template <int K>
 std::array<double, K> Solver::fetch(const double* dptr) {
   cuda_check(cudaMemcpyAsync(pinned, dptr, K * sizeof(double), cudaMemcpyDeviceToHost, e.st),
              "fetch");
+  stats().d2h_bytes += K * (long long)sizeof(double);
   e.sync();
   std::array<double, K> r;
   std::copy(pinned, pinned + K, r.begin());
@@ -409,6 +410,23 @@ int Solver::step() {
   log.alpha_primal = alpha;
   log.alpha_dual = ad;
   return finish(kRunning);
+}
+
+double Solver::step_timed(int* st_out) {
+  if (status != kRunning) start();
+  cudaEvent_t a, z;
+  cuda_check(cudaEventCreate(&a), "event");
+  cuda_check(cudaEventCreate(&z), "event");
+  cudaEventRecord(a, e.st);
+  const int s = step();
+  cudaEventRecord(z, e.st);
+  cudaEventSynchronize(z);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, z);
+  cudaEventDestroy(a);
+  cudaEventDestroy(z);
+  if (st_out) *st_out = s;
+  return ms;
 }
 
 int Solver::solve() {

@@ -48,6 +48,9 @@ class Solver {
   void start();      // initial_iterate (ipm.cpp:59-105)
   int step();        // one IPM iteration; returns a SolveStatusCode
   int solve();       // start + steps until done
+  // one step bracketed by CUDA events on the engine stream (restarts the
+  // solve first when it already terminated); returns the device ms
+  double step_timed(int* st_out);
 
   int status = kRunning;
   int iter = 0;

@@ -15,6 +15,8 @@
 #include "ad_kernels.cuh"
 #include "ad_launch.hpp"
 
+#include "stats.hpp"
+
 namespace bipm {
 
 namespace {
@@ -380,20 +382,30 @@ void check(const char* what) {
 void launch_ad_bundle(const DevAd& A, const AdBuffers& b, cudaStream_t st) {
   const long long M = A.M;
   ad_forward_kernel<true><<<blocks(M * (A.nbus + A.nbr + A.ngen)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_slack_kernel<true><<<blocks(M * (A.nsd + 1)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_values_kernel<<<blocks(M * (1 + A.n_x + A.m)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_jacobian_kernel<<<blocks(M * (A.gx.n + A.gu.n + A.hx.n + A.hu.n)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_weights_kernel<<<blocks(M * A.n_b), kB, 0, st>>>(A, b);
+  note_launch();
   ad_second_kernel<<<blocks(M * (A.nbus + A.nbr + A.ngen + A.nsd)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_hessian_kernel<<<blocks(M * (A.wxx.n + A.wxu.n + A.wuu.n + A.n_d)), kB, 0, st>>>(A, b);
+  note_launch();
   check("ad_bundle");
 }
 
 void launch_ad_values(const DevAd& A, const AdBuffers& b, cudaStream_t st) {
   const long long M = A.M;
   ad_forward_kernel<false><<<blocks(M * (A.nbus + A.nbr + A.ngen)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_slack_kernel<false><<<blocks(M * (A.nsd + 1)), kB, 0, st>>>(A, b);
+  note_launch();
   ad_values_kernel<<<blocks(M * (1 + A.n_x + A.m)), kB, 0, st>>>(A, b);
+  note_launch();
   check("ad_values");
 }
 

@@ -5,6 +5,8 @@
 
 #include "ipm_kernels.hpp"
 
+#include "stats.hpp"
+
 namespace bipm {
 
 namespace {
@@ -59,6 +61,7 @@ void finalize(const double* partial, int nblocks, const int (&op)[K], double* ou
   for (int k = 0; k < K; ++k) o[k] = op[k];
   finalize_kernel<K><<<1, 32, 0, st>>>(partial, nblocks, nullptr, out, o[0], o[1], o[2], o[3],
                                        o[4], o[5], o[6], o[7]);
+  note_launch();
 }
 
 int red_blocks(long long n) {
@@ -684,6 +687,7 @@ __global__ void pu_rhs_kernel(int n, const double* S, const double* r, double* p
 void launch_pu_rhs(int n, const double* S, const double* r, double* pu, bool first,
                    cudaStream_t st) {
   pu_rhs_kernel<<<ew_blocks(n), kB, 0, st>>>(n, S, r, pu, first ? 1 : 0);
+  note_launch();
   check("pu_rhs");
 }
 
@@ -692,6 +696,7 @@ void launch_kkt_error_xs(const IpmDims& d, const DevIter& it, const DevBounds& b
                          double* partial, double* out6, cudaStream_t st) {
   const int nb = red_blocks((long long)d.M * (d.n_x + d.m));
   kkt_error_xs_kernel<<<nb, kB, 0, st>>>(d, it, b, grad, g, h, mu, partial);
+  note_launch();
   const int ops[6] = {kMax, kMax, kMax, kMax, kMax, kSum};
   finalize<6>(partial, nb, ops, out6, st);
   check("kkt_error_xs");
@@ -699,12 +704,14 @@ void launch_kkt_error_xs(const IpmDims& d, const DevIter& it, const DevBounds& b
 
 void launch_grad_u_sum(const IpmDims& d, const double* grad, double* gsum, cudaStream_t st) {
   grad_u_sum_kernel<<<ew_blocks(d.n_u), kB, 0, st>>>(d, grad, gsum);
+  note_launch();
   check("grad_u_sum");
 }
 
 void launch_kkt_error_u(const IpmDims& d, const DevIter& it, const DevBounds& b,
                         const double* gsum, double mu, double* out3, cudaStream_t st) {
   kkt_error_u_kernel<<<1, kB, 0, st>>>(d, it, b, gsum, mu, out3);
+  note_launch();
   check("kkt_error_u");
 }
 
@@ -714,6 +721,7 @@ void launch_assemble_xs(const IpmDims& d, const DevIter& it, const DevBounds& b,
                         cudaStream_t st) {
   assemble_xs_kernel<<<ew_blocks((long long)d.M * (d.n_x + d.m)), kB, 0, st>>>(
       d, it, b, grad, h, mu, sigma_x, r1x, sigma_s, r2, r4, flag);
+  note_launch();
   check("assemble_xs");
 }
 
@@ -721,6 +729,7 @@ void launch_assemble_u(const IpmDims& d, const DevIter& it, const DevBounds& b,
                        const double* gsum, double mu, double* sigma_u, double* r1u, int* flag,
                        cudaStream_t st) {
   assemble_u_kernel<<<ew_blocks(d.n_u), kB, 0, st>>>(d, it, b, gsum, mu, sigma_u, r1u, flag);
+  note_launch();
   check("assemble_u");
 }
 
@@ -730,12 +739,14 @@ void launch_condensed_rhs(const IpmDims& d, const DevCsr& hx, const DevCsr& hu,
                           double* part_u, cudaStream_t st) {
   condensed_rhs_kernel<<<ew_blocks((long long)d.M * (d.n_x + d.n_u)), kB, 0, st>>>(
       d, hx, hu, hx_v, hu_v, sigma_s, r4, r2, r1x, rhat1, part_u);
+  note_launch();
   check("condensed_rhs");
 }
 
 void launch_scenario_sum(int M, int n, const double* part, const double* base, double* out,
                          cudaStream_t st) {
   scenario_sum_kernel<<<ew_blocks(n), kB, 0, st>>>(M, n, part, base, out);
+  note_launch();
   check("scenario_sum");
 }
 
@@ -744,6 +755,7 @@ void launch_aug_residual(const AugResidualArgs& a, double* partial, double* out1
   const IpmDims& d = a.d;
   const int nb = red_blocks((long long)d.M * (2 * d.n_x + 2 * d.m + d.n_u));
   aug_residual_kernel<<<nb, kB, 0, st>>>(a, partial);
+  note_launch();
   const int ops[1] = {kMax};
   finalize<1>(partial, nb, ops, out1, st);
   check("aug_residual");
@@ -751,6 +763,7 @@ void launch_aug_residual(const AugResidualArgs& a, double* partial, double* out1
 
 void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st) {
   aug_residual_u_kernel<<<1, kB, 0, st>>>(a, o1u, out1);
+  note_launch();
   check("aug_residual_u");
 }
 
@@ -759,6 +772,7 @@ void launch_rhs_scale(const IpmDims& d, const double* r1x, const double* r1u, co
                       cudaStream_t st) {
   const int nb = red_blocks(2LL * d.M * (d.n_x + d.m) + d.n_u);
   rhs_scale_kernel<<<nb, kB, 0, st>>>(d, r1x, r1u, r2, r3, r4, partial);
+  note_launch();
   const int ops[1] = {kMax};
   finalize<1>(partial, nb, ops, out1, st);
   check("rhs_scale");
@@ -766,6 +780,7 @@ void launch_rhs_scale(const IpmDims& d, const double* r1x, const double* r1u, co
 
 void launch_axpy_step(const IpmDims& d, DevStep a, DevStep q, cudaStream_t st) {
   axpy_step_kernel<<<ew_blocks((long long)d.M * (d.n_x + d.m) + d.n_u), kB, 0, st>>>(d, a, q);
+  note_launch();
   check("axpy_step");
 }
 
@@ -774,6 +789,7 @@ void launch_bound_steps(const IpmDims& d, const DevIter& it, const DevBounds& b,
                         cudaStream_t st) {
   const int nb = red_blocks((long long)d.M * (d.n_x + d.m) + d.n_u);
   bound_steps_kernel<<<nb, kB, 0, st>>>(d, it, b, p, mu, tau, bs, partial);
+  note_launch();
   const int ops[2] = {kMin, kMin};
   finalize<2>(partial, nb, ops, out2, st);
   check("bound_steps");
@@ -784,6 +800,7 @@ void launch_apply_step(const IpmDims& d, const DevIter& it, DevIter trial, const
                        cudaStream_t st) {
   apply_step_kernel<<<ew_blocks((long long)d.M * (d.n_x + d.m) + d.n_u), kB, 0, st>>>(
       d, it, trial, b, p, bs, ap, ad, mu);
+  note_launch();
   check("apply_step");
 }
 
@@ -791,6 +808,7 @@ void launch_primal_trial(const IpmDims& d, const DevIter& it, DevIter trial, con
                          double alpha, cudaStream_t st) {
   primal_trial_kernel<<<ew_blocks((long long)d.M * (d.n_x + d.m) + d.n_u), kB, 0, st>>>(
       d, it, trial, p, alpha);
+  note_launch();
   check("primal_trial");
 }
 
@@ -803,6 +821,7 @@ void launch_merit(const IpmDims& d, const DevIter& it, const DevBounds& b, const
   const int nb = red_blocks((long long)d.M * (d.n_x + d.n_u + d.m + 1));
   merit_kernel<<<nb, kB, 0, st>>>(d, it, b, p, grad, f, g, h, gx, gu, hx, hu, gx_v, gu_v, hx_v,
                                   hu_v, mu, partial);
+  note_launch();
   const int ops[8] = {kSum, kMax, kMax, kSum, kSum, kSum, kSum, kSum};
   finalize<8>(partial, nb, ops, out8, st);
   check("merit");
@@ -811,6 +830,7 @@ void launch_merit(const IpmDims& d, const DevIter& it, const DevBounds& b, const
 void launch_merit_u(const IpmDims& d, const DevIter& it, const DevBounds& b, const double* pu,
                     double mu, double* out2, cudaStream_t st) {
   merit_u_kernel<<<1, kB, 0, st>>>(d, it, b, pu, mu, out2);
+  note_launch();
   check("merit_u");
 }
 
@@ -819,6 +839,7 @@ void launch_ls_values(const IpmDims& d, const DevIter& trial, const DevBounds& b
                       double* out3, cudaStream_t st) {
   const int nb = red_blocks((long long)d.M * (d.n_x + d.m + 1));
   ls_values_kernel<<<nb, kB, 0, st>>>(d, trial, b, f, g, h, partial);
+  note_launch();
   const int ops[3] = {kSum, kSum, kSum};
   finalize<3>(partial, nb, ops, out3, st);
   check("ls_values");
@@ -827,12 +848,14 @@ void launch_ls_values(const IpmDims& d, const DevIter& trial, const DevBounds& b
 void launch_init_slacks(const IpmDims& d, DevIter it, const DevBounds& b, const double* h,
                         double mu0, cudaStream_t st) {
   init_slacks_kernel<<<ew_blocks((long long)d.M * d.m), kB, 0, st>>>(d, it, b, h, mu0);
+  note_launch();
   check("init_slacks");
 }
 
 void launch_init_x(const IpmDims& d, DevIter it, const DevBounds& b, const double* x0,
                    double mu0, cudaStream_t st) {
   init_x_kernel<<<ew_blocks((long long)d.M * d.n_x), kB, 0, st>>>(d, it, b, x0, mu0);
+  note_launch();
   check("init_x");
 }
 

@@ -19,6 +19,8 @@
 #include "kkt_kernels.hpp"
 #include "sweeps.cuh"
 
+#include "stats.hpp"
+
 namespace bipm {
 
 namespace {
@@ -463,6 +465,7 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                         int* status, double piv_tol, cudaStream_t st) {
   if (M <= 0) return;
   lu_refactor_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, status, piv_tol);
+  note_launch();
   check_launch("lu_refactor");
 }
 
@@ -504,6 +507,7 @@ void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
     attr_set = true;
   }
   reduce_tiles_kernel<kSolveBlock><<<dim3(tiles, a.nchunks), kSolveBlock, smem, st>>>(a);
+  note_launch();
   check_launch("reduce_tiles");
 }
 
@@ -514,6 +518,7 @@ void launch_sum_parts(const double* parts, int nparts, long long len, double* ou
   const int B = 256;
   sum_parts_kernel<<<int((len + B - 1) / B), B, 0, st>>>(parts, nparts, len, out, diag_add, dw,
                                                           n_mat, sub_vec);
+  note_launch();
   check_launch("sum_parts");
 }
 
@@ -537,6 +542,7 @@ void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
     attr_set = true;
   }
   reduce_rhs_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
+  note_launch();
   check_launch("reduce_rhs");
 }
 
@@ -560,6 +566,7 @@ void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
     attr_set = true;
   }
   recover_state_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
+  note_launch();
   check_launch("recover_state");
 }
 
@@ -571,6 +578,7 @@ void launch_recover_slack(const DevCsr& hx, const DevCsr& hu, int m, int n_x, in
   if (n <= 0) return;
   recover_slack_kernel<<<int((n + 255) / 256), 256, 0, st>>>(hx, hu, m, n_x, M, hx_v, hu_v, px,
                                                               pu, sigma_s, r2, r4, pz, ps);
+  note_launch();
   check_launch("recover_slack");
 }
 
@@ -581,16 +589,19 @@ void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, cons
   if (n <= 0) return;
   condense_kernel<<<int((n + 255) / 256), 256, 0, st>>>(c, M, W, ldw, A, lda, B, ldb, sigma, lds,
                                                          out);
+  note_launch();
   check_launch("condense");
 }
 
 void launch_shift_cholesky(double* K, int n, int* info, double*, cudaStream_t st) {
   shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
+  note_launch();
   check_launch("shift_cholesky");
 }
 
 void launch_cholesky_solve(const double* L, int n, double* b, cudaStream_t st) {
   cholesky_solve_kernel<<<1, kDenseBlock, 0, st>>>(L, n, b);
+  note_launch();
   check_launch("cholesky_solve");
 }
 
