@@ -162,7 +162,8 @@ int bipm_solver_step_timed(bipm_solver* s, int32_t* status, double* device_ms);
 /* instrumentation: out = kernels launched by this library, H2D bytes, D2H bytes */
 int bipm_counters(int64_t out[3]);
 /* CUDA-event timing of the named kernel groups (lu_refactor, reduce_tiles,
- * reduce_rhs, cholesky, recover_state, condense, ad_bundle, ad_values) */
+ * reduce_rhs, cholesky, recover_state, condense, ad_bundle, ad_values);
+ * enabling starts a new window (clears), disabling keeps the totals */
 int bipm_ctx_profile(bipm_ctx* c, int32_t enable);
 int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* count);
 /* out = reduce tile width, scenarios per CTA, chunks, panel-in-smem, nnz(L),

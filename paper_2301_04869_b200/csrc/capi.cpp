@@ -81,6 +81,25 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
       {"lu_l_ptr", &P.LU.l_ptr},     {"lu_l_col", &P.LU.l_col},     {"lu_u_ptr", &P.LU.u_ptr},
       {"lu_u_col", &P.LU.u_col},     {"lu_mul_ptr", &P.LU.mul_ptr}};
   if (auto it = ivecs.find(name); it != ivecs.end()) return ints(*it->second);
+  static thread_local std::vector<idx> scalars;
+  if (name == "lu_shape") {
+    scalars = {P.LU.n, P.LU.nnz_l, P.LU.nnz_f, P.LU.t0, P.LU.tl};
+    return ints(scalars);
+  }
+  const std::map<std::string, const std::vector<idx>*> lu_more = {
+      {"lu_ft_src", &P.LU.ft_src},     {"lu_diag", &P.LU.diag},     {"lu_a_src", &P.LU.a_src},
+      {"lu_dense_src0", &P.LU.dense_src[0]}, {"lu_dense_src1", &P.LU.dense_src[1]},
+      {"lu_dense_src2", &P.LU.dense_src[2]}, {"lu_dense_src3", &P.LU.dense_src[3]}};
+  if (auto it = lu_more.find(name); it != lu_more.end()) return ints(*it->second);
+  const std::map<std::string, const SweepPlan*> sweeps = {
+      {"sL", &P.LU.sL}, {"sU", &P.LU.sU}, {"sUt", &P.LU.sUt}, {"sLt", &P.LU.sLt}};
+  for (const auto& [pre, sw] : sweeps) {
+    if (name == "lu_" + pre + "_ptr") return ints(sw->ptr);
+    if (name == "lu_" + pre + "_col") return ints(sw->col);
+    if (name == "lu_" + pre + "_lvl_ptr") return ints(sw->lvl_ptr);
+    if (name == "lu_" + pre + "_items") return ints(sw->items);
+    if (name == "lu_" + pre + "_tail_items") return ints(sw->tail_items);
+  }
   throw Error(kInvalidArgument, "unknown problem array '" + name + "'");
 }
 
@@ -305,8 +324,8 @@ int bipm_counters(int64_t out[3]) {
 
 int bipm_ctx_profile(bipm_ctx* c, int32_t enable) {
   return guarded([&] {
+    if (enable && !c->eng->profiling) c->eng->ktimers.clear();  // a new profiling window
     c->eng->profiling = enable != 0;
-    c->eng->ktimers.clear();
   });
 }
 

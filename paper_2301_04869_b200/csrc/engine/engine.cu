@@ -75,7 +75,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
     lu_arrays.back().upload(v);
     return lu_arrays.back().get();
   };
-  lu_arrays.reserve(40);
+  lu_arrays.reserve(80);
   lu.n = L.n;
   lu.nnz_l = L.nnz_l;
   lu.nnz_f = L.nnz_f;
@@ -108,6 +108,29 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   lu.mul_ptr = up(L.mul_ptr);
   lu.mul_l = up(L.mul_l);
   lu.mul_u = up(L.mul_u);
+  lu.t0 = L.t0;
+  lu.tl = L.tl;
+  lu.ft_src = up(L.ft_src);
+  {
+    std::vector<idx> ds;
+    for (const auto& v : L.dense_src) ds.insert(ds.end(), v.begin(), v.end());
+    if (ds.empty()) ds.push_back(-1);
+    lu.dense_src = up(ds);
+  }
+  auto sweep = [&](const SweepPlan& S) {
+    DevSweep d{};
+    d.col = up(S.col.empty() ? std::vector<idx>{0} : S.col);
+    d.items = up(S.items.empty() ? std::vector<idx>{0, 0, 0, 0} : S.items);
+    d.lvl_ptr = up(S.lvl_ptr);
+    d.n_lvl = idx(S.lvl_ptr.size()) - 1;
+    d.tail_items = up(S.tail_items.empty() ? std::vector<idx>{0, 0, 0, 0} : S.tail_items);
+    d.n_tail = idx(S.tail_items.size() / 4);
+    return d;
+  };
+  lu.sL = sweep(L.sL);
+  lu.sU = sweep(L.sU);
+  lu.sUt = sweep(L.sUt);
+  lu.sLt = sweep(L.sLt);
 
   const size_t Ms = size_t(M);
   for (Bundle& b : bundles) {
@@ -136,6 +159,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   sigma_u.resize(size_t(Mo.n_u));
   rhat2.resize(size_t(Mo.n_u));
   F.resize(Ms * size_t(L.nnz_f));
+  FT.resize(Ms * size_t(L.nnz_f));
+  Dt.resize(std::max<size_t>(1, Ms * 4 * size_t(L.tl) * size_t(L.tl)));
   lu_status.resize(Ms);
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));
@@ -168,7 +193,8 @@ void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 
 idx Engine::factor_gx() {
   timed("lu_refactor", [&] {
-    launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), lu_status.get(), 1e-12, st);
+    launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
+                       lu_status.get(), 1e-12, st);
   });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
@@ -195,6 +221,8 @@ void Engine::condense_launch() {
 
 void Engine::reduce_local(double dw) {
   red.F = F.get();
+  red.FT = FT.get();
+  red.D = Dt.get();
   red.gu_v = bd().gu.get();
   red.kxx_v = kxx.get();
   red.kxu_v = kxu.get();
@@ -217,6 +245,8 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   a.n_u = pb.M.n_u;
   a.M = M;
   a.F = F.get();
+  a.FT = FT.get();
+  a.D = Dt.get();
   a.gu_v = bd().gu.get();
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();
@@ -257,6 +287,8 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.n_u = pb.M.n_u;
   a.M = M;
   a.F = F.get();
+  a.FT = FT.get();
+  a.D = Dt.get();
   a.gu_v = bd().gu.get();
   a.kxx_v = kxx.get();
   a.kxu_v = kxu.get();

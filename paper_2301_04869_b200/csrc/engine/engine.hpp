@@ -84,7 +84,7 @@ class Engine {
   DArr<double> kxx, kxu, kuu;                  // condensed blocks
   DArr<double> sigma_x, sigma_s, rhat1, rhat3, r2, r4;
   DArr<double> sigma_u, rhat2;                 // n_u (replicated)
-  DArr<double> F;                              // LU factors [M][nnz_f]
+  DArr<double> F, FT, Dt;                      // LU factors [M][nnz_f], transposed, dense tails
   DArr<int> lu_status;
   // ---- reduction workspace
   ReduceLaunch red{};

@@ -239,6 +239,144 @@ std::vector<idx> min_degree_order(const Csr& S) {
   return order;
 }
 
+namespace {
+
+// Trailing block solved densely: the run of narrow forward levels (<= 2 rows)
+// at the end of the schedule, capped at 256 rows.
+idx choose_tail(const std::vector<idx>& fwd_level, idx n) {
+  idx nlev = 0;
+  for (idx v : fwd_level) nlev = std::max(nlev, v + 1);
+  std::vector<idx> width(size_t(nlev), 0);
+  for (idx v : fwd_level) ++width[size_t(v)];
+  idx t0 = n;
+  for (idx i = n - 1; i >= 0; --i) {
+    if (width[size_t(fwd_level[size_t(i)])] > 2) break;
+    if (n - i > 256) break;
+    t0 = i;
+  }
+  // rows in the tail must come after every non-tail row of their levels
+  return (n - t0) >= 8 ? t0 : n;
+}
+
+
+}  // namespace
+
+void build_sweeps(LuPlan& P, const std::vector<std::vector<idx>>& lrow,
+                  const std::vector<std::vector<idx>>& urow, const std::vector<idx>& fl) {
+  const idx n = P.n;
+  P.t0 = choose_tail(fl, n);
+  P.tl = n - P.t0;
+  const idx t0 = P.t0;
+  // --- CSR layouts with direct value indexing
+  SweepPlan& L = P.sL;
+  SweepPlan& U = P.sU;
+  SweepPlan& Ut = P.sUt;
+  SweepPlan& Lt = P.sLt;
+  L.has_diag = false, L.forward = true;
+  U.has_diag = true, U.forward = false;
+  Ut.has_diag = true, Ut.forward = true;
+  Lt.has_diag = false, Lt.forward = false;
+  for (SweepPlan* S : {&L, &U, &Ut, &Lt}) S->ptr.assign(1, 0);
+  for (idx i = 0; i < n; ++i) {
+    for (idx j : lrow[size_t(i)]) L.col.push_back(j);  // F[t] for t < nnz_l
+    L.ptr.push_back(idx(L.col.size()));
+    U.col.push_back(i);  // diag first; F[nnz_l + t]
+    for (idx c : urow[size_t(i)]) U.col.push_back(c);
+    U.ptr.push_back(idx(U.col.size()));
+  }
+  // FT: U' rows then L' rows
+  P.ft_src.clear();
+  auto u_slot_of = [&](idx r, idx c) {
+    if (r == c) return P.diag[size_t(r)];
+    const auto b = P.u_col.begin() + P.u_ptr[size_t(r)], e = P.u_col.begin() + P.u_ptr[size_t(r) + 1];
+    return P.u_slot[size_t(std::lower_bound(b, e, c) - P.u_col.begin())];
+  };
+  auto l_slot_of = [&](idx r, idx c) {
+    const auto b = P.l_col.begin() + P.l_ptr[size_t(r)], e = P.l_col.begin() + P.l_ptr[size_t(r) + 1];
+    return idx(std::lower_bound(b, e, c) - P.l_col.begin());
+  };
+  for (idx i = 0; i < n; ++i) {
+    Ut.col.push_back(i);
+    P.ft_src.push_back(P.diag[size_t(i)]);
+    for (idx k : lrow[size_t(i)]) {  // U(k, i), k < i
+      Ut.col.push_back(k);
+      P.ft_src.push_back(u_slot_of(k, i));
+    }
+    Ut.ptr.push_back(idx(Ut.col.size()));
+  }
+  for (idx i = 0; i < n; ++i) {
+    for (idx r : urow[size_t(i)]) {  // L(r, i), r > i
+      Lt.col.push_back(r);
+      P.ft_src.push_back(l_slot_of(r, i));
+    }
+    Lt.ptr.push_back(idx(Lt.col.size()));
+  }
+  // --- level schedules over the non-tail rows
+  std::vector<idx> lev(size_t(n), 0);
+  auto fill_items = [&](SweepPlan& S, const std::vector<std::vector<idx>>& dep, bool forward) {
+    std::fill(lev.begin(), lev.end(), -1);
+    idx nlev = 0;
+    if (forward) {
+      for (idx i = 0; i < t0; ++i) {
+        idx v = 0;
+        for (idx j : dep[size_t(i)])
+          if (j < t0) v = std::max(v, lev[size_t(j)] + 1);
+        lev[size_t(i)] = v;
+        nlev = std::max(nlev, v + 1);
+      }
+    } else {
+      for (idx i = t0 - 1; i >= 0; --i) {
+        idx v = 0;
+        for (idx j : dep[size_t(i)])
+          if (j < t0) v = std::max(v, lev[size_t(j)] + 1);
+        lev[size_t(i)] = v;
+        nlev = std::max(nlev, v + 1);
+      }
+    }
+    std::vector<std::vector<idx>> by(static_cast<size_t>(nlev));
+    for (idx i = 0; i < t0; ++i) by[size_t(lev[size_t(i)])].push_back(i);
+    S.lvl_ptr.assign(1, 0);
+    S.items.clear();
+    for (const auto& rows : by) {
+      for (idx r : rows) {
+        S.items.insert(S.items.end(), {r, S.ptr[size_t(r)], S.ptr[size_t(r) + 1], 0});
+      }
+      S.lvl_ptr.push_back(idx(S.items.size() / 4));
+    }
+    S.tail_items.clear();
+    if (forward)
+      for (idx r = t0; r < n; ++r) {
+        idx split = S.ptr[size_t(r)] + (S.has_diag ? 1 : 0);
+        while (split < S.ptr[size_t(r) + 1] && S.col[size_t(split)] < t0) ++split;
+        S.tail_items.insert(S.tail_items.end(), {r, S.ptr[size_t(r)], split, 0});
+      }
+  };
+  fill_items(L, lrow, true);
+  fill_items(U, urow, false);
+  fill_items(Ut, lrow, true);
+  fill_items(Lt, urow, false);
+  // --- dense tail blocks (column-major tl x tl)
+  const idx tl = P.tl;
+  for (auto& v : P.dense_src) v.assign(size_t(tl) * size_t(tl), -1);
+  for (idx a = 0; a < tl; ++a)
+    for (idx b = 0; b < tl; ++b) {
+      const idx r = t0 + a, c = t0 + b;  // entry (r, c) of the tail block
+      idx lslot = -1, uslot = -1;
+      if (r > c) {
+        const auto& lr = lrow[size_t(r)];
+        if (std::binary_search(lr.begin(), lr.end(), c)) lslot = l_slot_of(r, c);
+      } else {
+        const auto& ur = urow[size_t(r)];
+        if (r == c || std::binary_search(ur.begin(), ur.end(), c)) uslot = u_slot_of(r, c);
+      }
+      // column-major position of (a, b) is b * tl + a
+      P.dense_src[0][size_t(b) * tl + a] = lslot;  // L_TT
+      P.dense_src[1][size_t(a) * tl + b] = lslot;  // L_TT' : (b, a)
+      P.dense_src[2][size_t(b) * tl + a] = uslot;  // U_TT
+      P.dense_src[3][size_t(a) * tl + b] = uslot;  // U_TT'
+    }
+}
+
 LuPlan make_lu_plan(const Csr& A) {
   if (A.rows != A.cols) throw Error(kInvalidArgument, "lu plan: matrix not square");
   const idx n = A.rows;
@@ -399,6 +537,7 @@ LuPlan make_lu_plan(const Csr& A) {
       P.mul_l.push_back(a);
       P.mul_u.push_back(b);
     }
+  build_sweeps(P, lrow, urow, fl);
   P.lvl_u_ptr.assign(1, 0);
   P.lvl_l_ptr.assign(1, 0);
   for (idx l = 0; l < nf; ++l) {

@@ -51,6 +51,20 @@ struct DerivPlan {
 DerivPlan make_deriv_plan(const OpfModel& M, const LaneDeps& deps);
 CondenseProgram plan_condense_program(const Csr& W, const Csr& A, const Csr& B);
 
+// One triangular sweep over the permuted rows in "direct value" form: entry t
+// of row i has column col[t] and value V[t] of the sweep's value array (F or
+// FT below); with has_diag the first entry of each row is its diagonal.
+// Rows [t0, n) (the trailing separator block) are not level-scheduled: they
+// are solved as a dense triangle in registers; forward sweeps first gather
+// their entries with col < t0 (tail_items).
+struct SweepPlan {
+  bool has_diag = false, forward = true;
+  std::vector<idx> ptr, col;
+  std::vector<idx> lvl_ptr;     // item ranges per level
+  std::vector<idx> items;       // 4 ints per item: row, beg, end, 0
+  std::vector<idx> tail_items;  // 4 ints per tail row (forward sweeps): row, beg, split, 0
+};
+
 // Static-pivot LU of a structurally symmetric n x n pattern (P A P' = L U).
 // Factor values of one scenario live in one array of length nnz_f:
 //   [0, nnz_l)        strict lower L, row-major by permuted row
@@ -77,9 +91,21 @@ struct LuPlan {
   std::vector<idx> piv_of;      // per factor slot: pivot slot for L entries, -1 for U
   std::vector<idx> mul_ptr, mul_l, mul_u;
   long long flops() const { return 2LL * (long long)mul_l.size(); }
+
+  // ---- sweep layouts for the solve kernels
+  // F  = [L strict rows | U rows (diag first)]      (the refactor output)
+  // FT = [U' rows (diag first, then U(k,i), k<i) | L' rows (L(r,i), r>i)]
+  idx t0 = 0, tl = 0;             // dense tail rows [t0, n), tl = n - t0
+  std::vector<idx> ft_src;        // FT[p] = F[ft_src[p]]
+  // dense tail blocks, column-major tl x tl, source F slot or -1 (zero):
+  //   0: L_TT (unit lower)   1: L_TT' (unit upper)   2: U_TT   3: U_TT'
+  std::vector<idx> dense_src[4];
+  SweepPlan sL, sU, sUt, sLt;
 };
 
 std::vector<idx> min_degree_order(const Csr& sym_pattern);
 LuPlan make_lu_plan(const Csr& gx_pattern);
+void build_sweeps(LuPlan& P, const std::vector<std::vector<idx>>& lrow,
+                  const std::vector<std::vector<idx>>& urow, const std::vector<idx>& fwd_level);
 
 }  // namespace bipm

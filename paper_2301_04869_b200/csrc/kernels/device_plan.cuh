@@ -5,6 +5,16 @@
 
 namespace bipm {
 
+// One triangular sweep (host: SweepPlan in host/plan.hpp).
+struct DevSweep {
+  const int* col;
+  const int* items;       // int4 per item: row, begin, end, 0
+  const int* lvl_ptr;     // item ranges per level
+  int n_lvl;
+  const int* tail_items;  // int4 per tail row (forward sweeps): row, begin, split, 0
+  int n_tail;
+};
+
 // Static-pivot LU plan of G_x (host: LuPlan in host/plan.hpp).
 struct DevLu {
   int n, nnz_l, nnz_f, n_fwd, n_bwd;
@@ -17,6 +27,11 @@ struct DevLu {
   const int *fwd_ptr, *fwd_rows, *bwd_ptr, *bwd_rows;
   const int *lvl_u_ptr, *lvl_u_slot, *lvl_l_ptr, *lvl_l_slot;
   const int *a_src, *piv_of, *mul_ptr, *mul_l, *mul_u;
+  // solve layouts: transposed factor copy and dense tail blocks
+  int t0, tl;
+  const int* ft_src;     // [nnz_f]
+  const int* dense_src;  // [4 tl tl]
+  DevSweep sL, sU, sUt, sLt;
 };
 
 // A shared CSR pattern with an optional column-major (transposed) view:

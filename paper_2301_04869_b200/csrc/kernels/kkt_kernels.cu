@@ -25,7 +25,8 @@ namespace bipm {
 
 namespace {
 
-constexpr int kSolveBlock = 256;
+constexpr int kSolveBlock = 256;   // single right-hand side kernels
+constexpr int kReduceBlock = 1024; // multi-RHS reduction: one CTA per SM, latency hiding
 constexpr int kLuBlock = 256;
 constexpr int kDenseBlock = 1024;
 
@@ -72,7 +73,8 @@ __device__ __forceinline__ int find_in_row(const int* ptr, const int* ind, int r
 // ---------------------------------------------------------------- LU refactor
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const double* __restrict__ gx,
-                                                            int nnz_gx, double* F, int* status,
+                                                            int nnz_gx, double* F, double* FT,
+                                                            double* D, int* status,
                                                             double piv_tol) {
   const int s = blockIdx.x;
   const double* __restrict__ A = gx + size_t(s) * nnz_gx;
@@ -125,11 +127,26 @@ __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const doubl
   }
   bad = block_reduce<BLOCK>(bad, true);
   if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
+  // solve layouts: transposed copy and dense tail blocks
+  double* FTs = FT + size_t(s) * P.nnz_f;
+  for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
+  const int nd = 4 * P.tl * P.tl;
+  double* Ds = D + size_t(s) * nd;
+  for (int q = threadIdx.x; q < nd; q += BLOCK) {
+    const int src = P.dense_src[q];
+    Ds[q] = src >= 0 ? Fs[src] : 0.0;
+  }
 }
 
 // ----------------------------------------------------------- Schur reduction
+__device__ __forceinline__ FactorView factor_of(const DevLu& P, const double* F, const double* FT,
+                                                const double* D, int s) {
+  return FactorView{F + size_t(s) * P.nnz_f, FT + size_t(s) * P.nnz_f,
+                    D + size_t(s) * 4 * P.tl * P.tl};
+}
+
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) reduce_tiles_kernel(ReduceLaunch a) {
+__global__ void __launch_bounds__(BLOCK, 1) reduce_tiles_kernel(ReduceLaunch a) {
   extern __shared__ double sm[];
   const int tile = blockIdx.x, chunk = blockIdx.y;
   const int cta = chunk * gridDim.x + tile;
@@ -145,7 +162,7 @@ __global__ void __launch_bounds__(BLOCK) reduce_tiles_kernel(ReduceLaunch a) {
   for (int i = threadIdx.x; i < n_u * k; i += BLOCK) acc[i] = 0.0;
   const int s_lo = chunk * a.chunk, s_hi = min(a.M, s_lo + a.chunk);
   for (int s = s_lo; s < s_hi; ++s) {
-    const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+    const FactorView F = factor_of(P, a.F, a.FT, a.D, s);
     const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
     const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
     const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
@@ -260,7 +277,7 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
   const DevLu& P = a.lu;
   double* X = in_smem ? sm : scratch + size_t(s) * 2 * n_x;
   double* Z = X + n_x;
-  const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+  const FactorView F = factor_of(P, a.F, a.FT, a.D, s);
   const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
   const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
   const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
@@ -304,7 +321,7 @@ __global__ void __launch_bounds__(BLOCK) recover_state_kernel(RecoverLaunch a, d
   const DevLu& P = a.lu;
   double* X = in_smem ? sm : scratch + size_t(s) * 2 * n_x;
   double* Z = X + n_x;
-  const double* __restrict__ F = a.F + size_t(s) * P.nnz_f;
+  const FactorView F = factor_of(P, a.F, a.FT, a.D, s);
   const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
   const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
   const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
@@ -462,9 +479,9 @@ size_t single_rhs_smem(int n_x) {
 }  // namespace
 
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
-                        int* status, double piv_tol, cudaStream_t st) {
+                        double* FT, double* D, int* status, double piv_tol, cudaStream_t st) {
   if (M <= 0) return;
-  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, status, piv_tol);
+  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol);
   note_launch();
   check_launch("lu_refactor");
 }
@@ -502,11 +519,11 @@ void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
   const size_t smem = reduce_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(reduce_tiles_kernel<kSolveBlock>,
+    cudaFuncSetAttribute(reduce_tiles_kernel<kReduceBlock>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  reduce_tiles_kernel<kSolveBlock><<<dim3(tiles, a.nchunks), kSolveBlock, smem, st>>>(a);
+  reduce_tiles_kernel<kReduceBlock><<<dim3(tiles, a.nchunks), kReduceBlock, smem, st>>>(a);
   note_launch();
   check_launch("reduce_tiles");
 }

@@ -12,14 +12,16 @@ namespace bipm {
 // Batched static-pivot refactor of G_x: F[s] = LU(P G_x[s] P').  status[s]
 // is set to 1 when a pivot falls below piv_tol * max|G_x[s]| (or is not
 // finite), mirroring SingularBlockError (linalg.cpp:69-73).
+// Also writes the transposed copy FT [M][nnz_f] and the dense tail blocks
+// D [M][4 tl tl] used by the solve kernels.
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
-                        int* status, double piv_tol, cudaStream_t st);
+                        double* FT, double* D, int* status, double piv_tol, cudaStream_t st);
 
 struct ReduceLaunch {
   DevLu lu;
   DevCsr gu, kxx, kxu, kuu;
   int n_x, n_u, M;
-  const double *F, *gu_v, *kxx_v, *kxu_v, *kuu_v, *sigma_x;
+  const double *F, *FT, *D, *gu_v, *kxx_v, *kxu_v, *kuu_v, *sigma_x;
   double dw;
   int kc;           // right-hand-side columns per tile
   int chunk;        // scenarios per CTA
@@ -43,7 +45,7 @@ struct RhsLaunch {
   DevLu lu;
   DevCsr gu, kxx, kxu;
   int n_x, n_u, M;
-  const double *F, *gu_v, *kxx_v, *kxu_v, *sigma_x;
+  const double *F, *FT, *D, *gu_v, *kxx_v, *kxu_v, *sigma_x;
   const double *rhat1, *rhat3;  // [M][n_x]
   double dw;
   double* part;  // [M][n_u] per-scenario contributions
@@ -54,7 +56,7 @@ struct RecoverLaunch {
   DevLu lu;
   DevCsr gu, kxx, kxu;
   int n_x, n_u, M;
-  const double *F, *gu_v, *kxx_v, *kxu_v, *sigma_x;
+  const double *F, *FT, *D, *gu_v, *kxx_v, *kxu_v, *sigma_x;
   const double *rhat1, *rhat3, *pu;
   double dw;
   double *px, *py;  // [M][n_x]

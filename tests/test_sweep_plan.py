@@ -1,0 +1,91 @@
+"""Host-side check of the static-pivot LU plan and its solve layouts (no GPU):
+the plan's level schedules, tail split, transposed copy and dense tail maps,
+executed in numpy exactly as the CUDA sweeps execute them
+(paper_2301_04869_b200/csrc/kernels/sweeps.cuh), solve with random factors of
+the plan's own pattern to machine precision against dense triangular solves."""
+import numpy as np
+import pytest
+import scipy.linalg as sl
+
+from conftest import case_path
+from paper_2301_04869_b200 import _native as nat
+
+
+def emulate(p, F):
+    n, nnz_l, nnz_f, t0, tl = p.array("lu_shape")
+    FT = F[p.array("lu_ft_src")]
+    dense = []
+    for b in range(4):
+        src = p.array(f"lu_dense_src{b}")
+        d = np.where(src >= 0, F[np.maximum(src, 0)], 0.0)
+        dense.append(d.reshape(tl, tl).T if tl else np.zeros((0, 0)))  # column-major -> [i, j]
+
+    def level(name, V, x, diag):
+        lp, items, col = p.array(f"lu_{name}_lvl_ptr"), p.array(f"lu_{name}_items"), \
+            p.array(f"lu_{name}_col")
+        items = items.reshape(-1, 4)
+        for lv in range(len(lp) - 1):
+            upd = {}
+            for row, b, e, _ in items[lp[lv]:lp[lv + 1]]:
+                bb = b + (1 if diag else 0)
+                acc = np.dot(V[bb:e], x[col[bb:e]])
+                upd[row] = (x[row] - acc) / V[b] if diag else x[row] - acc
+            for r, v in upd.items():
+                x[r] = v
+
+    def gather(name, V, x, diag):
+        items, col = p.array(f"lu_{name}_tail_items").reshape(-1, 4), p.array(f"lu_{name}_col")
+        for row, b, split, _ in items:
+            bb = b + (1 if diag else 0)
+            x[row] -= np.dot(V[bb:split], x[col[bb:split]])
+
+    def tail(D, x, unit, lower):
+        if tl == 0:
+            return
+        T = np.tril(D) if lower else np.triu(D)
+        if unit:
+            np.fill_diagonal(T, 1.0)
+        x[t0:] = sl.solve_triangular(T, x[t0:], lower=lower, unit_diagonal=unit)
+
+    def solve_L(x):
+        level("sL", F, x, False); gather("sL", F, x, False); tail(dense[0], x, True, True)
+
+    def solve_U(x):
+        tail(dense[2], x, False, False); level("sU", F[nnz_l:], x, True)
+
+    def solve_Ut(x):
+        level("sUt", FT, x, True); gather("sUt", FT, x, True); tail(dense[3], x, False, True)
+
+    def solve_Lt(x):
+        tail(dense[1], x, True, False); level("sLt", FT[nnz_f - nnz_l:], x, False)
+
+    return solve_L, solve_U, solve_Ut, solve_Lt
+
+
+@pytest.mark.parametrize("case", ["case118", "case1354pegase"])
+def test_sweeps_solve_the_factor_pattern(case):
+    p = nat.Problem(case_path(case), 2, 0.05, 0)
+    n, nnz_l, nnz_f, t0, tl = p.array("lu_shape")
+    rng = np.random.default_rng(3)
+    F = rng.uniform(-0.2, 0.2, nnz_f) / 8
+    diag = p.array("lu_diag")
+    F[diag] = rng.uniform(1.0, 2.0, n) * np.sign(rng.uniform(-1, 1, n))
+    # dense L and U from the plan's row layouts
+    L = np.eye(n)
+    lp, lc = p.array("lu_l_ptr"), p.array("lu_l_col")
+    for i in range(n):
+        L[i, lc[lp[i]:lp[i + 1]]] = F[lp[i]:lp[i + 1]]
+    U = np.zeros((n, n))
+    sp, sc = p.array("lu_sU_ptr"), p.array("lu_sU_col")
+    for i in range(n):
+        U[i, sc[sp[i]:sp[i + 1]]] = F[nnz_l + sp[i]:nnz_l + sp[i + 1]]
+    solve_L, solve_U, solve_Ut, solve_Lt = emulate(p, F)
+    b = rng.normal(size=n)
+    for fn, M, lower in ((solve_L, L, True), (solve_U, U, False), (solve_Ut, U.T, True),
+                         (solve_Lt, L.T, False)):
+        x = b.copy()
+        fn(x)
+        ref = sl.solve_triangular(M, b, lower=lower)
+        assert np.abs(x - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+    if case == "case1354pegase":
+        assert tl >= 64  # the separator chain goes to the dense tail
