@@ -166,9 +166,15 @@ int bipm_counters(int64_t out[3]);
  * enabling starts a new window (clears), disabling keeps the totals */
 int bipm_ctx_profile(bipm_ctx* c, int32_t enable);
 int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* count);
+/* debug: clock64 stamps of the reduction phases of CTA (0,0) (16 slots) */
+int bipm_ctx_phase_stamps(bipm_ctx* c, int32_t enable, int64_t out[16]);
 /* out = reduce tile width, scenarios per CTA, chunks, panel-in-smem, nnz(L),
  * nnz(L+U), LU multiply-adds, SM count */
 int bipm_ctx_info(bipm_ctx* c, int64_t out[8]);
+/* factor_dense_sym + solve (linalg.hpp:116, kkt.cpp:965-976): K (n x n,
+ * column-major) shifted by 1e-13 max(1,|K|_inf), Cholesky; *pd = 1 when
+ * positive definite, then rhs is overwritten by K^{-1} rhs */
+int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, int32_t* pd);
 /* whole solve: start + steps until a terminal status */
 int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u);
 

@@ -79,6 +79,8 @@ SIGNATURES = {
     "bipm_ctx_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, _D,
                                             ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_dense_factor_solve": (ctypes.c_int, [ctypes.c_int32, _D, _D, _I]),
+    "bipm_ctx_phase_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -229,6 +231,11 @@ class Context:
                                          ctypes.byref(n)))
         return ms.value, n.value
 
+    def phase_stamps(self, enable: bool):
+        out = (ctypes.c_int64 * 16)()
+        check(lib().bipm_ctx_phase_stamps(self._h, 1 if enable else 0, out))
+        return list(out)
+
     def info(self) -> dict:
         out = (ctypes.c_int64 * 8)()
         check(lib().bipm_ctx_info(self._h, out))
@@ -297,3 +304,12 @@ def counters() -> dict:
     out = (ctypes.c_int64 * 3)()
     check(lib().bipm_counters(out))
     return {"launches": out[0], "h2d_bytes": out[1], "d2h_bytes": out[2]}
+
+
+def dense_factor_solve(K: np.ndarray, b: np.ndarray):
+    """factor_dense_sym + solve on the GPU: (positive_definite, K^{-1} b)."""
+    K = np.ascontiguousarray(np.asarray(K, dtype=np.float64).T)  # column-major
+    x = np.array(b, dtype=np.float64)
+    pd = ctypes.c_int32(0)
+    check(lib().bipm_dense_factor_solve(len(x), dptr(K), dptr(x), ctypes.byref(pd)))
+    return bool(pd.value), x

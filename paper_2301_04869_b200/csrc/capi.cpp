@@ -337,6 +337,22 @@ int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* cou
   });
 }
 
+int bipm_ctx_phase_stamps(bipm_ctx* c, int32_t enable, int64_t out[16]) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    if (out && e.phase.size()) {  // stamps of the previous reduction
+      e.phase.download(reinterpret_cast<long long*>(out), 16, e.st);
+      e.sync();
+    }
+    if (enable) {
+      if (!e.phase.size()) e.phase.resize(16);
+      e.phase.zero(e.st);
+    } else {
+      e.phase.resize(0);
+    }
+  });
+}
+
 int bipm_ctx_info(bipm_ctx* c, int64_t out[8]) {
   return guarded([&] {
     const Engine& e = *c->eng;
@@ -348,6 +364,28 @@ int bipm_ctx_info(bipm_ctx* c, int64_t out[8]) {
     out[5] = e.pb.LU.nnz_f;
     out[6] = (int64_t)e.pb.LU.mul_l.size();
     out[7] = e.sm_count;
+  });
+}
+
+int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, int32_t* pd) {
+  return guarded([&] {
+    cudaStream_t st;
+    cuda_check(cudaStreamCreate(&st), "stream");
+    DArr<double> K, b;
+    DArr<int> info(1);
+    K.upload(k_colmajor, size_t(n) * n, st);
+    b.upload(rhs, size_t(n), st);
+    launch_shift_cholesky(K.get(), n, info.get(), nullptr, st);
+    int inf = 0;
+    info.download(&inf, 1, st);
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    *pd = inf == 0 ? 1 : 0;
+    if (inf == 0) {
+      launch_cholesky_solve(K.get(), n, b.get(), st);
+      b.download(rhs, size_t(n), st);
+      cuda_check(cudaStreamSynchronize(st), "sync");
+    }
+    cudaStreamDestroy(st);
   });
 }
 

@@ -231,6 +231,7 @@ void Engine::reduce_local(double dw) {
   red.dw = dw;
   red.partial = red_partial.get();
   red.scratch = red_scratch.get();
+  red.phase = phase.size() ? phase.get() : nullptr;
   timed("reduce_tiles", [&] { launch_reduce_tiles(red, st); });
 }
 

@@ -90,6 +90,7 @@ class Engine {
   ReduceLaunch red{};
   DArr<double> red_partial, red_scratch, rhs_part;
   DArr<double> khat, rhs;   // n_u x n_u (column-major), n_u
+  DArr<long long> phase;    // optional reduction phase stamps (debug)
   DArr<int> chol_info;
 
   // ---- operators (device-resident inputs/outputs)

@@ -42,16 +42,19 @@ __device__ void block_partial(double (&v)[K], const int (&op)[K], double* partia
   }
 }
 
+// one warp per slot: lane-strided partials, then a fixed xor tree (deterministic)
 template <int K>
 __global__ void finalize_kernel(const double* partial, int nblocks, const int* ops_unused,
                                 double* out, int o0, int o1, int o2, int o3, int o4, int o5,
                                 int o6, int o7) {
   const int ops[8] = {o0, o1, o2, o3, o4, o5, o6, o7};
-  const int k = threadIdx.x;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (k >= K) return;
-  double a = ident(ops[k]);
-  for (int b = 0; b < nblocks; ++b) a = combine(ops[k], a, partial[size_t(b) * K + k]);
-  out[k] = a;
+  const int op = ops[k];
+  double a = ident(op);
+  for (int b = lane; b < nblocks; b += 32) a = combine(op, a, partial[size_t(b) * K + k]);
+  for (int off = 16; off > 0; off >>= 1) a = combine(op, a, __shfl_xor_sync(0xffffffffu, a, off));
+  if (lane == 0) out[k] = a;
 }
 
 template <int K>
@@ -59,7 +62,7 @@ void finalize(const double* partial, int nblocks, const int (&op)[K], double* ou
               cudaStream_t st) {
   int o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   for (int k = 0; k < K; ++k) o[k] = op[k];
-  finalize_kernel<K><<<1, 32, 0, st>>>(partial, nblocks, nullptr, out, o[0], o[1], o[2], o[3],
+  finalize_kernel<K><<<1, 32 * K, 0, st>>>(partial, nblocks, nullptr, out, o[0], o[1], o[2], o[3],
                                        o[4], o[5], o[6], o[7]);
   note_launch();
 }

@@ -26,7 +26,7 @@ namespace bipm {
 namespace {
 
 constexpr int kSolveBlock = 256;   // single right-hand side kernels
-constexpr int kReduceBlock = 1024; // multi-RHS reduction: one CTA per SM, latency hiding
+constexpr int kReduceBlock = 512;  // multi-RHS reduction: one CTA per SM, 128-register budget
 constexpr int kLuBlock = 256;
 constexpr int kDenseBlock = 1024;
 
@@ -145,123 +145,131 @@ __device__ __forceinline__ FactorView factor_of(const DevLu& P, const double* F,
                     D + size_t(s) * 4 * P.tl * P.tl};
 }
 
-template <int BLOCK>
+template <int BLOCK, int K>
 __global__ void __launch_bounds__(BLOCK, 1) reduce_tiles_kernel(ReduceLaunch a) {
   extern __shared__ double sm[];
   const int tile = blockIdx.x, chunk = blockIdx.y;
   const int cta = chunk * gridDim.x + tile;
-  const int j0 = tile * a.kc;
-  const int k = min(a.kc, a.n_u - j0);
-  const int n_x = a.n_x, n_u = a.n_u, ldx = k;
-  const size_t per_cta = size_t(n_x) * a.kc * (a.panel_in_smem ? 1 : 2);
+  const int j0 = tile * K;
+  const int k = min(K, a.n_u - j0);
+  const int n_x = a.n_x, n_u = a.n_u;
+  const size_t per_cta = size_t(n_x) * K * (a.panel_in_smem ? 1 : 2);
   double* acc = sm;
   double* S = a.scratch + size_t(cta) * per_cta;
-  double* X = a.panel_in_smem ? sm + size_t(n_u) * a.kc : S + size_t(n_x) * a.kc;
+  double* X = a.panel_in_smem ? sm + size_t(n_u) * K : S + size_t(n_x) * K;
   const DevLu& P = a.lu;
 
-  for (int i = threadIdx.x; i < n_u * k; i += BLOCK) acc[i] = 0.0;
+  for (int i = threadIdx.x; i < n_u * K; i += BLOCK) acc[i] = 0.0;
   const int s_lo = chunk * a.chunk, s_hi = min(a.M, s_lo + a.chunk);
+  const bool stamp = a.phase && cta == 0 && threadIdx.x == 0;
+  int np = 0;
+  auto mark = [&](int s) {
+    if (stamp && s == s_lo) a.phase[np++] = clock64();
+  };
   for (int s = s_lo; s < s_hi; ++s) {
     const FactorView F = factor_of(P, a.F, a.FT, a.D, s);
+    mark(s);
     const double* __restrict__ gu = a.gu_v + size_t(s) * a.gu.nnz;
     const double* __restrict__ kxx = a.kxx_v + size_t(s) * a.kxx.nnz;
     const double* __restrict__ kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
     const double* __restrict__ kuu = a.kuu_v + size_t(s) * a.kuu.nnz;
     const double* __restrict__ sig = a.sigma_x + size_t(s) * n_x;
 
-    // V = Cartesian columns [j0, j0+k): X = P G_u V
-    for (int i = threadIdx.x; i < n_x * k; i += BLOCK) X[i] = 0.0;
+    // V = Cartesian columns [j0, j0+k): X = P G_u V (columns >= k stay zero)
+    for (int i = threadIdx.x; i < n_x * K; i += BLOCK) X[i] = 0.0;
     __syncthreads();
-    for (int c = 0; c < k; ++c)
-      for (int q = a.gu.t_ptr[j0 + c] + threadIdx.x; q < a.gu.t_ptr[j0 + c + 1]; q += BLOCK)
-        X[P.iperm[a.gu.t_row[q]] * ldx + c] = gu[a.gu.t_slot[q]];
+    {
+      const int q0 = a.gu.t_ptr[j0], q1 = a.gu.t_ptr[j0 + k];
+      for (int q = q0 + threadIdx.x; q < q1; q += BLOCK) {
+        int c = 0;
+        while (a.gu.t_ptr[j0 + c + 1] <= q) ++c;
+        X[P.iperm[a.gu.t_row[q]] * K + c] = gu[a.gu.t_slot[q]];
+      }
+    }
     __syncthreads();
-    // X = G_x^{-1} G_u V  (so T = -X)
-    sweep_L<BLOCK>(P, F, X, k, ldx);
-    sweep_U<BLOCK>(P, F, X, k, ldx);
+    mark(s);
+    // X = G_x^{-1} G_u V, T = -X
+    level_sweep<BLOCK, K, false>(P.sL, F.F, X);
+    mark(s);
+    tail_gather<BLOCK, K, false>(P.sL, F.F, X);
+    mark(s);
+    dense_tail_pair<BLOCK, K, true, false>(P, dense_block(P, F, 0), dense_block(P, F, 2), X);
+    mark(s);
+    level_sweep<BLOCK, K, true>(P.sU, F.F + P.nnz_l, X);
+    mark(s);
 
     // acc += K_xu' T + K_uu V;  S = P (K~_xx T + K_xu V)
-    for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
-      const int u = it / k, c = it % k;
+    for (int it = threadIdx.x; it < n_u * K; it += BLOCK) {
+      const int u = it / K, c = it % K;
       double v = 0.0;
       for (int q = a.kxu.t_ptr[u]; q < a.kxu.t_ptr[u + 1]; ++q)
-        v -= kxu[a.kxu.t_slot[q]] * X[P.iperm[a.kxu.t_row[q]] * ldx + c];
-      const int ku = find_in_row(a.kuu.ptr, a.kuu.ind, u, j0 + c);
-      if (ku >= 0) v += kuu[ku];
+        v -= kxu[a.kxu.t_slot[q]] * X[P.iperm[a.kxu.t_row[q]] * K + c];
+      if (c < k) {
+        const int ku = find_in_row(a.kuu.ptr, a.kuu.ind, u, j0 + c);
+        if (ku >= 0) v += kuu[ku];
+      }
       acc[it] += v;
     }
-    for (int it = threadIdx.x; it < n_x * k; it += BLOCK) {
-      const int p = it / k, c = it % k;
+    for (int it = threadIdx.x; it < n_x * K; it += BLOCK) {
+      const int p = it / K, c = it % K;
       const int i = P.perm[p];
       double v = 0.0;
       for (int t = a.kxx.ptr[i]; t < a.kxx.ptr[i + 1]; ++t)
-        v -= kxx[t] * X[P.iperm[a.kxx.ind[t]] * ldx + c];
-      v -= (sig[i] + a.dw) * X[p * ldx + c];
-      const int ks = find_in_row(a.kxu.ptr, a.kxu.ind, i, j0 + c);
-      if (ks >= 0) v += kxu[ks];
-      S[p * ldx + c] = v;
+        v -= kxx[t] * X[P.iperm[a.kxx.ind[t]] * K + c];
+      v -= (sig[i] + a.dw) * X[p * K + c];
+      if (c < k) {
+        const int ks = find_in_row(a.kxu.ptr, a.kxu.ind, i, j0 + c);
+        if (ks >= 0) v += kxu[ks];
+      }
+      S[p * K + c] = v;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < n_x * k; i += BLOCK) X[i] = S[i];
+    mark(s);
+    for (int i = threadIdx.x; i < n_x * K; i += BLOCK) X[i] = S[i];
     __syncthreads();
     // X = P G_x^{-T} L_x  (Y[perm[p]] = X[p])
-    sweep_Ut<BLOCK>(P, F, X, k, ldx);
-    sweep_Lt<BLOCK>(P, F, X, k, ldx);
+    level_sweep<BLOCK, K, true>(P.sUt, F.FT, X);
+    mark(s);
+    tail_gather<BLOCK, K, true>(P.sUt, F.FT, X);
+    mark(s);
+    dense_tail_pair<BLOCK, K, false, true>(P, dense_block(P, F, 3), dense_block(P, F, 1), X);
+    mark(s);
+    level_sweep<BLOCK, K, false>(P.sLt, F.FT + (P.nnz_f - P.nnz_l), X);
+    mark(s);
     // acc -= G_u' Y
-    for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
-      const int u = it / k, c = it % k;
+    for (int it = threadIdx.x; it < n_u * K; it += BLOCK) {
+      const int u = it / K, c = it % K;
       double v = 0.0;
       for (int q = a.gu.t_ptr[u]; q < a.gu.t_ptr[u + 1]; ++q)
-        v += gu[a.gu.t_slot[q]] * X[P.iperm[a.gu.t_row[q]] * ldx + c];
+        v += gu[a.gu.t_slot[q]] * X[P.iperm[a.gu.t_row[q]] * K + c];
       acc[it] -= v;
     }
     __syncthreads();
+    mark(s);
   }
   double* out = a.partial + size_t(chunk) * n_u * n_u;
-  for (int it = threadIdx.x; it < n_u * k; it += BLOCK) {
-    const int u = it / k, c = it % k;
-    out[size_t(j0 + c) * n_u + u] = acc[it];
+  for (int it = threadIdx.x; it < n_u * K; it += BLOCK) {
+    const int u = it / K, c = it % K;
+    if (c < k) out[size_t(j0 + c) * n_u + u] = acc[it];
   }
 }
 
-__device__ double tree_sum(const double* p, long long stride, int lo, int hi) {
-  // fixed half-split order (executor.hpp:37-59), iterative over a small stack
-  struct Frame { int lo, hi, state; double left; };
-  Frame st[32];
-  int top = 0;
-  st[0] = {lo, hi, 0, 0.0};
-  double ret = 0.0;
-  while (top >= 0) {
-    Frame& f = st[top];
-    if (f.hi - f.lo == 1) {
-      ret = p[f.lo * stride];
-      --top;
-      continue;
-    }
-    const int mid = f.lo + (f.hi - f.lo) / 2;
-    if (f.state == 0) {
-      f.state = 1;
-      st[top + 1] = {f.lo, mid, 0, 0.0};
-      ++top;
-    } else if (f.state == 1) {
-      f.left = ret;
-      f.state = 2;
-      st[top + 1] = {mid, f.hi, 0, 0.0};
-      ++top;
-    } else {
-      ret = f.left + ret;
-      --top;
-    }
-  }
-  return ret;
-}
-
-__global__ void sum_parts_kernel(const double* parts, int nparts, long long len, double* out,
-                                 const double* diag_add, double dw, int n_mat,
+__global__ void sum_parts_kernel(const double* __restrict__ parts, int nparts, long long len,
+                                 double* out, const double* diag_add, double dw, int n_mat,
                                  const double* sub_vec) {
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= len) return;
-  double v = tree_sum(parts + j, len, 0, nparts);
+  // fixed order: four interleaved running sums combined pairwise
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int c = 0;
+  for (; c + 3 < nparts; c += 4) {
+    s0 += parts[(long long)c * len + j];
+    s1 += parts[(long long)(c + 1) * len + j];
+    s2 += parts[(long long)(c + 2) * len + j];
+    s3 += parts[(long long)(c + 3) * len + j];
+  }
+  for (; c < nparts; ++c) s0 += parts[(long long)c * len + j];
+  double v = (s0 + s1) + (s2 + s3);
   if (n_mat > 0 && diag_add && (j % (n_mat + 1)) == 0) v += diag_add[j / (n_mat + 1)] + dw;
   if (sub_vec) v -= sub_vec[j];
   out[j] = v;
@@ -287,8 +295,7 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
 
   for (int p = threadIdx.x; p < n_x; p += BLOCK) X[p] = r3[P.perm[p]];
   __syncthreads();
-  sweep_L<BLOCK>(P, F, X, 1, 1);
-  sweep_U<BLOCK>(P, F, X, 1, 1);  // X = P a
+  solve_LU<BLOCK, 1>(P, F, X);  // X = P a
   // Z = P (rhat1 - K~ a)
   for (int p = threadIdx.x; p < n_x; p += BLOCK) {
     const int i = P.perm[p];
@@ -299,8 +306,7 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
     Z[p] = v;
   }
   __syncthreads();
-  sweep_Ut<BLOCK>(P, F, Z, 1, 1);
-  sweep_Lt<BLOCK>(P, F, Z, 1, 1);
+  solve_LUt<BLOCK, 1>(P, F, Z);
   double* out = a.part + size_t(s) * a.n_u;
   for (int u = threadIdx.x; u < a.n_u; u += BLOCK) {
     double v = 0.0;
@@ -339,8 +345,7 @@ __global__ void __launch_bounds__(BLOCK) recover_state_kernel(RecoverLaunch a, d
     X[p] = r3[i] + 1.0 * acc;
   }
   __syncthreads();
-  sweep_L<BLOCK>(P, F, X, 1, 1);
-  sweep_U<BLOCK>(P, F, X, 1, 1);
+  solve_LU<BLOCK, 1>(P, F, X);
   for (int p = threadIdx.x; p < n_x; p += BLOCK) {
     X[p] = -X[p];
     px[P.perm[p]] = X[p];
@@ -358,8 +363,7 @@ __global__ void __launch_bounds__(BLOCK) recover_state_kernel(RecoverLaunch a, d
     Z[p] = v + 1.0 * au;
   }
   __syncthreads();
-  sweep_Ut<BLOCK>(P, F, Z, 1, 1);
-  sweep_Lt<BLOCK>(P, F, Z, 1, 1);
+  solve_LUt<BLOCK, 1>(P, F, Z);
   for (int p = threadIdx.x; p < n_x; p += BLOCK) py[P.perm[p]] = -Z[p];
 }
 
@@ -403,6 +407,97 @@ __global__ void condense_kernel(CondenseDev c, int M, const double* __restrict__
   for (int t = c.ptr[o]; t < c.ptr[o + 1]; ++t)
     v = __dadd_rn(v, __dmul_rn(__dmul_rn(As[c.ka[t]], Ss[c.r[t]]), Bs[c.kb[t]]));
   out[size_t(s) * c.nout + o] = v;
+}
+
+// ------------------------------------------------ dense Cholesky, n <= 150
+// The whole matrix in shared memory; right-looking by columns (LAPACK dpotrf
+// semantics: fail at the first pivot that is not > 0 or is NaN).
+constexpr int kSmallChol = 150;
+
+__global__ void __launch_bounds__(kDenseBlock) shift_cholesky_small_kernel(double* K, int n,
+                                                                          int* info) {
+  extern __shared__ double A[];  // n x n column-major
+  __shared__ int fail;
+  double mx = 0.0;
+  for (int i = threadIdx.x; i < n * n; i += kDenseBlock) {
+    const double v = K[i];
+    A[i] = v;
+    mx = fmax(mx, fabs(v));
+  }
+  mx = block_reduce<kDenseBlock>(mx, true);
+  const double shift = 1e-13 * fmax(1.0, mx);
+  for (int i = threadIdx.x; i < n; i += kDenseBlock) A[i * n + i] += shift;
+  if (threadIdx.x == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double ajj = A[j * n + j];
+      if (!(ajj > 0.0) || isnan(ajj))
+        fail = j + 1;
+      else
+        A[j * n + j] = sqrt(ajj);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ljj = A[j * n + j];
+    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) A[j * n + i] /= ljj;
+    __syncthreads();
+    // trailing update of the lower triangle: A(i,k) -= L(i,j) L(k,j), j < k <= i
+    const int m = n - j - 1;
+    for (int t = threadIdx.x; t < m * m; t += kDenseBlock) {
+      const int kk = t / m, ii = t - kk * m;  // column kk, row ii of the trailing block
+      if (ii < kk) continue;
+      const int k = j + 1 + kk, i = j + 1 + ii;
+      A[k * n + i] -= A[j * n + i] * A[j * n + k];
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n * n; i += kDenseBlock) K[i] = A[i];
+  if (threadIdx.x == 0) *info = fail;
+}
+
+// L L' x = b for column-major lower L: one warp, x in registers (row i on
+// lane i % 32), pivot broadcast by shuffle.
+template <int NQ>
+__global__ void cholesky_solve_warp_kernel(const double* __restrict__ L, int n, double* b) {
+  const int lane = threadIdx.x & 31;
+  double x[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) x[q] = (q * 32 + lane < n) ? b[q * 32 + lane] : 0.0;
+  // forward: L y = b
+#pragma unroll
+  for (int qj = 0; qj < NQ; ++qj) {
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = qj * 32 + jj;
+      if (j >= n) break;
+      const double* __restrict__ col = L + size_t(j) * n;
+      if (lane == jj) x[qj] /= col[j];
+      const double xj = __shfl_sync(0xffffffffu, x[qj], jj);
+#pragma unroll
+      for (int q = qj; q < NQ; ++q) {
+        const int i = q * 32 + lane;
+        if (i > j && i < n) x[q] -= col[i] * xj;
+      }
+    }
+  }
+  // backward: L' x = y, column-oriented over rows of L
+#pragma unroll
+  for (int qj = NQ - 1; qj >= 0; --qj) {
+    for (int jj = 31; jj >= 0; --jj) {
+      const int j = qj * 32 + jj;
+      if (j >= n) continue;
+      if (lane == jj) x[qj] /= L[size_t(j) * n + j];
+      const double xj = __shfl_sync(0xffffffffu, x[qj], jj);
+#pragma unroll
+      for (int q = 0; q <= qj; ++q) {
+        const int i = q * 32 + lane;
+        if (i < j) x[q] -= L[size_t(i) * n + j] * xj;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q)
+    if (q * 32 + lane < n) b[q * 32 + lane] = x[q];
 }
 
 // ---------------------------------------------------------- dense Cholesky
@@ -488,14 +583,18 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
 
 void plan_reduce_launch(ReduceLaunch& a, int smem_budget, int sm_count) {
   // widest tile (<= 32 columns) whose accumulator and panel fit on chip
-  int kc = 32;
-  while (kc > 1 && size_t(a.n_x + a.n_u) * kc * sizeof(double) > size_t(smem_budget)) --kc;
+  // widest power-of-two tile (<= 32 columns, <= n_u rounded up) whose
+  // accumulator and panel fit on chip
+  int cap = 1;
+  while (cap < 32 && cap < a.n_u) cap *= 2;
+  int kc = cap;
+  while (kc > 1 && size_t(a.n_x + a.n_u) * kc * sizeof(double) > size_t(smem_budget)) kc /= 2;
   a.panel_in_smem = size_t(a.n_x + a.n_u) * kc * sizeof(double) <= size_t(smem_budget);
   if (!a.panel_in_smem) {
-    kc = 32;
-    while (kc > 1 && size_t(a.n_u) * kc * sizeof(double) > size_t(smem_budget)) --kc;
+    kc = cap;
+    while (kc > 1 && size_t(a.n_u) * kc * sizeof(double) > size_t(smem_budget)) kc /= 2;
   }
-  a.kc = std::min(kc, a.n_u);
+  a.kc = kc;
   const int tiles = (a.n_u + a.kc - 1) / a.kc;
   const int per_sm = std::max(1, int(smem_budget / std::max<size_t>(1, reduce_smem_bytes(a))));
   int nchunks = std::max(1, (4 * sm_count * std::min(per_sm, 4) + tiles - 1) / tiles);
@@ -513,18 +612,30 @@ size_t reduce_scratch_doubles(const ReduceLaunch& a) {
   return size_t(tiles) * a.nchunks * a.n_x * a.kc * (a.panel_in_smem ? 1 : 2);
 }
 
-void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
-  if (a.M <= 0) return;
-  const int tiles = (a.n_u + a.kc - 1) / a.kc;
+template <int K>
+void launch_reduce_k(const ReduceLaunch& a, cudaStream_t st) {
+  const int tiles = (a.n_u + K - 1) / K;
   const size_t smem = reduce_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(reduce_tiles_kernel<kReduceBlock>,
+    cudaFuncSetAttribute(reduce_tiles_kernel<kReduceBlock, K>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  reduce_tiles_kernel<kReduceBlock><<<dim3(tiles, a.nchunks), kReduceBlock, smem, st>>>(a);
+  reduce_tiles_kernel<kReduceBlock, K><<<dim3(tiles, a.nchunks), kReduceBlock, smem, st>>>(a);
   note_launch();
+}
+
+void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
+  if (a.M <= 0) return;
+  switch (a.kc) {
+    case 1: launch_reduce_k<1>(a, st); break;
+    case 2: launch_reduce_k<2>(a, st); break;
+    case 4: launch_reduce_k<4>(a, st); break;
+    case 8: launch_reduce_k<8>(a, st); break;
+    case 16: launch_reduce_k<16>(a, st); break;
+    default: launch_reduce_k<32>(a, st); break;
+  }
   check_launch("reduce_tiles");
 }
 
@@ -611,13 +722,30 @@ void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, cons
 }
 
 void launch_shift_cholesky(double* K, int n, int* info, double*, cudaStream_t st) {
-  shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
+  if (n <= kSmallChol) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(shift_cholesky_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      attr_set = true;
+    }
+    shift_cholesky_small_kernel<<<1, kDenseBlock, size_t(n) * n * sizeof(double), st>>>(K, n, info);
+  } else {
+    shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
+  }
   note_launch();
   check_launch("shift_cholesky");
 }
 
 void launch_cholesky_solve(const double* L, int n, double* b, cudaStream_t st) {
-  cholesky_solve_kernel<<<1, kDenseBlock, 0, st>>>(L, n, b);
+  if (n <= 64)
+    cholesky_solve_warp_kernel<2><<<1, 32, 0, st>>>(L, n, b);
+  else if (n <= 128)
+    cholesky_solve_warp_kernel<4><<<1, 32, 0, st>>>(L, n, b);
+  else if (n <= 256)
+    cholesky_solve_warp_kernel<8><<<1, 32, 0, st>>>(L, n, b);
+  else
+    cholesky_solve_kernel<<<1, kDenseBlock, 0, st>>>(L, n, b);
   note_launch();
   check_launch("cholesky_solve");
 }

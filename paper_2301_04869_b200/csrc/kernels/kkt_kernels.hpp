@@ -29,6 +29,7 @@ struct ReduceLaunch {
   bool panel_in_smem;
   double* partial;  // [nchunks][n_u * n_u] column-major
   double* scratch;  // per-CTA L_x staging (+ panel when not in shared memory)
+  long long* phase; // optional: clock64 stamps of CTA (0,0), first scenario (16 slots)
 };
 void plan_reduce_launch(ReduceLaunch& a, int smem_budget_bytes, int sm_count);
 size_t reduce_scratch_doubles(const ReduceLaunch& a);

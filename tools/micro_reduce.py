@@ -1,0 +1,38 @@
+"""Micro-benchmark of the Schur reduction alone (CUDA-event kernel time) on a
+case's real patterns with seeded synthetic values.
+Usage: python tools/micro_reduce.py case N [reps]"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from paper_2301_04869_b200 import _native as nat  # noqa: E402
+from test_gpu_kkt import synthetic_condensed  # noqa: E402
+
+case, N = sys.argv[1], int(sys.argv[2])
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
+p = nat.Problem(os.path.join(ROOT, "paper_2301_04869_b200/data", case + ".m"), N, 0.05, 0)
+v = synthetic_condensed(p, N, seed=7)
+ctx = nat.Context(p)
+ctx.factor_gx(v["gx"])
+args = {k: v[k] for k in v if k != "gx"}
+ctx.reduce(0.5, **args)  # warm
+ctx.profile(True)
+for _ in range(reps):
+    ctx.reduce(0.5, **args)
+ctx.factor_gx(v["gx"])
+out = {g: ctx.kernel_time(g) for g in ("reduce_tiles", "reduce_rhs", "lu_refactor")}
+ctx.profile(False)
+print(json.dumps({"case": case, "N": N, "info": ctx.info(), "tl": int(p.array("lu_shape")[4]),
+                  "ms_per_call": {g: (t / max(1, n)) for g, (t, n) in out.items()}}))
+
+# phase breakdown of CTA (0,0), first scenario (clock64 cycles)
+ctx.phase_stamps(True)
+ctx.reduce(0.5, **args)
+st = ctx.phase_stamps(True)
+names = ["scatter", "L-levels", "L-tailgather", "tail L+U", "U-levels", "spmv", "Ut-levels",
+         "Ut-tailgather", "tail Ut+Lt", "Lt-levels", "GuY"]
+d = [st[i + 1] - st[i] for i in range(len(names)) if st[i + 1] > 0]
+print(json.dumps({"phase_cycles": dict(zip(names, d)), "total": st[len(d)] - st[0]}))
