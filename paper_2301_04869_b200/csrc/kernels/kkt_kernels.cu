@@ -619,7 +619,7 @@ void launch_reduce_k(const ReduceLaunch& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(reduce_tiles_kernel<kReduceBlock, K>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
   reduce_tiles_kernel<kReduceBlock, K><<<dim3(tiles, a.nchunks), kReduceBlock, smem, st>>>(a);
@@ -666,7 +666,7 @@ void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(reduce_rhs_kernel<kSolveBlock>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
   reduce_rhs_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
@@ -690,7 +690,7 @@ void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(recover_state_kernel<kSolveBlock>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr_set = true;
   }
   recover_state_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
@@ -723,12 +723,8 @@ void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, cons
 
 void launch_shift_cholesky(double* K, int n, int* info, double*, cudaStream_t st) {
   if (n <= kSmallChol) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(shift_cholesky_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
-      attr_set = true;
-    }
+    cudaFuncSetAttribute(shift_cholesky_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(size_t(n) * n * sizeof(double)));
     shift_cholesky_small_kernel<<<1, kDenseBlock, size_t(n) * n * sizeof(double), st>>>(K, n, info);
   } else {
     shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
