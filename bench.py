@@ -153,10 +153,12 @@ def bench_ours(a, rank, world):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    from paper_2301_04869_b200.distributed import sharded_context
     case_file = os.path.join(DATA_DIR, a.case + ".m")
     workload = f"{a.case}_N{a.scenarios}"
     p = nat.Problem(case_file, a.scenarios, a.sigma, a.seed)
-    ctx = nat.Context(p, device=dev)
+    # one scenario group per GPU; K_hat / rhs / norms all-reduced over NCCL
+    ctx = sharded_context(p, world, rank, device=dev, backend="nccl")
     info = ctx.info()
     solver = nat.Solver(ctx)
     solver.start()
@@ -196,7 +198,7 @@ def bench_ours(a, rank, world):
     h0 = nat.counters()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ctx2 = nat.Context(p, device=dev)
+    ctx2 = sharded_context(p, world, rank, device=dev, backend="nccl")
     res = nat.Solver(ctx2).solve()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -206,7 +208,8 @@ def bench_ours(a, rank, world):
     dom = max(kt, key=lambda g: kt[g][0])
     dom_ms, dom_n = kt[dom]
     peak, peak_kind = peaks()
-    algo = algorithmic_bytes(p, info, dom, a.scenarios)
+    M_local = ctx.hi - ctx.lo
+    algo = algorithmic_bytes(p, info, dom, M_local)
     achieved = (algo / (dom_ms / dom_n * 1e-3)) / 1e9 if dom_n else 0.0
     line = {
         "metric": METRIC, "value": round(ms_per_step, 4), "unit": "ms/iteration",
@@ -217,7 +220,8 @@ def bench_ours(a, rank, world):
                 f"N={a.scenarios} load scenarios N(1,{a.sigma}^2) seed {a.seed}",
         "config": {"workload": workload, "case": a.case, "scenarios": a.scenarios,
                    "sigma": a.sigma, "seed": a.seed,
-                   "parallelism": "1 GPU" if world == 1 else f"replicas x{world}",
+                   "parallelism": "1 GPU" if world == 1 else
+                   f"dp{world}: scenario groups per GPU, NCCL all-reduce of K_hat/rhs/norms",
                    "step": "one IPM iteration (iterations warmup.. of a fresh solve)",
                    "l2": "flushed (256 MiB write) before every timed iteration"},
         "total_solve_s": round(res["t_total"], 5), "iterations": res["iterations"],

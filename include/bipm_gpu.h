@@ -122,6 +122,20 @@ int bipm_eval_bundle(bipm_ctx* c, const double* X, const double* u, const double
 int bipm_eval_values(bipm_ctx* c, const double* X, const double* u, double* f, double* g,
                      double* h, int32_t* bad_block);
 
+/* ---- multi-GPU: one bipm_ctx per GPU owning a contiguous scenario group
+ * (partition, executor.cpp:7-19).  The reduced matrix / rhs partial sums and
+ * the scalar norms are all-reduced (all_reduce_sum, executor.cpp:39-61). */
+/* ranges[2g], ranges[2g+1] = [lo, hi) of group g: sizes differ by at most
+ * one, leading groups take the extra scenario */
+int bipm_partition(int32_t N, int32_t G, int32_t* ranges);
+/* NCCL (loaded with dlopen): rank 0 creates the id, every rank joins */
+int bipm_nccl_unique_id(uint8_t out[128]);
+int bipm_ctx_set_nccl(bipm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank);
+/* host-staged exchange through a callback (op: 0 sum, 1 max, 2 min, in place) */
+typedef void (*bipm_allreduce_fn)(void* user, double* buf, int64_t n, int32_t op);
+int bipm_ctx_set_host_comm(bipm_ctx* c, bipm_allreduce_fn fn, void* user, int32_t nranks,
+                           int32_t rank);
+
 /* ---- interior-point driver (ipm.cpp:435-664 on the reduced strategy) ---- */
 typedef struct bipm_solver bipm_solver;
 

@@ -80,6 +80,11 @@ SIGNATURES = {
                                             ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_info": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
     "bipm_dense_factor_solve": (ctypes.c_int, [ctypes.c_int32, _D, _D, _I]),
+    "bipm_partition": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, _I]),
+    "bipm_nccl_unique_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint8)]),
+    "bipm_ctx_set_nccl": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_uint8), ctypes.c_int32,
+                                         ctypes.c_int32]),
+    "bipm_ctx_set_host_comm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32]),
     "bipm_ctx_phase_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
 }
 
@@ -119,6 +124,22 @@ class _Condensed(ctypes.Structure):
 
 class _Bundle(ctypes.Structure):
     _fields_ = [(n, _D) for n in BUNDLE_FIELDS]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, _D, ctypes.c_int64, ctypes.c_int32)
+
+
+def partition(N: int, G: int):
+    """Contiguous scenario groups (executor.cpp:7-19) as [(lo, hi)] * G."""
+    out = (ctypes.c_int32 * (2 * G))()
+    check(lib().bipm_partition(N, G, out))
+    return [(out[2 * g], out[2 * g + 1]) for g in range(G)]
+
+
+def nccl_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    check(lib().bipm_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 class _SolveOptions(ctypes.Structure):
@@ -221,6 +242,18 @@ class Context:
         check(lib().bipm_eval_values(self._h, dptr(X), dptr(u), dptr(f), dptr(g), dptr(h),
                                      ctypes.byref(bad)))
         return f, g, h
+
+    def set_nccl(self, uid: bytes, nranks: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        check(lib().bipm_ctx_set_nccl(self._h, buf, nranks, rank))
+
+    def set_host_comm(self, allreduce, nranks: int, rank: int):
+        """allreduce(np.ndarray view, op) with op 0 sum / 1 max / 2 min, in place."""
+        def cb(_user, buf, n, op):
+            allreduce(np.ctypeslib.as_array(buf, shape=(n,)), op)
+        self._cb = ALLREDUCE_FN(cb)  # keep alive
+        check(lib().bipm_ctx_set_host_comm(self._h, ctypes.cast(self._cb, ctypes.c_void_p), None,
+                                           nranks, rank))
 
     def profile(self, enable: bool = True):
         check(lib().bipm_ctx_profile(self._h, 1 if enable else 0))

@@ -389,6 +389,36 @@ int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, in
   });
 }
 
+int bipm_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] { nccl_unique_id(out); });
+}
+
+int bipm_ctx_set_nccl(bipm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank) {
+  return guarded([&] { c->eng->comm = make_nccl_comm(id, nranks, rank, c->eng->device); });
+}
+
+int bipm_ctx_set_host_comm(bipm_ctx* c, bipm_allreduce_fn fn, void* user, int32_t nranks,
+                           int32_t rank) {
+  return guarded([&] {
+    if (!fn) throw Error(kInvalidArgument, "null all-reduce callback");
+    c->eng->comm = make_host_comm(fn, user, nranks, rank);
+  });
+}
+
+int bipm_partition(int32_t N, int32_t G, int32_t* ranges) {
+  return guarded([&] {
+    if (G < 1 || G > N) throw Error(kInvalidArgument, "partition: need 1 <= G <= N");
+    const int32_t base = N / G, rem = N % G;
+    int32_t lo = 0;
+    for (int32_t g = 0; g < G; ++g) {
+      const int32_t sz = base + (g < rem ? 1 : 0);
+      ranges[2 * g] = lo;
+      ranges[2 * g + 1] = lo + sz;
+      lo += sz;
+    }
+  });
+}
+
 int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u) {
   return guarded([&] {
     Solver s(*c->eng, to_options(opts));

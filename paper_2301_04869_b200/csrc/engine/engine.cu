@@ -258,12 +258,21 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   a.part = rhs_part.get();
   timed("reduce_rhs", [&] { launch_reduce_rhs(a, st); });
   launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st);
+  if (multi()) comm->allreduce(d_out, size_t(pb.M.n_u), RedOpKind::kSum, st);
 }
 
 void Engine::finish_reduce(double dw) {
   const int n_u = pb.M.n_u;
-  launch_sum_parts(red_partial.get(), red.nchunks, (long long)n_u * n_u, khat.get(),
-                   sigma_u.get(), dw, n_u, nullptr, st);
+  const long long nn = (long long)n_u * n_u;
+  if (!multi()) {
+    launch_sum_parts(red_partial.get(), red.nchunks, nn, khat.get(), sigma_u.get(), dw, n_u,
+                     nullptr, st);
+    return;
+  }
+  // local sum -> all-reduce over the scenario groups -> diagonal terms once
+  launch_sum_parts(red_partial.get(), red.nchunks, nn, khat.get(), nullptr, 0.0, 0, nullptr, st);
+  comm->allreduce(khat.get(), size_t(nn), RedOpKind::kSum, st);
+  launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st);
 }
 
 bool Engine::factor_khat() {

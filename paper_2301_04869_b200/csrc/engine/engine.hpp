@@ -17,6 +17,7 @@
 #include "../host/plan.hpp"
 #include "../kernels/ad_launch.hpp"
 #include "../kernels/kkt_kernels.hpp"
+#include "comm.hpp"
 #include "device_array.hpp"
 
 namespace bipm {
@@ -55,6 +56,8 @@ class Engine {
 
   const Problem& pb;
   const idx lo, hi, M;
+  std::unique_ptr<Comm> comm;  // null: single GPU (no exchange)
+  bool multi() const { return comm && comm->size() > 1; }
   int device = 0, sm_count = 148;
   cudaStream_t st = nullptr;
 
@@ -112,7 +115,8 @@ class Engine {
   // rhs of the reduced system from (rhat1, rhat3) (defaults: the engine's)
   void reduce_rhs_local(double delta_w, double* d_rhs_out, const double* d_rhat1 = nullptr,
                         const double* d_rhat3 = nullptr);
-  // finish_reduce (kkt.cpp:468-488) for a single engine
+  // finish_reduce (kkt.cpp:468-488): K_hat = sum of the partial tiles (all
+  // ranks) + diag(sigma_u + delta_w)
   void finish_reduce(double delta_w);
   // shift + Cholesky (kkt.cpp:965-971); true when positive definite
   bool factor_khat();

@@ -71,6 +71,8 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
   c_rhat2.resize(nu);
   rhs_sum.resize(nu);
   pu_rhs.resize(nu);
+  red_u.resize(nu);
+  dd_u.resize(2 * nu);
   ft.resize(size_t(d.M));
   gt.resize(nx);
   ht.resize(nm);
@@ -104,6 +106,24 @@ std::array<double, K> Solver::fetch(const double* dptr) {
 
 double Solver::fetch1(const double* dptr) { return fetch<1>(dptr)[0]; }
 
+void Solver::allred(double* dptr, size_t n, RedOpKind op) {
+  if (e.multi()) e.comm->allreduce(dptr, n, op, e.st);
+}
+
+double Solver::host_all(double v, RedOpKind op) {
+  if (!e.multi()) return v;
+  double* slot = scal.get() + 30;
+  cuda_check(cudaMemcpyAsync(slot, &v, sizeof(double), cudaMemcpyHostToDevice, e.st), "h2d");
+  e.comm->allreduce(slot, 1, op, e.st);
+  return fetch1(slot);
+}
+
+idx Solver::global_first_bad(idx local_bad) {
+  if (!e.multi()) return local_bad;
+  const double v = host_all(local_bad >= 0 ? double(local_bad) : 1e300, RedOpKind::kMin);
+  return v < 1e299 ? idx(v) : -1;
+}
+
 DevStep Solver::step_view(DArr<double>* s) {
   return DevStep{s[0].get(), s[1].get(), s[2].get(), s[3].get(), s[4].get()};
 }
@@ -113,8 +133,12 @@ Solver::Scaled Solver::scaled_error(const DevIter& it, Engine::Bundle& bd, doubl
   launch_kkt_error_xs(d, it, b, bd.grad.get(), bd.g.get(), bd.h.get(), mu_, partial.get(), sc,
                       e.st);
   launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
+  allred(gsum_u.get(), size_t(d.n_u), RedOpKind::kSum);
   launch_kkt_error_u(d, it, b, gsum_u.get(), mu_, sc + 8, e.st);
   launch_scenario_sum(d.M, 1, bd.f.get(), nullptr, sc + 11, e.st);
+  allred(sc, 5, RedOpKind::kMax);   // x/s norms and complementarity
+  allred(sc + 5, 1, RedOpKind::kSum);  // multiplier sum (x/s part)
+  allred(sc + 11, 1, RedOpKind::kSum);  // objective
   const auto v = fetch<12>(sc);
   objective = v[11];
   const double stat = std::max({v[0], v[1], v[8]});
@@ -153,7 +177,7 @@ void Solver::start() {
   s.lup.upload(lup);
   launch_init_x(d, cur(), b, dx0.get(), o.mu0, e.st);
   if (d.m > 0) {
-    const idx bad = e.eval_values(s.x.get(), s.u.get(), ft.get(), gt.get(), ht.get());
+    const idx bad = global_first_bad(e.eval_values(s.x.get(), s.u.get(), ft.get(), gt.get(), ht.get()));
     if (bad >= 0) throw Error(kNonFinite, "non-finite basis output at the start point", bad);
     launch_init_slacks(d, cur(), b, ht.get(), o.mu0, e.st);
   }
@@ -183,6 +207,7 @@ bool Solver::attempt(double dw, const DevIter& it) {
   // refinement against the unreduced augmented system (kkt.cpp:988-999)
   launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
                    scal.get() + 20, e.st);
+  allred(scal.get() + 20, 1, RedOpKind::kMax);
   const double scale = fetch1(scal.get() + 20);
   const DerivPlan& D = e.pb.D;
   (void)D;
@@ -219,7 +244,14 @@ bool Solver::attempt(double dw, const DevIter& it) {
     a.o4 = o4.get();
     a.o1u_part = o1u_part.get();
     launch_aug_residual(a, partial.get(), scal.get() + 21, e.st);
-    launch_aug_residual_u(a, o1u.get(), scal.get() + 22, e.st);
+    if (e.multi()) {
+      allred(scal.get() + 21, 1, RedOpKind::kMax);
+      launch_aug_residual_u_local(a, dd_u.get(), e.st);
+      allred(dd_u.get(), 2 * size_t(d.n_u), RedOpKind::kSum);
+      launch_aug_residual_u_finish(a, dd_u.get(), o1u.get(), scal.get() + 22, e.st);
+    } else {
+      launch_aug_residual_u(a, o1u.get(), scal.get() + 22, e.st);
+    }
     const auto v = fetch<2>(scal.get() + 21);
     const double rel = std::max(v[0], v[1]) / scale;
     if (rel <= 1e-12) break;
@@ -227,7 +259,7 @@ bool Solver::attempt(double dw, const DevIter& it) {
     // substitute_rhs (kkt.cpp:342-358): re-condense only the rhs from rho
     launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
                          o4.get(), o2.get(), o1x.get(), c_rhat1.get(), rhat2_part.get(), e.st);
-    launch_scenario_sum(d.M, d.n_u, rhat2_part.get(), o1u.get(), c_rhat2.get(), e.st);
+    condensed_u_sum(rhat2_part.get(), o1u.get(), c_rhat2.get());
     e.reduce_rhs_local(dw, rhs_sum.get(), c_rhat1.get(), o3.get());
     launch_pu_rhs(d.n_u, rhs_sum.get(), c_rhat2.get(), q[1].get(), false, e.st);
     e.solve_khat(q[1].get());
@@ -242,6 +274,7 @@ void Solver::compute_step(const DevIter& it) {
   Engine::Bundle& bd = e.bd();
   flag.zero(e.st);
   launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
+  allred(gsum_u.get(), size_t(d.n_u), RedOpKind::kSum);
   launch_assemble_xs(d, it, b, bd.grad.get(), bd.h.get(), mu, e.sigma_x.get(), r1x.get(),
                      e.sigma_s.get(), e.r2.get(), e.r4.get(), flag.get(), e.st);
   launch_assemble_u(d, it, b, gsum_u.get(), mu, e.sigma_u.get(), r1u.get(), flag.get(), e.st);
@@ -251,12 +284,12 @@ void Solver::compute_step(const DevIter& it) {
   e.condense_blocks();
   launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
                        e.r4.get(), e.r2.get(), r1x.get(), e.rhat1.get(), rhat2_part.get(), e.st);
-  launch_scenario_sum(d.M, d.n_u, rhat2_part.get(), r1u.get(), e.rhat2.get(), e.st);
+  condensed_u_sum(rhat2_part.get(), r1u.get(), e.rhat2.get());
   int fl = 0;
   flag.download(&fl, 1, e.st);
   e.sync();
-  if (fl) throw Error(kNonInterior, "iterate not strictly interior");
-  const idx sing = e.factor_gx();
+  if (host_all(double(fl), RedOpKind::kMax) > 0) throw Error(kNonInterior, "iterate not strictly interior");
+  const idx sing = global_first_bad(e.factor_gx());
   if (sing >= 0)
     throw Error(kSingularBlock,
                 "singular block " + std::to_string(sing) +
@@ -291,7 +324,7 @@ int Solver::step() {
   DevIter it = cur();
   if (!bundle_fresh) {
     const double ta = now();
-    const idx bad = e.eval_bundle(e.bd(), it.x, it.u, it.y, it.z, 1.0);
+    const idx bad = global_first_bad(e.eval_bundle(e.bd(), it.x, it.u, it.y, it.z, 1.0));
     if (bad >= 0) throw Error(kNonFinite, "non-finite basis output", bad);
     log.t_ad += now() - ta;
   }
@@ -335,6 +368,7 @@ int Solver::step() {
   DevBoundStep bs{bsv[0].get(), bsv[1].get(), bsv[2].get(), bsv[3].get(), bsv[4].get(), bsv[5].get()};
   const DevStep ps = step_view(p);
   launch_bound_steps(d, it, b, ps, mu, o.tau, bs, partial.get(), scal.get(), e.st);
+  allred(scal.get(), 2, RedOpKind::kMin);
   const auto caps = fetch<2>(scal.get());
   const double ap = std::min(1.0, caps[0]), ad = std::min(1.0, caps[1]);
 
@@ -345,7 +379,7 @@ int Solver::step() {
     DevIter tr = alt();
     launch_apply_step(d, it, tr, b, ps, bs, ap, ad, mu, e.st);
     const double ta = now();
-    const idx bad = e.eval_bundle(e.trial(), tr.x, tr.u, tr.y, tr.z, 1.0);
+    const idx bad = global_first_bad(e.eval_bundle(e.trial(), tr.x, tr.u, tr.y, tr.z, 1.0));
     double theta1 = kInf;
     const bool ok = bad < 0;
     if (ok) theta1 = scaled_error(tr, e.trial(), mu).total;
@@ -367,6 +401,9 @@ int Solver::step() {
   launch_merit(d, it, b, ps, bd.grad.get(), bd.f.get(), bd.g.get(), bd.h.get(), e.gx_p.v,
                e.gu_p.v, e.hx_p.v, e.hu_p.v, bd.gx.get(), bd.gu.get(), bd.hx.get(), bd.hu.get(),
                mu, partial.get(), scal.get(), e.st);
+  allred(scal.get(), 1, RedOpKind::kSum);
+  allred(scal.get() + 1, 2, RedOpKind::kMax);
+  allred(scal.get() + 3, 5, RedOpKind::kSum);
   launch_merit_u(d, it, b, p[1].get(), mu, scal.get() + 8, e.st);
   const auto mv = fetch<10>(scal.get());
   const double viol0 = mv[0];
@@ -383,10 +420,11 @@ int Solver::step() {
   for (int ls = 0; ls < 60; ++ls) {
     launch_primal_trial(d, it, tr, ps, alpha, e.st);
     const double ta = now();
-    const idx bad = e.eval_values(tr.x, tr.u, ft.get(), gt.get(), ht.get());
+    const idx bad = global_first_bad(e.eval_values(tr.x, tr.u, ft.get(), gt.get(), ht.get()));
     if (bad < 0) {
       launch_ls_values(d, tr, b, ft.get(), gt.get(), ht.get(), partial.get(), scal.get() + 12,
                        e.st);
+      allred(scal.get() + 12, 3, RedOpKind::kSum);
       launch_merit_u(d, tr, b, nullptr, mu, scal.get() + 15, e.st);
       const auto w = fetch<5>(scal.get() + 12);
       log.t_ad += now() - ta;
@@ -427,6 +465,17 @@ double Solver::step_timed(int* st_out) {
   cudaEventDestroy(z);
   if (st_out) *st_out = s;
   return ms;
+}
+
+// base + sum over scenarios of part (and over ranks when sharded)
+void Solver::condensed_u_sum(const double* part, const double* base, double* out) {
+  if (!e.multi()) {
+    launch_scenario_sum(d.M, d.n_u, part, base, out, e.st);
+    return;
+  }
+  launch_scenario_sum(d.M, d.n_u, part, nullptr, red_u.get(), e.st);
+  allred(red_u.get(), size_t(d.n_u), RedOpKind::kSum);
+  launch_scenario_sum(1, d.n_u, red_u.get(), base, out, e.st);
 }
 
 int Solver::solve() {

@@ -76,6 +76,11 @@ class Solver {
   bool attempt(double dw, const DevIter& it);  // one inertia-loop attempt (kkt.cpp:954-1001)
   void compute_step(const DevIter& it);         // solve_reduced (kkt.cpp:945-1006)
   double fetch1(const double* d);
+  // cross-rank exchange (no-ops on a single GPU)
+  void allred(double* d, size_t n, RedOpKind op);
+  double host_all(double v, RedOpKind op);
+  idx global_first_bad(idx local_bad);
+  void condensed_u_sum(const double* part, const double* base, double* out);
   template <int K>
   std::array<double, K> fetch(const double* d);
   DevStep step_view(DArr<double>* s);
@@ -97,7 +102,7 @@ class Solver {
   DArr<double> p[5], q[5];  // px, pu, ps, pz, py
   DArr<double> bsv[6];
   DArr<double> o1x, o1u, o2, o3, o4, o1u_part;
-  DArr<double> c_rhat1, c_rhat2, rhs_sum, pu_rhs;
+  DArr<double> c_rhat1, c_rhat2, rhs_sum, pu_rhs, red_u, dd_u;
   DArr<double> ft, gt, ht;  // line-search trial values
   DArr<double> partial, scal;
   DArr<int> flag;

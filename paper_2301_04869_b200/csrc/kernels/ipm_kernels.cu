@@ -238,25 +238,25 @@ __global__ void scenario_sum_kernel(int M, int n, const double* part, const doub
 }
 
 // ------------------------------------------- double-double accumulation
-struct dd {
+struct dd_pair {
   double hi, lo;
 };
-__device__ __forceinline__ dd two_sum(double a, double b) {
+__device__ __forceinline__ dd_pair two_sum(double a, double b) {
   const double s = a + b;
   const double bb = s - a;
   return {s, (a - (s - bb)) + (b - bb)};
 }
-__device__ __forceinline__ dd dd_add(dd a, dd b) {
-  dd s = two_sum(a.hi, b.hi);
+__device__ __forceinline__ dd_pair dd_add(dd_pair a, dd_pair b) {
+  dd_pair s = two_sum(a.hi, b.hi);
   s.lo += a.lo + b.lo;
   return two_sum(s.hi, s.lo);
 }
-__device__ __forceinline__ dd dd_add_prod(dd a, double x, double y) {
+__device__ __forceinline__ dd_pair dd_add_prod(dd_pair a, double x, double y) {
   const double p = x * y;
   const double e = fma(x, y, -p);
-  return dd_add(a, dd{p, e});
+  return dd_add(a, dd_pair{p, e});
 }
-__device__ __forceinline__ dd dd_add_d(dd a, double x) { return dd_add(a, dd{x, 0.0}); }
+__device__ __forceinline__ dd_pair dd_add_d(dd_pair a, double x) { return dd_add(a, dd_pair{x, 0.0}); }
 
 __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, double* partial) {
   constexpr int ops[1] = {kMax};
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
     const double* pu = a.p.pu;
     if (r < d.n_x) {  // row 1 (x block)
       const int i = r;
-      dd t{0.0, 0.0};
+      dd_pair t{0.0, 0.0};
       const double* w = a.wxx_v + size_t(s) * a.wxx.nnz;
       for (int q = a.wxx.ptr[i]; q < a.wxx.ptr[i + 1]; ++q) t = dd_add_prod(t, w[q], px[a.wxx.ind[q]]);
       const double* wu = a.wxu_v + size_t(s) * a.wxu.nnz;
@@ -297,7 +297,7 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
     r -= d.n_x;
     if (r < d.m) {  // row 2
       const size_t k = size_t(s) * d.m + r;
-      dd t{0.0, 0.0};
+      dd_pair t{0.0, 0.0};
       t = dd_add_prod(t, a.sigma_s[k], ps[r]);
       t = dd_add_d(t, pz[r]);
       t = dd_add_d(t, a.r2[k]);
@@ -309,7 +309,7 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
     r -= d.m;
     if (r < d.n_x) {  // row 3: G p_d + r3 (delta_c = 0 on the reduced path)
       const int i = r;
-      dd t{0.0, 0.0};
+      dd_pair t{0.0, 0.0};
       const double* gx = a.gx_v + size_t(s) * a.gx.nnz;
       for (int q = a.gx.ptr[i]; q < a.gx.ptr[i + 1]; ++q) t = dd_add_prod(t, gx[q], px[a.gx.ind[q]]);
       const double* gu = a.gu_v + size_t(s) * a.gu.nnz;
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
     r -= d.n_x;
     if (r < d.m) {  // row 4: H p_d + p_s + r4
       const int i = r;
-      dd t{0.0, 0.0};
+      dd_pair t{0.0, 0.0};
       const double* hx = a.hx_v + size_t(s) * a.hx.nnz;
       for (int q = a.hx.ptr[i]; q < a.hx.ptr[i + 1]; ++q) t = dd_add_prod(t, hx[q], px[a.hx.ind[q]]);
       const double* hu = a.hu_v + size_t(s) * a.hu.nnz;
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
     r -= d.m;  // u row partial of this scenario: W_xu' p_x + W_uu p_u + G_u' p_y + H_u' p_z
     {
       const int i = r;
-      dd t{0.0, 0.0};
+      dd_pair t{0.0, 0.0};
       const double* wu = a.wxu_v + size_t(s) * a.wxu.nnz;
       for (int q = a.wxu.t_ptr[i]; q < a.wxu.t_ptr[i + 1]; ++q)
         t = dd_add_prod(t, wu[a.wxu.t_slot[q]], px[a.wxu.t_row[q]]);
@@ -364,12 +364,41 @@ __global__ void aug_residual_u_kernel(AugResidualArgs a, double* o1u, double* ou
   double vmax[1] = {0.0};
   const IpmDims& d = a.d;
   for (int i = threadIdx.x; i < d.n_u; i += kB) {
-    dd t{a.r1u[i], 0.0};
+    dd_pair t{a.r1u[i], 0.0};
     t = dd_add_d(t, (a.sigma_u[i] + a.dw) * a.p.pu[i]);
     for (int s = 0; s < d.M; ++s) {
       const size_t k = (size_t(s) * d.n_u + i) * 2;
-      t = dd_add(t, dd{a.o1u_part[k], a.o1u_part[k + 1]});
+      t = dd_add(t, dd_pair{a.o1u_part[k], a.o1u_part[k + 1]});
     }
+    const double o = t.hi + t.lo;
+    o1u[i] = o;
+    vmax[0] = fmax(vmax[0], fabs(o));
+  }
+  block_partial<1>(vmax, ops, out);
+}
+
+__global__ void aug_residual_u_local_kernel(AugResidualArgs a, double* dd) {
+  const IpmDims& d = a.d;
+  for (int i = threadIdx.x + blockIdx.x * kB; i < d.n_u; i += kB * gridDim.x) {
+    dd_pair t{0.0, 0.0};
+    for (int s = 0; s < d.M; ++s) {
+      const size_t k = (size_t(s) * d.n_u + i) * 2;
+      t = dd_add(t, dd_pair{a.o1u_part[k], a.o1u_part[k + 1]});
+    }
+    dd[2 * i] = t.hi;
+    dd[2 * i + 1] = t.lo;
+  }
+}
+
+__global__ void aug_residual_u_finish_kernel(AugResidualArgs a, const double* dd, double* o1u,
+                                             double* out) {
+  constexpr int ops[1] = {kMax};
+  double vmax[1] = {0.0};
+  const IpmDims& d = a.d;
+  for (int i = threadIdx.x; i < d.n_u; i += kB) {
+    dd_pair t{a.r1u[i], 0.0};
+    t = dd_add_d(t, (a.sigma_u[i] + a.dw) * a.p.pu[i]);
+    t = dd_add(t, dd_pair{dd[2 * i], dd[2 * i + 1]});
     const double o = t.hi + t.lo;
     o1u[i] = o;
     vmax[0] = fmax(vmax[0], fabs(o));
@@ -768,6 +797,19 @@ void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, 
   aug_residual_u_kernel<<<1, kB, 0, st>>>(a, o1u, out1);
   note_launch();
   check("aug_residual_u");
+}
+
+void launch_aug_residual_u_local(const AugResidualArgs& a, double* dd, cudaStream_t st) {
+  aug_residual_u_local_kernel<<<ew_blocks(a.d.n_u), kB, 0, st>>>(a, dd);
+  note_launch();
+  check("aug_residual_u_local");
+}
+
+void launch_aug_residual_u_finish(const AugResidualArgs& a, const double* dd, double* o1u,
+                                  double* out1, cudaStream_t st) {
+  aug_residual_u_finish_kernel<<<1, kB, 0, st>>>(a, dd, o1u, out1);
+  note_launch();
+  check("aug_residual_u_finish");
 }
 
 void launch_rhs_scale(const IpmDims& d, const double* r1x, const double* r1u, const double* r2,

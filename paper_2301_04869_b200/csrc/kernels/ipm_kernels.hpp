@@ -88,6 +88,11 @@ void launch_aug_residual(const AugResidualArgs& a, double* partial, double* out1
                          cudaStream_t st);
 // o1u = r1u + (sigma_u + dw) p_u + sum_s part (double-double); out[0] = max|o1u|
 void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st);
+// sharded variant: dd[2 n_u] = local sum of the per-scenario u-row partials
+// (hi, lo); after the cross-rank all-reduce, finish adds r1u + (sigma_u+dw) p_u
+void launch_aug_residual_u_local(const AugResidualArgs& a, double* dd, cudaStream_t st);
+void launch_aug_residual_u_finish(const AugResidualArgs& a, const double* dd, double* o1u,
+                                  double* out1, cudaStream_t st);
 // max(1, |r1x|, |r1u|, |r2|, |r3|, |r4|) partial pieces
 void launch_rhs_scale(const IpmDims& d, const double* r1x, const double* r1u, const double* r2,
                       const double* r3, const double* r4, double* partial, double* out1,
