@@ -55,3 +55,16 @@ def test_max_iter_status():
     p = nat.Problem(case_path("case9"), 8, 0.05, 0)
     r = nat.Solver(nat.Context(p), max_iter=3).solve()
     assert r["status_name"] == "MaxIter" and r["iterations"] == 3
+
+
+def test_case1354_N256_matches_reference_at_scale():
+    """BASELINE configs[2] workload on one GPU: same iteration count and
+    objective as the reference CPU solve (tests/golden/solves_large.json)."""
+    ref = json.load(open(os.path.join(GOLDEN, "solves_large.json")))[
+        "case1354pegase_N256_s0.05_seed0"]
+    p = nat.Problem(case_path("case1354pegase"), 256, 0.05, 0)
+    r = nat.Solver(nat.Context(p)).solve()
+    assert r["status_name"] == "Optimal" and r["iterations"] == ref["iterations"]
+    assert abs(r["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
+    u_ref = np.array(ref["u"])
+    assert np.abs(r["u"] - u_ref).max() <= 1e-6 * max(1.0, np.abs(u_ref).max())
