@@ -88,8 +88,7 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
   }
   const std::map<std::string, const std::vector<idx>*> lu_more = {
       {"lu_ft_src", &P.LU.ft_src},     {"lu_diag", &P.LU.diag},     {"lu_a_src", &P.LU.a_src},
-      {"lu_dense_src0", &P.LU.dense_src[0]}, {"lu_dense_src1", &P.LU.dense_src[1]},
-      {"lu_dense_src2", &P.LU.dense_src[2]}, {"lu_dense_src3", &P.LU.dense_src[3]}};
+      {"lu_dense_src0", &P.LU.dense_src[0]}, {"lu_dense_src1", &P.LU.dense_src[1]}};
   if (auto it = lu_more.find(name); it != lu_more.end()) return ints(*it->second);
   const std::map<std::string, const SweepPlan*> sweeps = {
       {"sL", &P.LU.sL}, {"sU", &P.LU.sU}, {"sUt", &P.LU.sUt}, {"sLt", &P.LU.sLt}};

@@ -160,7 +160,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   rhat2.resize(size_t(Mo.n_u));
   F.resize(Ms * size_t(L.nnz_f));
   FT.resize(Ms * size_t(L.nnz_f));
-  Dt.resize(std::max<size_t>(1, Ms * 4 * size_t(L.tl) * size_t(L.tl)));
+  Dt.resize(std::max<size_t>(1, Ms * 2 * size_t(L.tl) * size_t(L.tl)));
   lu_status.resize(Ms);
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));

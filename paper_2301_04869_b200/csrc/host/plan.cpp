@@ -242,7 +242,9 @@ std::vector<idx> min_degree_order(const Csr& S) {
 namespace {
 
 // Trailing block solved densely: the run of narrow forward levels (<= 2 rows)
-// at the end of the schedule, capped at 256 rows.
+// at the end of the schedule, capped at kMaxTail rows (the refactor stages
+// L_TT and U_TT in shared memory to form W = (L_TT U_TT)^{-1}).
+constexpr idx kMaxTail = 112;
 idx choose_tail(const std::vector<idx>& fwd_level, idx n) {
   idx nlev = 0;
   for (idx v : fwd_level) nlev = std::max(nlev, v + 1);
@@ -251,7 +253,7 @@ idx choose_tail(const std::vector<idx>& fwd_level, idx n) {
   idx t0 = n;
   for (idx i = n - 1; i >= 0; --i) {
     if (width[size_t(fwd_level[size_t(i)])] > 2) break;
-    if (n - i > 256) break;
+    if (n - i > kMaxTail) break;
     t0 = i;
   }
   // rows in the tail must come after every non-tail row of their levels
@@ -371,9 +373,7 @@ void build_sweeps(LuPlan& P, const std::vector<std::vector<idx>>& lrow,
       }
       // column-major position of (a, b) is b * tl + a
       P.dense_src[0][size_t(b) * tl + a] = lslot;  // L_TT
-      P.dense_src[1][size_t(a) * tl + b] = lslot;  // L_TT' : (b, a)
-      P.dense_src[2][size_t(b) * tl + a] = uslot;  // U_TT
-      P.dense_src[3][size_t(a) * tl + b] = uslot;  // U_TT'
+      P.dense_src[1][size_t(b) * tl + a] = uslot;  // U_TT
     }
 }
 

@@ -98,8 +98,10 @@ struct LuPlan {
   idx t0 = 0, tl = 0;             // dense tail rows [t0, n), tl = n - t0
   std::vector<idx> ft_src;        // FT[p] = F[ft_src[p]]
   // dense tail blocks, column-major tl x tl, source F slot or -1 (zero):
-  //   0: L_TT (unit lower)   1: L_TT' (unit upper)   2: U_TT   3: U_TT'
-  std::vector<idx> dense_src[4];
+  //   0: L_TT (unit lower)   1: U_TT (upper)
+  // The refactor turns them into W = (L_TT U_TT)^{-1} (row-major) and W'
+  // (row-major), so a solve's tail is one dense product per sweep pair.
+  std::vector<idx> dense_src[2];
   SweepPlan sL, sU, sUt, sLt;
 };
 

@@ -127,14 +127,40 @@ __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const doubl
   }
   bad = block_reduce<BLOCK>(bad, true);
   if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
-  // solve layouts: transposed copy and dense tail blocks
+  // solve layouts: transposed copy ...
   double* FTs = FT + size_t(s) * P.nnz_f;
   for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
-  const int nd = 4 * P.tl * P.tl;
-  double* Ds = D + size_t(s) * nd;
-  for (int q = threadIdx.x; q < nd; q += BLOCK) {
+  // ... and W = (L_TT U_TT)^{-1}: stage the tail triangles in shared memory,
+  // thread j solves L U w = e_j for column j (written row-major to W and W')
+  const int tl = P.tl;
+  if (tl == 0) return;
+  extern __shared__ double tri[];  // [L_TT | U_TT], column-major
+  const int tt = tl * tl;
+  for (int q = threadIdx.x; q < 2 * tt; q += BLOCK) {
     const int src = P.dense_src[q];
-    Ds[q] = src >= 0 ? Fs[src] : 0.0;
+    tri[q] = src >= 0 ? Fs[src] : 0.0;
+  }
+  __syncthreads();
+  const double* Lt = tri;
+  const double* Ut = tri + tt;
+  double* W = D + size_t(s) * 2 * tt;
+  double* Wt = W + tt;
+  for (int j = threadIdx.x; j < tl; j += BLOCK) {
+    // forward: y = L^{-1} e_j (y_i = 0 for i < j), kept in W[:, j]
+    for (int i = 0; i < j; ++i) W[i * tl + j] = 0.0;
+    W[j * tl + j] = 1.0;
+    for (int i = j + 1; i < tl; ++i) {
+      double acc = 0.0;
+      for (int k = j; k < i; ++k) acc += Lt[k * tl + i] * W[k * tl + j];
+      W[i * tl + j] = -acc;
+    }
+    // backward: w = U^{-1} y
+    for (int i = tl - 1; i >= 0; --i) {
+      double acc = W[i * tl + j];
+      for (int k = i + 1; k < tl; ++k) acc -= Ut[k * tl + i] * W[k * tl + j];
+      W[i * tl + j] = acc / Ut[i * tl + i];
+    }
+    for (int i = 0; i < tl; ++i) Wt[j * tl + i] = W[i * tl + j];
   }
 }
 
@@ -193,7 +219,7 @@ __global__ void __launch_bounds__(BLOCK, 1) reduce_tiles_kernel(ReduceLaunch a) 
     mark(s);
     tail_gather<BLOCK, K, false>(P.sL, F.F, X);
     mark(s);
-    dense_tail_pair<BLOCK, K, true, false>(P, dense_block(P, F, 0), dense_block(P, F, 2), X);
+    dense_tail_gemm<BLOCK, K>(P, dense_block(P, F, 0), X);
     mark(s);
     level_sweep<BLOCK, K, true>(P.sU, F.F + P.nnz_l, X);
     mark(s);
@@ -232,7 +258,7 @@ __global__ void __launch_bounds__(BLOCK, 1) reduce_tiles_kernel(ReduceLaunch a) 
     mark(s);
     tail_gather<BLOCK, K, true>(P.sUt, F.FT, X);
     mark(s);
-    dense_tail_pair<BLOCK, K, false, true>(P, dense_block(P, F, 3), dense_block(P, F, 1), X);
+    dense_tail_gemm<BLOCK, K>(P, dense_block(P, F, 1), X);
     mark(s);
     level_sweep<BLOCK, K, false>(P.sLt, F.FT + (P.nnz_f - P.nnz_l), X);
     mark(s);
@@ -576,7 +602,10 @@ size_t single_rhs_smem(int n_x) {
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, cudaStream_t st) {
   if (M <= 0) return;
-  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol);
+  const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
+  cudaFuncSetAttribute(lu_refactor_kernel<kLuBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol);
   note_launch();
   check_launch("lu_refactor");
 }

@@ -10,12 +10,10 @@
 // per-item index arithmetic is hoisted out of the entry loop.
 //
 // Dense tail: the trailing separator block [t0, n) of the elimination order is
-// a long chain of one-row levels; it is solved as a dense triangle with the
-// panel column held in registers of one warp (row i on lane i % 32, register
-// i / 32), the pivot value broadcast by shuffle and the next column of the
-// dense block prefetched one step ahead.  The L and U tails (and the U' and
-// L' tails) are adjacent in the solve order and run back to back without
-// leaving registers.
+// a long chain of one-row levels.  Its L and U triangles (and the U', L'
+// ones) are adjacent in the solve order, so the pair is one multiplication by
+// W = (L_TT U_TT)^{-1} (W' for the transposed solve), formed once per
+// refactor: 2 tl dependent steps become one parallel tl x tl x K product.
 #pragma once
 
 #include "device_plan.cuh"
@@ -122,117 +120,46 @@ __device__ void tail_gather(const DevSweep& S, const double* __restrict__ V, dou
   __syncthreads();
 }
 
-// Dense triangular solves of the tail block in registers of one warp.
-// D is the column-major tl x tl matrix; lower/forward or upper/backward.
-// Columns stream through a 4-deep register ring (prefetch distance 4).
-template <int NQ>
-__device__ __forceinline__ void load_col(const double* __restrict__ D, int tl, int j,
-                                         double (&v)[NQ]) {
-  const int lane = threadIdx.x & 31;
-  const bool ok = j >= 0 && j < tl;
-  const double* __restrict__ col = D + size_t(ok ? j : 0) * tl;
+// Dense tail: X_T <- W X_T for every panel column, W = (L_TT U_TT)^{-1} (or
+// its transpose) precomputed by the refactor, row-major tl x tl.  Up to 8
+// outputs per thread are formed in registers before any is written back.
+template <int BLOCK, int K>
+__device__ void dense_tail_gemm(const DevLu& P, const double* __restrict__ W, double* X) {
+  const int tl = P.tl, t0 = P.t0;
+  if (tl == 0) return;
+  constexpr int kMaxOut = 8;
+  const int n = tl * K;
+  double r[kMaxOut];
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    const int i = q * 32 + lane;
-    v[q] = (ok && i < tl) ? col[i] : 0.0;
-  }
-}
-
-template <int NQ, bool kUnit>
-__device__ __forceinline__ void dense_forward(const double* __restrict__ D, int tl, double (&xr)[NQ]) {
-  constexpr int R = NQ <= 4 ? 4 : 2;  // ring depth (register budget)
-  const int lane = threadIdx.x & 31;
-  double ring[R][NQ];
-#pragma unroll
-  for (int u = 0; u < R; ++u) load_col<NQ>(D, tl, u, ring[u]);
-#pragma unroll
-  for (int qj = 0; qj < NQ; ++qj) {
-    if (qj * 32 >= tl) break;
-    // not unrolled: the ring is loop-carried, so each column load is issued
-    // R steps before its use instead of being sunk next to it
-#pragma unroll 1
-    for (int jb = 0; jb < 32; jb += R) {
-#pragma unroll
-      for (int u = 0; u < R; ++u) {
-        const int jj = jb + u, j = qj * 32 + jj;
-        if (j < tl) {
-          if (!kUnit && lane == jj) xr[qj] /= ring[u][qj];
-          const double xj = __shfl_sync(0xffffffffu, xr[qj], jj);
-#pragma unroll
-          for (int q = qj; q < NQ; ++q)
-            if (q * 32 + lane > j) xr[q] -= ring[u][q] * xj;
-        }
-        load_col<NQ>(D, tl, j + R, ring[u]);
+  for (int q = 0; q < kMaxOut; ++q) {
+    const int o = threadIdx.x + q * BLOCK;
+    r[q] = 0.0;
+    if (o < n) {
+      const int i = o / K, c = o % K;
+      const double* __restrict__ w = W + size_t(i) * tl;
+      const double* __restrict__ xc = X + t0 * K + c;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int k = 0;
+      for (; k + 3 < tl; k += 4) {
+        a0 += w[k] * xc[k * K];
+        a1 += w[k + 1] * xc[(k + 1) * K];
+        a2 += w[k + 2] * xc[(k + 2) * K];
+        a3 += w[k + 3] * xc[(k + 3) * K];
       }
+      for (; k < tl; ++k) a0 += w[k] * xc[k * K];
+      r[q] = (a0 + a1) + (a2 + a3);
     }
   }
-}
-
-template <int NQ, bool kUnit>
-__device__ __forceinline__ void dense_backward(const double* __restrict__ D, int tl, double (&xr)[NQ]) {
-  constexpr int R = NQ <= 4 ? 4 : 2;
-  const int lane = threadIdx.x & 31;
-  // walk j = NQ*32-1 down to 0; columns >= tl are skipped
-  double ring[R][NQ];
-  const int top = NQ * 32 - 1;
+  __syncthreads();
 #pragma unroll
-  for (int u = 0; u < R; ++u) load_col<NQ>(D, tl, top - u, ring[u]);
-#pragma unroll
-  for (int qj = NQ - 1; qj >= 0; --qj) {
-#pragma unroll 1
-    for (int jb = 31; jb >= 0; jb -= R) {
-#pragma unroll
-      for (int u = 0; u < R; ++u) {
-        const int jj = jb - u, j = qj * 32 + jj;
-        if (j < tl) {
-          if (!kUnit && lane == jj) xr[qj] /= ring[u][qj];
-          const double xj = __shfl_sync(0xffffffffu, xr[qj], jj);
-#pragma unroll
-          for (int q = 0; q <= qj; ++q)
-            if (q * 32 + lane < j) xr[q] -= ring[u][q] * xj;
-        }
-        load_col<NQ>(D, tl, j - R, ring[u]);
-      }
-    }
+  for (int q = 0; q < kMaxOut; ++q) {
+    const int o = threadIdx.x + q * BLOCK;
+    if (o < n) X[(t0 + o / K) * K + o % K] = r[q];
   }
-}
-
-// Tail pair on every panel column: forward triangle D1 (unit when kUnit1),
-// then backward triangle D2 (unit when kUnit2).  D1 or D2 may be null.
-template <int NQ, bool kUnit1, bool kUnit2>
-__device__ void dense_tail_pair_nq(const double* D1, const double* D2, double* X, int t0, int tl,
-                                   int K, int nwarps) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int c = warp; c < K; c += nwarps) {
-    double xr[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = q * 32 + lane;
-      xr[q] = i < tl ? X[(t0 + i) * K + c] : 0.0;
-    }
-    if (D1) dense_forward<NQ, kUnit1>(D1, tl, xr);
-    if (D2) dense_backward<NQ, kUnit2>(D2, tl, xr);
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      const int i = q * 32 + lane;
-      if (i < tl) X[(t0 + i) * K + c] = xr[q];
-    }
-  }
-}
-
-template <int BLOCK, int K, bool kUnit1, bool kUnit2>
-__device__ void dense_tail_pair(const DevLu& P, const double* D1, const double* D2, double* X) {
-  if (P.tl == 0) return;
-  constexpr int kWarps = BLOCK / 32;
-  if (P.tl <= 64)
-    dense_tail_pair_nq<2, kUnit1, kUnit2>(D1, D2, X, P.t0, P.tl, K, kWarps);
-  else if (P.tl <= 128)
-    dense_tail_pair_nq<4, kUnit1, kUnit2>(D1, D2, X, P.t0, P.tl, K, kWarps);
-  else
-    dense_tail_pair_nq<8, kUnit1, kUnit2>(D1, D2, X, P.t0, P.tl, K, kWarps);
   __syncthreads();
 }
 
+// D = [W row-major | W' row-major], W = (L_TT U_TT)^{-1}
 __device__ __forceinline__ const double* dense_block(const DevLu& P, const FactorView& f, int b) {
   return f.D + size_t(b) * P.tl * P.tl;
 }
@@ -242,7 +169,7 @@ template <int BLOCK, int K>
 __device__ void solve_LU(const DevLu& P, const FactorView& f, double* X) {
   level_sweep<BLOCK, K, false>(P.sL, f.F, X);
   tail_gather<BLOCK, K, false>(P.sL, f.F, X);
-  dense_tail_pair<BLOCK, K, true, false>(P, dense_block(P, f, 0), dense_block(P, f, 2), X);
+  dense_tail_gemm<BLOCK, K>(P, dense_block(P, f, 0), X);
   level_sweep<BLOCK, K, true>(P.sU, f.F + P.nnz_l, X);
 }
 
@@ -251,7 +178,7 @@ template <int BLOCK, int K>
 __device__ void solve_LUt(const DevLu& P, const FactorView& f, double* X) {
   level_sweep<BLOCK, K, true>(P.sUt, f.FT, X);
   tail_gather<BLOCK, K, true>(P.sUt, f.FT, X);
-  dense_tail_pair<BLOCK, K, false, true>(P, dense_block(P, f, 3), dense_block(P, f, 1), X);
+  dense_tail_gemm<BLOCK, K>(P, dense_block(P, f, 1), X);
   level_sweep<BLOCK, K, false>(P.sLt, f.FT + (P.nnz_f - P.nnz_l), X);
 }
 

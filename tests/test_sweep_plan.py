@@ -15,10 +15,15 @@ def emulate(p, F):
     n, nnz_l, nnz_f, t0, tl = p.array("lu_shape")
     FT = F[p.array("lu_ft_src")]
     dense = []
-    for b in range(4):
+    for b in range(2):
         src = p.array(f"lu_dense_src{b}")
         d = np.where(src >= 0, F[np.maximum(src, 0)], 0.0)
         dense.append(d.reshape(tl, tl).T if tl else np.zeros((0, 0)))  # column-major -> [i, j]
+    # what the refactor forms: W = (L_TT U_TT)^{-1}
+    if tl:
+        LT = np.tril(dense[0], -1) + np.eye(tl)
+        UT = np.triu(dense[1])
+        W = np.linalg.solve(UT, np.linalg.solve(LT, np.eye(tl)))
 
     def level(name, V, x, diag):
         lp, items, col = p.array(f"lu_{name}_lvl_ptr"), p.array(f"lu_{name}_items"), \
@@ -39,27 +44,19 @@ def emulate(p, F):
             bb = b + (1 if diag else 0)
             x[row] -= np.dot(V[bb:split], x[col[bb:split]])
 
-    def tail(D, x, unit, lower):
-        if tl == 0:
-            return
-        T = np.tril(D) if lower else np.triu(D)
-        if unit:
-            np.fill_diagonal(T, 1.0)
-        x[t0:] = sl.solve_triangular(T, x[t0:], lower=lower, unit_diagonal=unit)
+    def solve_LU(x):  # sweeps.cuh solve_LU
+        level("sL", F, x, False); gather("sL", F, x, False)
+        if tl:
+            x[t0:] = W @ x[t0:]
+        level("sU", F[nnz_l:], x, True)
 
-    def solve_L(x):
-        level("sL", F, x, False); gather("sL", F, x, False); tail(dense[0], x, True, True)
+    def solve_LUt(x):  # sweeps.cuh solve_LUt
+        level("sUt", FT, x, True); gather("sUt", FT, x, True)
+        if tl:
+            x[t0:] = W.T @ x[t0:]
+        level("sLt", FT[nnz_f - nnz_l:], x, False)
 
-    def solve_U(x):
-        tail(dense[2], x, False, False); level("sU", F[nnz_l:], x, True)
-
-    def solve_Ut(x):
-        level("sUt", FT, x, True); gather("sUt", FT, x, True); tail(dense[3], x, False, True)
-
-    def solve_Lt(x):
-        tail(dense[1], x, True, False); level("sLt", FT[nnz_f - nnz_l:], x, False)
-
-    return solve_L, solve_U, solve_Ut, solve_Lt
+    return solve_LU, solve_LUt
 
 
 @pytest.mark.parametrize("case", ["case118", "case1354pegase"])
@@ -79,13 +76,13 @@ def test_sweeps_solve_the_factor_pattern(case):
     sp, sc = p.array("lu_sU_ptr"), p.array("lu_sU_col")
     for i in range(n):
         U[i, sc[sp[i]:sp[i + 1]]] = F[nnz_l + sp[i]:nnz_l + sp[i + 1]]
-    solve_L, solve_U, solve_Ut, solve_Lt = emulate(p, F)
+    solve_LU, solve_LUt = emulate(p, F)
     b = rng.normal(size=n)
-    for fn, M, lower in ((solve_L, L, True), (solve_U, U, False), (solve_Ut, U.T, True),
-                         (solve_Lt, L.T, False)):
+    A = L @ U
+    for fn, M in ((solve_LU, A), (solve_LUt, A.T)):
         x = b.copy()
         fn(x)
-        ref = sl.solve_triangular(M, b, lower=lower)
-        assert np.abs(x - ref).max() <= 1e-10 * max(1.0, np.abs(ref).max())
+        ref = np.linalg.solve(M, b)
+        assert np.abs(x - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
     if case == "case1354pegase":
         assert tl >= 64  # the separator chain goes to the dense tail
