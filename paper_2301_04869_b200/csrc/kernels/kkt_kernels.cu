@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const doubl
 __device__ __forceinline__ FactorView factor_of(const DevLu& P, const double* F, const double* FT,
                                                 const double* D, int s) {
   return FactorView{F + size_t(s) * P.nnz_f, FT + size_t(s) * P.nnz_f,
-                    D + size_t(s) * 4 * P.tl * P.tl};
+                    D + size_t(s) * 2 * P.tl * P.tl};
 }
 
 template <int BLOCK, int K>

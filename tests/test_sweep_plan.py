@@ -59,7 +59,7 @@ def emulate(p, F):
     return solve_LU, solve_LUt
 
 
-@pytest.mark.parametrize("case", ["case118", "case1354pegase"])
+@pytest.mark.parametrize("case", ["case9", "case118", "case1354pegase"])
 def test_sweeps_solve_the_factor_pattern(case):
     p = nat.Problem(case_path(case), 2, 0.05, 0)
     n, nnz_l, nnz_f, t0, tl = p.array("lu_shape")
