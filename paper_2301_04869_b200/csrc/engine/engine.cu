@@ -191,6 +191,13 @@ Engine::~Engine() {
 
 void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 
+void Engine::factor_gx_launch() {
+  timed("lu_refactor", [&] {
+    launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
+                       lu_status.get(), 1e-12, st);
+  });
+}
+
 idx Engine::factor_gx() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
@@ -425,7 +432,7 @@ void Engine::upload_ad() {
 }
 
 idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const double* dY,
-                        const double* dZ, double obj_w) {
+                        const double* dZ, double obj_w, bool check) {
   AdBuffers b{};
   b.X = dX;
   b.u = du;
@@ -450,7 +457,7 @@ idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const d
   b.bad = bad.get();
   bad.zero(st);
   timed("ad_bundle", [&] { launch_ad_bundle(ad, b, st); });
-  return first_bad();
+  return check ? first_bad() : -1;
 }
 
 idx Engine::eval_values(const double* dX, const double* du, double* df, double* dg,

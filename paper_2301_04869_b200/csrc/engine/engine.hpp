@@ -99,13 +99,16 @@ class Engine {
   // ---- operators (device-resident inputs/outputs)
   // eval_bundle_range (autodiff.cpp:484-516) into `out`; returns the lowest
   // global scenario index with a non-finite basis / derivative, or -1.
+  // check=false only launches: the per-scenario flags stay in `bad` for a
+  // later fused reduction (Solver::kkt_eval) and -1 is returned
   idx eval_bundle(Bundle& out, const double* dX, const double* du, const double* dY,
-                  const double* dZ, double obj_w);
+                  const double* dZ, double obj_w, bool check = true);
   // batch_eval (autodiff.cpp:256-281): f, g, h only
   idx eval_values(const double* dX, const double* du, double* df, double* dg, double* dh);
   // factor_gx_range (kkt.cpp:190-196): returns the lowest singular global
   // scenario index or -1.
   idx factor_gx();
+  void factor_gx_launch();  // refactor only; statuses stay in lu_status
   // condense (kkt.cpp:123-170) of the K blocks from the bundle and sigma_s
   void condense_blocks();
   void condense_launch();

@@ -79,6 +79,8 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
   partial.resize(600 * 8);
   scal.resize(32);
   flag.resize(1);
+  eval_counter.resize(1);
+  eval_counter.zero(e.st);
   cuda_check(cudaMallocHost(&pinned, 64 * sizeof(double)), "cudaMallocHost");
   // multiplier count of the scaled error (ipm.cpp:345-379): structural
   double fin_x = 0, fin_s = 0, fin_u = 0;
@@ -128,29 +130,37 @@ DevStep Solver::step_view(DArr<double>* s) {
   return DevStep{s[0].get(), s[1].get(), s[2].get(), s[3].get(), s[4].get()};
 }
 
-Solver::Scaled Solver::scaled_error(const DevIter& it, Engine::Bundle& bd, double mu_) {
+Solver::ErrEval Solver::kkt_eval(const DevIter& it, Engine::Bundle& bd, const double mus[4],
+                                 bool check_bad) {
   double* sc = scal.get();
-  launch_kkt_error_xs(d, it, b, bd.grad.get(), bd.g.get(), bd.h.get(), mu_, partial.get(), sc,
-                      e.st);
   launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
   allred(gsum_u.get(), size_t(d.n_u), RedOpKind::kSum);
-  launch_kkt_error_u(d, it, b, gsum_u.get(), mu_, sc + 8, e.st);
-  launch_scenario_sum(d.M, 1, bd.f.get(), nullptr, sc + 11, e.st);
-  allred(sc, 5, RedOpKind::kMax);   // x/s norms and complementarity
-  allred(sc + 5, 1, RedOpKind::kSum);  // multiplier sum (x/s part)
-  allred(sc + 11, 1, RedOpKind::kSum);  // objective
-  const auto v = fetch<12>(sc);
-  objective = v[11];
-  const double stat = std::max({v[0], v[1], v[8]});
-  const double primal = std::max(v[2], v[3]);
-  const double comp = std::max(v[4], v[9]);
-  const double avg = mult_count > 0 ? (v[5] + v[10]) / mult_count : 0.0;
+  launch_kkt_eval(d, it, b, bd.grad.get(), bd.g.get(), bd.h.get(), bd.f.get(),
+                  check_bad ? e.bad.get() : nullptr, e.lo, gsum_u.get(), mus, partial.get(),
+                  eval_counter.get(), sc, e.st);
+  allred(sc, 8, RedOpKind::kMax);      // x/s norms and complementarities
+  allred(sc + 8, 2, RedOpKind::kSum);  // multiplier sum, objective
+  allred(sc + 10, 1, RedOpKind::kMin); // lowest non-finite scenario
+  const auto v = fetch<17>(sc);
+  ErrEval E;
+  E.stat = std::max({v[0], v[1], v[11]});
+  E.primal = std::max(v[2], v[3]);
+  for (int k = 0; k < 4; ++k) E.comp[k] = std::max(v[4 + k], v[12 + k]);
+  E.mult = v[8] + v[16];
+  E.obj = v[9];
+  E.bad = v[10] < 1e299 ? idx(v[10]) : -1;
+  return E;
+}
+
+// IPOPT-style scaled error (ipm.cpp:345-379) at barrier parameter k of E
+Solver::Scaled Solver::scaled_of(const ErrEval& E, int k) const {
+  const double avg = mult_count > 0 ? E.mult / mult_count : 0.0;
   const double s_d = std::max(100.0, avg) / 100.0;
   Scaled r;
-  r.stationarity = stat / s_d;
-  r.primal = primal;
-  r.comp = comp / s_d;
-  r.comp_raw = comp;
+  r.stationarity = E.stat / s_d;
+  r.primal = E.primal;
+  r.comp = E.comp[k] / s_d;
+  r.comp_raw = E.comp[k];
   r.total = std::max({r.stationarity, r.primal, r.comp});
   return r;
 }
@@ -199,16 +209,18 @@ bool Solver::attempt(double dw, const DevIter& it) {
   e.reduce_local(dw);
   e.finish_reduce(dw);
   e.reduce_rhs_local(dw, rhs_sum.get());
+  // refinement scale (independent of the factor) rides on the Cholesky sync
+  launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
+                   scal.get() + 20, e.st);
+  allred(scal.get() + 20, 1, RedOpKind::kMax);
+  cudaMemcpyAsync(pinned + 40, scal.get() + 20, sizeof(double), cudaMemcpyDeviceToHost, e.st);
   if (!e.factor_khat()) return false;
+  const double scale = pinned[40];
   // solve_with(c, first_sum): p_u, then state/adjoint and slack/dual recovery
   launch_pu_rhs(d.n_u, rhs_sum.get(), e.rhat2.get(), p[1].get(), true, e.st);
   e.solve_khat(p[1].get());
   e.recover(dw, p[1].get(), p[0].get(), p[4].get(), p[3].get(), p[2].get());
   // refinement against the unreduced augmented system (kkt.cpp:988-999)
-  launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
-                   scal.get() + 20, e.st);
-  allred(scal.get() + 20, 1, RedOpKind::kMax);
-  const double scale = fetch1(scal.get() + 20);
   const DerivPlan& D = e.pb.D;
   (void)D;
   for (int round = 0; round < o.refine_rounds; ++round) {
@@ -285,11 +297,21 @@ void Solver::compute_step(const DevIter& it) {
   launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
                        e.r4.get(), e.r2.get(), r1x.get(), e.rhat1.get(), rhat2_part.get(), e.st);
   condensed_u_sum(rhat2_part.get(), r1u.get(), e.rhat2.get());
-  int fl = 0;
-  flag.download(&fl, 1, e.st);
+  e.factor_gx_launch();
+  // one round trip for the interiority flag and the refactor statuses
+  std::vector<int> st_host(static_cast<size_t>(d.M) + 1);
+  flag.download(st_host.data(), 1, e.st);
+  e.lu_status.download(st_host.data() + 1, size_t(d.M), e.st);
   e.sync();
-  if (host_all(double(fl), RedOpKind::kMax) > 0) throw Error(kNonInterior, "iterate not strictly interior");
-  const idx sing = global_first_bad(e.factor_gx());
+  if (host_all(double(st_host[0]), RedOpKind::kMax) > 0)
+    throw Error(kNonInterior, "iterate not strictly interior");
+  idx local_sing = -1;
+  for (idx k = 0; k < d.M; ++k)
+    if (st_host[size_t(k) + 1]) {
+      local_sing = e.lo + k;
+      break;
+    }
+  const idx sing = global_first_bad(local_sing);
   if (sing >= 0)
     throw Error(kSingularBlock,
                 "singular block " + std::to_string(sing) +
@@ -322,15 +344,20 @@ int Solver::step() {
   log.iter = iter;
   const double t_iter = now();
   DevIter it = cur();
+  bool evaluated = false;
   if (!bundle_fresh) {
     const double ta = now();
-    const idx bad = global_first_bad(e.eval_bundle(e.bd(), it.x, it.u, it.y, it.z, 1.0));
-    if (bad >= 0) throw Error(kNonFinite, "non-finite basis output", bad);
+    e.eval_bundle(e.bd(), it.x, it.u, it.y, it.z, 1.0, /*check=*/false);
+    evaluated = true;
     log.t_ad += now() - ta;
   }
   bundle_fresh = false;
-  const Scaled e0 = scaled_error(it, e.bd(), 0.0);
-  log.objective = objective;
+  // residuals at mu = 0 and at the next barrier parameters in one pass
+  double mus[4] = {0.0, mu, update_mu(mu, o), update_mu(update_mu(mu, o), o)};
+  ErrEval E = kkt_eval(it, e.bd(), mus, evaluated);
+  if (E.bad >= 0) throw Error(kNonFinite, "non-finite basis output", E.bad);
+  const Scaled e0 = scaled_of(E, 0);
+  log.objective = objective = E.obj;
   log.inf_pr = e0.primal;
   log.inf_du = e0.stationarity;
   log.complementarity = e0.comp_raw;
@@ -349,12 +376,21 @@ int Solver::step() {
     log.mu = mu;
     return finish(kOptimal);
   }
-  for (;;) {
-    const Scaled emu = scaled_error(it, e.bd(), mu);
+  // barrier subproblem test and monotone mu decrease (ipm.cpp:484-492)
+  double theta0 = 0.0;
+  for (int k = 1;;) {
+    if (k > 3) {  // beyond the precomputed candidates: another pass
+      mus[1] = mu, mus[2] = update_mu(mu, o), mus[3] = update_mu(mus[2], o);
+      E = kkt_eval(it, e.bd(), mus, false);
+      k = 1;
+    }
+    const Scaled emu = scaled_of(E, k);
     if (emu.total <= o.kappa_eps * mu && mu > o.tol / 10.0) {
       mu = update_mu(mu, o);
+      ++k;
       continue;
     }
+    theta0 = emu.total;  // = the reference's fresh residual at the final mu
     break;
   }
   log.mu = mu;
@@ -374,17 +410,15 @@ int Solver::step() {
 
   // full-step primal-dual acceptance (ipm.cpp:518-563)
   {
-    const double theta0 = scaled_error(it, e.bd(), mu).total;
-    const double obj_it = objective;
     DevIter tr = alt();
     launch_apply_step(d, it, tr, b, ps, bs, ap, ad, mu, e.st);
     const double ta = now();
-    const idx bad = global_first_bad(e.eval_bundle(e.trial(), tr.x, tr.u, tr.y, tr.z, 1.0));
-    double theta1 = kInf;
-    const bool ok = bad < 0;
-    if (ok) theta1 = scaled_error(tr, e.trial(), mu).total;
-    objective = obj_it;
+    e.eval_bundle(e.trial(), tr.x, tr.u, tr.y, tr.z, 1.0, /*check=*/false);
+    const double tmus[4] = {mu, mu, mu, mu};
+    const ErrEval E1 = kkt_eval(tr, e.trial(), tmus, true);
     log.t_ad += now() - ta;
+    const bool ok = E1.bad < 0;
+    const double theta1 = ok ? scaled_of(E1, 0).total : kInf;
     if (ok && theta1 <= 0.99 * theta0) {
       icur = 1 - icur;
       e.swap_bundles();

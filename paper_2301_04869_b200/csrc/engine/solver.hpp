@@ -72,7 +72,14 @@ class Solver {
     DArr<double> x, u, s, y, z, klo, kup, nlo, nup, llo, lup;
     DevIter view();
   };
-  Scaled scaled_error(const DevIter& it, Engine::Bundle& bd, double mu);
+  // one fused residual pass at mus[0..3]; bad flags of the last bundle
+  // evaluation are folded in when check_bad (lowest non-finite scenario)
+  struct ErrEval {
+    double stat, primal, comp[4], mult, obj;
+    idx bad;
+  };
+  ErrEval kkt_eval(const DevIter& it, Engine::Bundle& bd, const double mus[4], bool check_bad);
+  Scaled scaled_of(const ErrEval& E, int k) const;
   bool attempt(double dw, const DevIter& it);  // one inertia-loop attempt (kkt.cpp:954-1001)
   void compute_step(const DevIter& it);         // solve_reduced (kkt.cpp:945-1006)
   double fetch1(const double* d);
@@ -106,6 +113,7 @@ class Solver {
   DArr<double> ft, gt, ht;  // line-search trial values
   DArr<double> partial, scal;
   DArr<int> flag;
+  DArr<unsigned int> eval_counter;
   double* pinned = nullptr;
   int corrections = 0, refinements = 0;
   double last_dw = 0;

@@ -57,6 +57,27 @@ __global__ void finalize_kernel(const double* partial, int nblocks, const int* o
   if (lane == 0) out[k] = a;
 }
 
+// Same reduction written to dst[0..K) (single-block use).
+template <int K>
+__device__ void block_reduce_to(double (&v)[K], const int (&op)[K], double* dst) {
+  __shared__ double sh2[K][kB / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+    for (int off = 16; off > 0; off >>= 1)
+      v[k] = combine(op[k], v[k], __shfl_xor_sync(0xffffffffu, v[k], off));
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < K; ++k) sh2[k][warp] = v[k];
+  __syncthreads();
+  if (threadIdx.x < K) {
+    const int k = threadIdx.x;
+    double a = ident(op[k]);
+    for (int w = 0; w < kB / 32; ++w) a = combine(op[k], a, sh2[k][w]);
+    dst[k] = a;
+  }
+}
+
 template <int K>
 void finalize(const double* partial, int nblocks, const int (&op)[K], double* out,
               cudaStream_t st) {
@@ -114,6 +135,104 @@ __global__ void __launch_bounds__(kB) kkt_error_xs_kernel(IpmDims d, DevIter it,
     }
   }
   block_partial<6>(v, ops, partial);
+}
+
+constexpr int kEvalXs = 11;
+__global__ void __launch_bounds__(kB) kkt_eval_kernel(IpmDims d, DevIter it, DevBounds b,
+                                                      const double* grad, const double* g,
+                                                      const double* h, const double* f,
+                                                      const int* bad, int lo,
+                                                      const double* gsum, double mu0, double mu1,
+                                                      double mu2, double mu3, double* partial,
+                                                      unsigned int* counter, double* out) {
+  constexpr int ops[kEvalXs] = {kMax, kMax, kMax, kMax, kMax, kMax, kMax, kMax, kSum, kSum, kMin};
+  const double mus[4] = {mu0, mu1, mu2, mu3};
+  double v[kEvalXs] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 1e300};
+  const long long nx = (long long)d.M * d.n_x, ns = (long long)d.M * d.m;
+  for (long long id = blockIdx.x * (long long)kB + threadIdx.x; id < nx + ns + d.M;
+       id += (long long)gridDim.x * kB) {
+    if (id < nx) {
+      const int s = int(id / d.n_x), i = int(id % d.n_x);
+      const double lo_ = b.xlo[i], up = b.xup[i], xv = it.x[id];
+      v[0] = fmax(v[0], fabs(grad[size_t(s) * d.n_d + i] - it.klo[id] + it.kup[id]));
+      v[2] = fmax(v[2], fabs(g[id]));
+      v[8] += fabs(it.y[id]);
+      if (isfinite(lo_)) {
+        const double p = (xv - lo_) * it.klo[id];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[4 + k] = fmax(v[4 + k], fabs(p - mus[k]));
+        v[8] += fabs(it.klo[id]);
+      }
+      if (isfinite(up)) {
+        const double p = (up - xv) * it.kup[id];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[4 + k] = fmax(v[4 + k], fabs(p - mus[k]));
+        v[8] += fabs(it.kup[id]);
+      }
+    } else if (id < nx + ns) {
+      const long long q = id - nx;
+      const int i = int(q % d.m);
+      const double lo_ = b.slo[i], up = b.sup[i], sv = it.s[q];
+      v[1] = fmax(v[1], fabs(it.z[q] - it.nlo[q] + it.nup[q]));
+      v[3] = fmax(v[3], fabs(h[q] + sv));
+      v[8] += fabs(it.z[q]);
+      if (isfinite(lo_)) {
+        const double p = (sv - lo_) * it.nlo[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[4 + k] = fmax(v[4 + k], fabs(p - mus[k]));
+        v[8] += fabs(it.nlo[q]);
+      }
+      if (isfinite(up)) {
+        const double p = (up - sv) * it.nup[q];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[4 + k] = fmax(v[4 + k], fabs(p - mus[k]));
+        v[8] += fabs(it.nup[q]);
+      }
+    } else {
+      const int s = int(id - nx - ns);
+      v[9] += f[s];
+      if (bad && bad[s]) v[10] = fmin(v[10], double(lo + s));
+    }
+  }
+  block_partial<kEvalXs>(v, ops, partial);
+  // last block: fixed-order combination of the partials, then the u part
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int k = warp; k < kEvalXs; k += kB / 32) {
+    const int op = ops[k];
+    double a = ident(op);
+    for (int blk = lane; blk < int(gridDim.x); blk += 32)
+      a = combine(op, a, ((volatile double*)partial)[size_t(blk) * kEvalXs + k]);
+    for (int off = 16; off > 0; off >>= 1) a = combine(op, a, __shfl_xor_sync(0xffffffffu, a, off));
+    if (lane == 0) out[k] = a;
+  }
+  constexpr int uops[6] = {kMax, kMax, kMax, kMax, kMax, kSum};
+  double u[6] = {0, 0, 0, 0, 0, 0};
+  for (int i = threadIdx.x; i < d.n_u; i += kB) {
+    const double lo_ = b.ulo[i], up = b.uup[i], uv = it.u[i];
+    u[0] = fmax(u[0], fabs(gsum[i] + (-it.llo[i] + it.lup[i])));
+    if (isfinite(lo_)) {
+      const double p = (uv - lo_) * it.llo[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[1 + k] = fmax(u[1 + k], fabs(p - mus[k]));
+      u[5] += fabs(it.llo[i]);
+    }
+    if (isfinite(up)) {
+      const double p = (up - uv) * it.lup[i];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) u[1 + k] = fmax(u[1 + k], fabs(p - mus[k]));
+      u[5] += fabs(it.lup[i]);
+    }
+  }
+  __syncthreads();
+  block_reduce_to<6>(u, uops, out + 11);
+  if (threadIdx.x == 0) *counter = 0u;  // reusable
 }
 
 __global__ void grad_u_sum_kernel(IpmDims d, const double* grad, double* gsum) {
@@ -732,6 +851,17 @@ void launch_kkt_error_xs(const IpmDims& d, const DevIter& it, const DevBounds& b
   const int ops[6] = {kMax, kMax, kMax, kMax, kMax, kSum};
   finalize<6>(partial, nb, ops, out6, st);
   check("kkt_error_xs");
+}
+
+void launch_kkt_eval(const IpmDims& d, const DevIter& it, const DevBounds& b, const double* grad,
+                     const double* g, const double* h, const double* f, const int* bad, int lo,
+                     const double* gsum_u, const double mus[4], double* partial,
+                     unsigned int* counter, double* out, cudaStream_t st) {
+  const int nb = red_blocks((long long)d.M * (d.n_x + d.m + 1));
+  kkt_eval_kernel<<<nb, kB, 0, st>>>(d, it, b, grad, g, h, f, bad, lo, gsum_u, mus[0], mus[1],
+                                     mus[2], mus[3], partial, counter, out);
+  note_launch();
+  check("kkt_eval");
 }
 
 void launch_grad_u_sum(const IpmDims& d, const double* grad, double* gsum, cudaStream_t st) {

@@ -51,6 +51,18 @@ void launch_grad_u_sum(const IpmDims& d, const double* grad, double* gsum_u, cud
 void launch_kkt_error_u(const IpmDims& d, const DevIter& it, const DevBounds& b,
                         const double* gsum_u, double mu, double* out3, cudaStream_t st);
 
+// Fused residual evaluation (assemble_residuals + scaled_error ingredients,
+// autodiff.cpp:441-482, ipm.cpp:345-379) for up to 4 barrier parameters in one
+// pass; the last block to finish combines the block partials in a fixed order
+// and adds the control part.  out[17]:
+//   0 max|stat_x|  1 max|stat_s|  2 max|g|  3 max|h+s|  4..7 comp(mu_k) x/s
+//   8 sum|mult| x/s  9 sum f  10 lowest non-finite global scenario (1e300: none)
+//   11 max|stat_u| 12..15 comp(mu_k) u  16 sum|lambda|
+void launch_kkt_eval(const IpmDims& d, const DevIter& it, const DevBounds& b, const double* grad,
+                     const double* g, const double* h, const double* f, const int* bad, int lo,
+                     const double* gsum_u, const double mus[4], double* partial,
+                     unsigned int* counter, double* out, cudaStream_t st);
+
 // ---- augmented / condensed systems -----------------------------------------
 // sigma_x, r1x, sigma_s, r2, r4 (kkt.cpp:83-99); *flag = 1 if not interior
 void launch_assemble_xs(const IpmDims& d, const DevIter& it, const DevBounds& b,
