@@ -76,7 +76,7 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
   ft.resize(size_t(d.M));
   gt.resize(nx);
   ht.resize(nm);
-  partial.resize(600 * 8);
+  partial.resize(600 * 16);  // up to 592 blocks x 16 reduction slots
   scal.resize(32);
   flag.resize(1);
   eval_counter.resize(1);
