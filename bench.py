@@ -199,6 +199,8 @@ def bench_ours(a, rank, world):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx2 = sharded_context(p, world, rank, device=dev, backend="nccl")
+    torch.cuda.synchronize()
+    t_ctx = time.perf_counter() - t0
     res = nat.Solver(ctx2).solve()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
@@ -228,7 +230,7 @@ def bench_ours(a, rank, world):
         "objective": res["objective"], "status": res["status_name"],
         "clocks": clk.summary(),
         "e2e": {"value": round(1e3 * e2e_s / iters, 4), "unit": "ms/iteration",
-                "total_s": round(e2e_s, 5),
+                "total_s": round(e2e_s, 5), "context_upload_s": round(t_ctx, 5),
                 "h2d_bytes_per_step": int((h1["h2d_bytes"] - h0["h2d_bytes"]) / iters),
                 "d2h_bytes_per_step": int((h1["d2h_bytes"] - h0["d2h_bytes"]) / iters)},
         "gpu_launches": int(c1["launches"] - c0["launches"]),

@@ -1,0 +1,250 @@
+// Blocked dense Cholesky of the reduced matrix K_hat (n_u x n_u, column-major,
+// lower) for n_u above the shared-memory kernel's range, with the trailing
+// update on the FP64 tensor pipe (mma.sync.m8n8k4.f64 -> SASS DMMA; tcgen05 has
+// no f64 kind).
+//
+// Reference: factor_dense_sym -> LAPACKE_dpotrf('L') (linalg.cpp:129-145,
+// lapack.cpp:26-31) after the 1e-13 max(1,|K|_inf) diagonal shift
+// (kkt.cpp:965-968); a pivot that is not > 0 (or NaN) fails the factor, which
+// is exactly when the reference's attempt is rejected (kkt.cpp:970-971).
+//
+// Per panel of kNb = 32 columns: (1) factor the diagonal block in shared
+// memory, (2) L21 = A21 L11^{-T} row-parallel, (3) A22 -= L21 L21' on the lower
+// triangle in 64 x 64 tiles, four warps of 32 x 32 DMMA fragments each.
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "kkt_kernels.hpp"
+#include "stats.hpp"
+
+namespace bipm {
+
+namespace {
+
+constexpr int kNb = 32;
+constexpr int kTile = 64;
+
+void check(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// |K|_inf then the diagonal shift; info reset
+__global__ void shift_kernel(double* K, int n, int* info) {
+  __shared__ double red[32];
+  double mx = 0.0;
+  for (long long i = threadIdx.x; i < (long long)n * n; i += blockDim.x) mx = fmax(mx, fabs(K[i]));
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.0;
+    for (int off = 16; off > 0; off >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double shift = 1e-13 * fmax(1.0, red[0]);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) K[size_t(i) * n + i] += shift;
+  if (threadIdx.x == 0) *info = 0;
+}
+
+// (1) diagonal block [c0, c0+w) in shared memory, one thread per row
+__global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
+  __shared__ double A[kNb][kNb + 1];
+  __shared__ int fail;
+  if (*info) return;
+  const int w = min(kNb, n - c0), r = threadIdx.x;
+  if (r < w)
+    for (int c = 0; c <= r; ++c) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
+  if (r == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < w; ++j) {
+    if (r == j) {
+      const double ajj = A[j][j];
+      if (!(ajj > 0.0) || isnan(ajj))
+        fail = c0 + j + 1;
+      else
+        A[j][j] = sqrt(ajj);
+    }
+    __syncthreads();
+    if (fail) break;
+    if (r > j && r < w) A[r][j] /= A[j][j];
+    __syncthreads();
+    if (r > j && r < w)
+      for (int k = j + 1; k <= r; ++k) A[r][k] -= A[r][j] * A[k][j];
+    __syncthreads();
+  }
+  if (fail) {
+    if (r == 0) *info = fail;
+    return;
+  }
+  if (r < w)
+    for (int c = 0; c <= r; ++c) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
+}
+
+// (2) L21 = A21 L11^{-T}: one thread per row below the panel
+__global__ void panel_trsm_kernel(double* K, int n, int c0, const int* info) {
+  __shared__ double L[kNb][kNb + 1];
+  if (*info) return;
+  const int w = min(kNb, n - c0);
+  for (int q = threadIdx.x; q < w * w; q += blockDim.x) {
+    const int rr = q / w, cc = q % w;
+    L[rr][cc] = cc <= rr ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
+  }
+  __syncthreads();
+  const int r = c0 + w + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[kNb];
+#pragma unroll
+  for (int j = 0; j < kNb; ++j) x[j] = j < w ? K[size_t(c0 + j) * n + r] : 0.0;
+#pragma unroll
+  for (int j = 0; j < kNb; ++j) {
+    if (j >= w) break;
+    double v = x[j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) v -= x[k] * L[j][k];
+    x[j] = v / L[j][j];
+  }
+#pragma unroll
+  for (int j = 0; j < kNb; ++j)
+    if (j < w) K[size_t(c0 + j) * n + r] = x[j];
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// (3) A22 -= L21 L21' on lower tiles (I >= J) of the trailing matrix
+__global__ void __launch_bounds__(128) panel_update_kernel(double* K, int n, int c0,
+                                                           const int* info) {
+  __shared__ double sa[kTile][kNb + 1];
+  __shared__ double sb[kTile][kNb + 1];
+  if (*info) return;
+  const int t0 = c0 + kNb;  // trailing start
+  // lower-triangle tile enumeration: blockIdx.x -> (I, J), I >= J
+  int I = int((sqrt(8.0 * blockIdx.x + 1.0) - 1.0) / 2.0);
+  while ((I + 1) * (I + 2) / 2 <= int(blockIdx.x)) ++I;
+  while (I * (I + 1) / 2 > int(blockIdx.x)) --I;
+  const int J = int(blockIdx.x) - I * (I + 1) / 2;
+  const int r0 = t0 + I * kTile, s0 = t0 + J * kTile;
+  for (int q = threadIdx.x; q < kTile * kNb; q += 128) {
+    const int rr = q % kTile, kk = q / kTile;  // coalesced along rows
+    const int ra = r0 + rr, rb = s0 + rr;
+    sa[rr][kk] = ra < n ? K[size_t(c0 + kk) * n + ra] : 0.0;
+    sb[rr][kk] = rb < n ? K[size_t(c0 + kk) * n + rb] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp sub-tile
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b2 = 0; b2 < 4; ++b2) acc[a][b2][0] = acc[a][b2][1] = 0.0;
+  const int gm = lane >> 2, gk = lane & 3;
+#pragma unroll
+  for (int k = 0; k < kNb; k += 4) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) af[a] = sa[wm + a * 8 + gm][k + gk];
+#pragma unroll
+    for (int b2 = 0; b2 < 4; ++b2) bf[b2] = sb[wn + b2 * 8 + gm][k + gk];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b2 = 0; b2 < 4; ++b2) dmma(acc[a][b2][0], acc[a][b2][1], af[a], bf[b2]);
+  }
+  // C fragment: row gm, cols 2*gk + {0,1}
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int r = r0 + wm + a * 8 + gm, c = s0 + wn + b2 * 8 + 2 * gk + v;
+        if (r < n && c < n && c <= r) K[size_t(c) * n + r] -= acc[a][b2][v];
+      }
+}
+
+// L L' x = b, blocked by 32 rows: one warp solves each diagonal triangle by
+// shuffles, the CTA updates the remaining rows.
+__global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __restrict__ L, int n,
+                                                            double* b) {
+  extern __shared__ double x[];  // n
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < n; c0 += 32) {  // forward
+    const int w = min(32, n - c0);
+    if (warp == 0) {
+      double xv = lane < w ? x[c0 + lane] : 0.0;
+      for (int j = 0; j < w; ++j) {
+        if (lane == j) xv /= L[size_t(c0 + j) * n + c0 + j];
+        const double xj = __shfl_sync(0xffffffffu, xv, j);
+        if (lane > j && lane < w) xv -= L[size_t(c0 + j) * n + c0 + lane] * xj;
+      }
+      if (lane < w) x[c0 + lane] = xv;
+    }
+    __syncthreads();
+    for (int i = c0 + w + threadIdx.x; i < n; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < w; ++j) acc += L[size_t(c0 + j) * n + i] * x[c0 + j];
+      x[i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int c0 = ((n - 1) / 32) * 32; c0 >= 0; c0 -= 32) {  // backward with L'
+    const int w = min(32, n - c0);
+    if (warp == 0) {
+      double xv = lane < w ? x[c0 + lane] : 0.0;
+      for (int j = w - 1; j >= 0; --j) {
+        if (lane == j) xv /= L[size_t(c0 + j) * n + c0 + j];
+        const double xj = __shfl_sync(0xffffffffu, xv, j);
+        if (lane < j) xv -= L[size_t(c0 + lane) * n + c0 + j] * xj;
+      }
+      if (lane < w) x[c0 + lane] = xv;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < c0; i += blockDim.x) {
+      double acc = 0.0;
+      for (int j = 0; j < w; ++j) acc += L[size_t(i) * n + c0 + j] * x[c0 + j];
+      x[i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = x[i];
+}
+
+}  // namespace
+
+void launch_blocked_cholesky(double* K, int n, int* info, cudaStream_t st) {
+  shift_kernel<<<1, 1024, 0, st>>>(K, n, info);
+  note_launch();
+  for (int c0 = 0; c0 < n; c0 += kNb) {
+    diag_factor_kernel<<<1, kNb, 0, st>>>(K, n, c0, info);
+    const int rows = n - c0 - kNb;
+    if (rows > 0) {
+      panel_trsm_kernel<<<(rows + 127) / 128, 128, 0, st>>>(K, n, c0, info);
+      const int nt = (rows + kTile - 1) / kTile;
+      panel_update_kernel<<<nt * (nt + 1) / 2, 128, 0, st>>>(K, n, c0, info);
+      note_launch(3);
+    } else {
+      note_launch(1);
+    }
+  }
+  check("blocked_cholesky");
+}
+
+void launch_blocked_solve(const double* L, int n, double* b, cudaStream_t st) {
+  const size_t smem = size_t(n) * sizeof(double);
+  cudaFuncSetAttribute(blocked_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  blocked_solve_kernel<<<1, 1024, smem, st>>>(L, n, b);
+  note_launch();
+  check("blocked_solve");
+}
+
+}  // namespace bipm

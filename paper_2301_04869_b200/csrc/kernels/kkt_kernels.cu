@@ -526,67 +526,6 @@ __global__ void cholesky_solve_warp_kernel(const double* __restrict__ L, int n, 
     if (q * 32 + lane < n) b[q * 32 + lane] = x[q];
 }
 
-// ---------------------------------------------------------- dense Cholesky
-__global__ void __launch_bounds__(kDenseBlock) shift_cholesky_kernel(double* K, int n, int* info) {
-  __shared__ int fail;
-  double mx = 0.0;
-  for (long long i = threadIdx.x; i < (long long)n * n; i += kDenseBlock) mx = fmax(mx, fabs(K[i]));
-  mx = block_reduce<kDenseBlock>(mx, true);
-  const double shift = 1e-13 * fmax(1.0, mx);
-  for (int i = threadIdx.x; i < n; i += kDenseBlock) K[size_t(i) * n + i] += shift;
-  if (threadIdx.x == 0) fail = 0;
-  __syncthreads();
-  for (int j = 0; j < n; ++j) {
-    double d = 0.0;
-    for (int k = threadIdx.x; k < j; k += kDenseBlock) {
-      const double l = K[size_t(k) * n + j];
-      d += l * l;
-    }
-    d = block_reduce<kDenseBlock>(d, false);
-    if (threadIdx.x == 0) {
-      const double ajj = K[size_t(j) * n + j] - d;
-      if (!(ajj > 0.0) || isnan(ajj)) {
-        fail = j + 1;
-      } else {
-        K[size_t(j) * n + j] = sqrt(ajj);
-      }
-    }
-    __syncthreads();
-    if (fail) break;
-    const double ljj = K[size_t(j) * n + j];
-    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) {
-      double v = K[size_t(j) * n + i];
-      for (int k = 0; k < j; ++k) v -= K[size_t(k) * n + i] * K[size_t(k) * n + j];
-      K[size_t(j) * n + i] = v / ljj;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *info = fail;
-}
-
-__global__ void __launch_bounds__(kDenseBlock) cholesky_solve_kernel(const double* L, int n, double* b) {
-  __shared__ double xj;
-  // forward: L y = b (column-oriented)
-  for (int j = 0; j < n; ++j) {
-    if (threadIdx.x == 0) {
-      xj = b[j] / L[size_t(j) * n + j];
-      b[j] = xj;
-    }
-    __syncthreads();
-    const double y = xj;
-    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) b[i] -= L[size_t(j) * n + i] * y;
-    __syncthreads();
-  }
-  // backward: L' x = y
-  for (int j = n - 1; j >= 0; --j) {
-    double d = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < n; i += kDenseBlock) d += L[size_t(j) * n + i] * b[i];
-    d = block_reduce<kDenseBlock>(d, false);
-    if (threadIdx.x == 0) b[j] = (b[j] - d) / L[size_t(j) * n + j];
-    __syncthreads();
-  }
-}
-
 void check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
@@ -755,11 +694,11 @@ void launch_shift_cholesky(double* K, int n, int* info, double*, cudaStream_t st
     cudaFuncSetAttribute(shift_cholesky_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(size_t(n) * n * sizeof(double)));
     shift_cholesky_small_kernel<<<1, kDenseBlock, size_t(n) * n * sizeof(double), st>>>(K, n, info);
+    note_launch();
+    check_launch("shift_cholesky");
   } else {
-    shift_cholesky_kernel<<<1, kDenseBlock, 0, st>>>(K, n, info);
+    launch_blocked_cholesky(K, n, info, st);  // DMMA trailing updates (dense_chol.cu)
   }
-  note_launch();
-  check_launch("shift_cholesky");
 }
 
 void launch_cholesky_solve(const double* L, int n, double* b, cudaStream_t st) {
@@ -769,8 +708,10 @@ void launch_cholesky_solve(const double* L, int n, double* b, cudaStream_t st) {
     cholesky_solve_warp_kernel<4><<<1, 32, 0, st>>>(L, n, b);
   else if (n <= 256)
     cholesky_solve_warp_kernel<8><<<1, 32, 0, st>>>(L, n, b);
-  else
-    cholesky_solve_kernel<<<1, kDenseBlock, 0, st>>>(L, n, b);
+  else {
+    launch_blocked_solve(L, n, b, st);
+    return;
+  }
   note_launch();
   check_launch("cholesky_solve");
 }

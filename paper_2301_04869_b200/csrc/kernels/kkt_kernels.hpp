@@ -84,5 +84,8 @@ void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, cons
 // info (device int): 0 when positive definite, else 1 + failing column.
 void launch_shift_cholesky(double* K, int n, int* info, double* work, cudaStream_t st);
 void launch_cholesky_solve(const double* Lfac, int n, double* b, cudaStream_t st);
+// n above the shared-memory kernel's range (dense_chol.cu)
+void launch_blocked_cholesky(double* K, int n, int* info, cudaStream_t st);
+void launch_blocked_solve(const double* L, int n, double* b, cudaStream_t st);
 
 }  // namespace bipm
