@@ -184,7 +184,13 @@ int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* cou
 int bipm_ctx_phase_stamps(bipm_ctx* c, int32_t enable, int64_t out[16]);
 /* out = reduce tile width, scenarios per CTA, chunks, panel-in-smem, nnz(L),
  * nnz(L+U), LU multiply-adds, SM count */
-int bipm_ctx_info(bipm_ctx* c, int64_t out[8]);
+int bipm_ctx_info(bipm_ctx* c, int64_t out[12]);
+/* debug: (step kind, clock64 before its data wait, after it) of every step of
+   the streamed reduction's first scenario in CTA (0,0) from the previous
+   reduction; n_out triples written */
+/* debug: raw copy of the reduction's stamp/trace buffer */
+int bipm_ctx_debug_buffer(bipm_ctx* c, int64_t* out, int64_t cap, int64_t* n_out);
+int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap, int32_t* n_out);
 /* factor_dense_sym + solve (linalg.hpp:116, kkt.cpp:965-976): K (n x n,
  * column-major) shifted by 1e-13 max(1,|K|_inf), Cholesky; *pd = 1 when
  * positive definite, then rhs is overwritten by K^{-1} rhs */

@@ -86,6 +86,10 @@ SIGNATURES = {
                                          ctypes.c_int32]),
     "bipm_ctx_set_host_comm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32]),
     "bipm_ctx_phase_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_ctx_debug_buffer": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                             ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_ctx_step_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
+                                            ctypes.c_int32, _I]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -269,11 +273,25 @@ class Context:
         check(lib().bipm_ctx_phase_stamps(self._h, 1 if enable else 0, out))
         return list(out)
 
+    def step_stamps(self, enable: bool, cap: int = 8192):
+        """(kind, clock64 before the step's data wait, after it) per step of the
+        streamed reduction (debug)."""
+        out = (ctypes.c_int64 * cap)()
+        n = ctypes.c_int32(0)
+        check(lib().bipm_ctx_step_stamps(self._h, 1 if enable else 0, out, cap, ctypes.byref(n)))
+        return [(out[3 * j], out[3 * j + 1], out[3 * j + 2]) for j in range(n.value)]
+
+    def debug_buffer(self, cap: int = 200000):
+        out = (ctypes.c_int64 * cap)()
+        n = ctypes.c_int64(0)
+        check(lib().bipm_ctx_debug_buffer(self._h, out, cap, ctypes.byref(n)))
+        return list(out[:n.value])
+
     def info(self) -> dict:
-        out = (ctypes.c_int64 * 8)()
+        out = (ctypes.c_int64 * 12)()
         check(lib().bipm_ctx_info(self._h, out))
         keys = ("tile_cols", "chunk", "nchunks", "panel_in_smem", "nnz_l", "nnz_f", "lu_madds",
-                "sm_count")
+                "sm_count", "streamed", "steps", "ring_bytes", "nnz_vs")
         return dict(zip(keys, list(out)))
 
     def __del__(self):

@@ -352,17 +352,59 @@ int bipm_ctx_phase_stamps(bipm_ctx* c, int32_t enable, int64_t out[16]) {
   });
 }
 
-int bipm_ctx_info(bipm_ctx* c, int64_t out[8]) {
+int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap,
+                         int32_t* n_out) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    const int P = e.use_stream ? e.sprog.steps : 0;
+    if (n_out) *n_out = 0;
+    if (out && e.phase.size() && P > 0) {
+      // (kind, clock64 before the data wait, clock64 after it) per step, then the end stamp
+      std::vector<long long> st(e.phase.size());
+      e.phase.download(st.data(), st.size(), e.st);
+      e.sync();
+      const int n = std::min<int>(cap / 3, P + 1);
+      for (int j = 0; j < n; ++j) {
+        out[3 * j] = j < P ? e.sprog.pat[size_t(e.sprog.issue[size_t(j)].pat_off)] : -1;
+        out[3 * j + 1] = st[size_t(2 * j)];
+        out[3 * j + 2] = j < P ? st[size_t(2 * j + 1)] : st[size_t(2 * j)];
+      }
+      if (n_out) *n_out = n;
+    }
+    if (enable) {
+      e.phase.resize(size_t(std::max(16, 2 * P + 2 + 60000)));
+      e.phase.zero(e.st);
+    } else {
+      e.phase.resize(0);
+    }
+  });
+}
+
+int bipm_ctx_debug_buffer(bipm_ctx* c, int64_t* out, int64_t cap, int64_t* n_out) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    const size_t n = std::min<size_t>(size_t(cap), e.phase.size());
+    if (n) e.phase.download(reinterpret_cast<long long*>(out), n, e.st);
+    e.sync();
+    *n_out = int64_t(n);
+  });
+}
+
+int bipm_ctx_info(bipm_ctx* c, int64_t out[12]) {
   return guarded([&] {
     const Engine& e = *c->eng;
-    out[0] = e.red.kc;
-    out[1] = e.red.chunk;
-    out[2] = e.red.nchunks;
-    out[3] = e.red.panel_in_smem ? 1 : 0;
+    out[0] = e.use_stream ? e.sl.K : e.red.kc;
+    out[1] = e.use_stream ? e.sl.chunk : e.red.chunk;
+    out[2] = e.use_stream ? e.sl.nchunks : e.red.nchunks;
+    out[3] = e.use_stream ? 1 : (e.red.panel_in_smem ? 1 : 0);
     out[4] = e.pb.LU.nnz_l;
     out[5] = e.pb.LU.nnz_f;
     out[6] = (int64_t)e.pb.LU.mul_l.size();
     out[7] = e.sm_count;
+    out[8] = e.use_stream ? 1 : 0;
+    out[9] = e.use_stream ? e.sprog.steps : 0;
+    out[10] = e.use_stream ? e.sl.ring_bytes : 0;
+    out[11] = e.use_stream ? e.sprog.nnz_vs : 0;
   });
 }
 

@@ -1,6 +1,8 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 namespace bipm {
 
@@ -147,10 +149,11 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
     b.grad.resize(Ms * size_t(Mo.n_d()));
   }
   upload_ad();
-  kxx.resize(Ms * nnz(D.kxx.out));
+  // +2: the streamed reduction's bulk copies start on a 16-byte boundary
+  kxx.resize(Ms * nnz(D.kxx.out) + 2);
   kxu.resize(Ms * nnz(D.kxu.out));
   kuu.resize(Ms * nnz(D.kuu.out));
-  sigma_x.resize(Ms * size_t(Mo.n_x));
+  sigma_x.resize(Ms * size_t(Mo.n_x) + 2);
   rhat1.resize(Ms * size_t(Mo.n_x));
   rhat3.resize(Ms * size_t(Mo.n_x));
   sigma_s.resize(Ms * size_t(Mo.m));
@@ -160,7 +163,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   rhat2.resize(size_t(Mo.n_u));
   F.resize(Ms * size_t(L.nnz_f));
   FT.resize(Ms * size_t(L.nnz_f));
-  Dt.resize(std::max<size_t>(1, Ms * 2 * size_t(L.tl) * size_t(L.tl)));
+  Dt.resize(std::max<size_t>(1, Ms * 2 * size_t(L.tl) * size_t(L.tl)) + 2);
   lu_status.resize(Ms);
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));
@@ -176,8 +179,99 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   red.n_u = Mo.n_u;
   red.M = M;
   plan_reduce_launch(red, 200 * 1024, sm_count);
-  red_partial.resize(size_t(red.nchunks) * Mo.n_u * Mo.n_u);
-  red_scratch.resize(reduce_scratch_doubles(red));
+  if (const char* e = std::getenv("BIPM_REDUCE")) use_stream = std::strcmp(e, "tiles") != 0;
+  if (use_stream) setup_stream();
+  if (use_stream) {
+    red_parts = sl.nchunks + 1;  // + the K_uu slab
+    red_partial.resize(size_t(red_parts) * Mo.n_u * Mo.n_u);
+    red_partial.zero(st);
+  } else {
+    red_parts = red.nchunks;
+    red_partial.resize(size_t(red.nchunks) * Mo.n_u * Mo.n_u);
+    red_scratch.resize(reduce_scratch_doubles(red));
+  }
+}
+
+void Engine::setup_stream() {
+  const DerivPlan& D = pb.D;
+  const LuPlan& L = pb.LU;
+  const int n_x = pb.M.n_x, n_u = pb.M.n_u;
+  // widest power-of-two tile whose panel leaves a useful ring (>= 40 KB)
+  int cap = 1;
+  while (cap < 32 && cap < n_u) cap *= 2;
+  const Csr gut = D.g.u.transpose_pattern(), kxut = D.kxu.out.transpose_pattern();
+  if (const char* e = std::getenv("BIPM_STREAM_K")) cap = std::max(1, std::min(cap, std::atoi(e)));
+  int K = cap;
+  int ring = 0, list_cap = 0;
+  for (; K >= 1; K /= 2) {
+    if ((size_t(n_u) * K + kStreamConsumers - 1) / kStreamConsumers > kStreamMaxQ) continue;
+    list_cap = 0;
+    for (int j0 = 0; j0 < n_u; j0 += K) {
+      const int j1 = std::min(n_u, j0 + K);
+      const int a = gut.ptr[size_t(j1)] - gut.ptr[size_t(j0)];
+      const int b = kxut.ptr[size_t(j1)] - kxut.ptr[size_t(j0)];
+      list_cap = std::max(list_cap, ((a + 1) & ~1) + ((b + 1) & ~1));
+    }
+    ring = stream_ring_capacity(n_x, K, L.tl, 4096, list_cap);
+    if (ring >= 40 * 1024) break;
+  }
+  if (K < 1) {
+    use_stream = false;  // panel does not fit: tile kernel with a global panel
+    return;
+  }
+  sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, kStreamConsumers, ring,
+                               kStreamLookahead);
+  sp_pat.upload(sprog.pat);
+  {
+    std::vector<int> iss;
+    iss.reserve(sprog.issue.size() * 12);
+    for (const StepIssue& is : sprog.issue) {
+      const int r[12] = {is.pat_off, is.pat_bytes, is.ring_off, is.val_arr, is.val_off,
+                         is.val_count, is.x_arr, is.x_off, is.x_count, is.val_ring, is.x_ring,
+                         is.wait_delta};
+      iss.insert(iss.end(), r, r + 12);
+    }
+    sp_issue.upload(iss);
+  }
+  sp_ring.upload(sprog.ring_off);
+  sp_vs_src.upload(sprog.vs_src);
+  sp_kxu_slot.upload(sprog.kxu_t_slot.empty() ? std::vector<idx>{0} : sprog.kxu_t_slot);
+  sp_gu_slot.upload(sprog.gu_t_slot.empty() ? std::vector<idx>{0} : sprog.gu_t_slot);
+  {
+    const Csr& ku = D.kuu.out;
+    std::vector<idx> r(size_t(ku.nnz())), c(ku.ind.begin(), ku.ind.end());
+    for (idx i = 0; i < ku.rows; ++i)
+      for (idx k = ku.ptr[size_t(i)]; k < ku.ptr[size_t(i) + 1]; ++k) r[size_t(k)] = i;
+    if (r.empty()) r.push_back(0), c.push_back(0);
+    kuu_row.upload(r);
+    kuu_col.upload(c);
+  }
+  const size_t Ms = size_t(M);
+  VS.resize(Ms * size_t(sprog.nnz_vs) + 2);
+  kxu_t.resize(Ms * nnz(D.kxu.out) + 2);
+  gu_t.resize(Ms * nnz(D.g.u) + 2);
+
+  sl.n_x = n_x;
+  sl.n_u = n_u;
+  sl.M = M;
+  sl.K = K;
+  sl.nq = sprog.nq;
+  sl.steps = sprog.steps;
+  sl.ring_bytes = ring;
+  sl.t0 = L.t0;
+  sl.tl = L.tl;
+  sl.list_cap = list_cap;
+  plan_stream_chunks(sl, sm_count);
+  sl.pat = sp_pat.get();
+  sl.issue = sp_issue.get();
+  sl.ring_off = sp_ring.get();
+  for (int k = 0; k < kStreamArrays; ++k) sl.stride[k] = sprog.stride[k];
+  sl.gu = gu_p.v;
+  sl.kxu = kxu_p.v;
+  sl.kuu = kuu_p.v;
+  sl.iperm = lu.iperm;
+  const int tiles = (n_u + K - 1) / K;
+  sp_scratch.resize(size_t(tiles) * sl.nchunks * n_x * K);
 }
 
 Engine::~Engine() {
@@ -194,14 +288,16 @@ void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 void Engine::factor_gx_launch() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
-                       lu_status.get(), 1e-12, st);
+                       lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
+                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr, st);
   });
 }
 
 idx Engine::factor_gx() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
-                       lu_status.get(), 1e-12, st);
+                       lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
+                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr, st);
   });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
@@ -227,6 +323,39 @@ void Engine::condense_launch() {
 }
 
 void Engine::reduce_local(double dw) {
+  if (use_stream) {
+    const DerivPlan& D = pb.D;
+    const int n_u = pb.M.n_u;
+    double* kuu_part = red_partial.get() + size_t(sl.nchunks) * n_u * n_u;
+    timed("reduce_tiles", [&] {
+      launch_gather_values(kxu.get(), nnz(D.kxu.out), sp_kxu_slot.get(), int(nnz(D.kxu.out)),
+                           kxu_t.get(), nnz(D.kxu.out), M, st);
+      launch_gather_values(bd().gu.get(), nnz(D.g.u), sp_gu_slot.get(), int(nnz(D.g.u)),
+                           gu_t.get(), nnz(D.g.u), M, st);
+      launch_kuu_sum(kuu.get(), nnz(D.kuu.out), kuu_row.get(), kuu_col.get(),
+                     int(nnz(D.kuu.out)), M, n_u, kuu_part, st);
+      sl.arr[kArrSweep] = VS.get();
+      sl.arr[kArrDense] = Dt.get();
+      sl.arr[kArrKxx] = kxx.get();
+      sl.arr[kArrKxuT] = kxu_t.get();
+      sl.arr[kArrGuT] = gu_t.get();
+      sl.arr[kArrSigma] = sigma_x.get();
+      sl.gu_v = bd().gu.get();
+      sl.kxu_v = kxu.get();
+      sl.kuu_v = kuu.get();
+      sl.dw = dw;
+      sl.partial = red_partial.get();
+      sl.scratch = sp_scratch.get();
+      sl.phase = phase.size() ? phase.get() : nullptr;
+      static const int dbg = [] {
+        const char* e = std::getenv("BIPM_STREAM_DEBUG");
+        return e ? std::atoi(e) : 0;
+      }();
+      sl.debug = dbg;
+      launch_reduce_stream(sl, st);
+    });
+    return;
+  }
   red.F = F.get();
   red.FT = FT.get();
   red.D = Dt.get();
@@ -272,12 +401,12 @@ void Engine::finish_reduce(double dw) {
   const int n_u = pb.M.n_u;
   const long long nn = (long long)n_u * n_u;
   if (!multi()) {
-    launch_sum_parts(red_partial.get(), red.nchunks, nn, khat.get(), sigma_u.get(), dw, n_u,
+    launch_sum_parts(red_partial.get(), red_parts, nn, khat.get(), sigma_u.get(), dw, n_u,
                      nullptr, st);
     return;
   }
   // local sum -> all-reduce over the scenario groups -> diagonal terms once
-  launch_sum_parts(red_partial.get(), red.nchunks, nn, khat.get(), nullptr, 0.0, 0, nullptr, st);
+  launch_sum_parts(red_partial.get(), red_parts, nn, khat.get(), nullptr, 0.0, 0, nullptr, st);
   comm->allreduce(khat.get(), size_t(nn), RedOpKind::kSum, st);
   launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st);
 }

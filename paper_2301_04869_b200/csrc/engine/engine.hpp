@@ -15,8 +15,10 @@
 #include "../host/ad_plan.hpp"
 #include "../host/grid_model.hpp"
 #include "../host/plan.hpp"
+#include "../host/stream_plan.hpp"
 #include "../kernels/ad_launch.hpp"
 #include "../kernels/kkt_kernels.hpp"
+#include "../kernels/reduce_stream.hpp"
 #include "comm.hpp"
 #include "device_array.hpp"
 
@@ -89,7 +91,15 @@ class Engine {
   DArr<double> sigma_u, rhat2;                 // n_u (replicated)
   DArr<double> F, FT, Dt;                      // LU factors [M][nnz_f], transposed, dense tails
   DArr<int> lu_status;
-  // ---- reduction workspace
+  // ---- streamed reduction (reduce_stream.cu): step program, sweep-ordered
+  // factor values, column-order K_xu / G_u copies
+  bool use_stream = true;
+  StreamProgram sprog;
+  StreamLaunch sl{};
+  DArr<int> sp_pat, sp_issue, sp_ring, sp_vs_src, sp_kxu_slot, sp_gu_slot, kuu_row, kuu_col;
+  DArr<double> VS, kxu_t, gu_t, sp_scratch;
+  int red_parts = 0;  // partial K_hat slabs summed by finish_reduce
+  // ---- reduction workspace (tile kernel, BIPM_REDUCE=tiles)
   ReduceLaunch red{};
   DArr<double> red_partial, red_scratch, rhs_part;
   DArr<double> khat, rhs;   // n_u x n_u (column-major), n_u
@@ -131,6 +141,7 @@ class Engine {
 
   void sync();
   void upload_ad();
+  void setup_stream();
 
   // optional CUDA-event timing of named kernel groups on the engine stream
   struct KTimer {

@@ -1,0 +1,362 @@
+#include "stream_plan.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace bipm {
+
+namespace {
+
+int round16(int bytes) { return (bytes + 15) & ~15; }
+int val_alloc(int count) { return count > 0 ? round16((count + 1) * 8) : 0; }
+
+struct Builder {
+  StreamProgram& S;
+  const int max_bytes;
+  int warp_rr = 0;  // round-robin position of the next unit chunk (all-warp steps)
+  int last_team = 16;
+  struct Pending {
+    int kind, flags, aux0, aux1;
+    std::vector<int> items;  // 4 ints per item
+    std::vector<int> col;
+    int val_arr = -1, val_off = 0, val_count = 0;
+    int x_arr = -1, x_off = 0, x_count = 0;
+    std::vector<int> levels;  // sweep steps: 4 ints per level (unit_begin, unit_end, lg, barrier)
+  };
+
+  static int pat_bytes(int n_items, int n_ent, int n_lev = 0) {
+    return 4 * kStepHeaderInts + 16 * n_lev + 16 * n_items + 4 * ((n_ent + 3) & ~3);
+  }
+  // lanes per work unit: all units in one pass of `lanes` threads, and at
+  // least ~3 entries per lane
+  static int lanes_log2(int units, int max_ent, int lanes) {
+    static const int per_lane = [] {
+      const char* e = std::getenv("BIPM_LANE_ENT");
+      return e ? std::max(1, std::atoi(e)) : 3;
+    }();
+    int lg = 0;
+    while (lg < 5 && units * (2 << lg) <= lanes && (2 << lg) * per_lane <= max_ent) ++lg;
+    return lg;
+  }
+  static int step_bytes(int n_items, int n_ent, int vcount, int xcount, int n_lev = 0) {
+    return pat_bytes(n_items, n_ent, n_lev) + val_alloc(vcount) + val_alloc(xcount);
+  }
+
+  void emit(Pending p) {
+    const int K = S.K, NG = K > 8 ? K / 8 : 1;
+    const int n_items = int(p.items.size() / 4);
+    const int n_lev = int(p.levels.size() / 4);
+    const int n_col = (int(p.col.size()) + 3) & ~3;
+    StepIssue is{};
+    is.pat_off = int(S.pat.size());
+    is.pat_bytes = pat_bytes(n_items, int(p.col.size()), n_lev);
+    const int par = (p.val_count > 0 ? ((p.val_off & 1) | (int(S.stride[p.val_arr] & 1) << 1)) : 0) |
+                    (p.x_count > 0 ? (((p.x_off & 1) << 2) | (int(S.stride[p.x_arr] & 1) << 3)) : 0);
+    // work units and lanes of the all-warp steps; rows become panel words
+    int units = 0, lg = 0, max_ent = 0;
+    for (int it = 0; it < n_items; ++it)
+      max_ent = std::max(max_ent, p.items[size_t(it) * 4 + 2] - p.items[size_t(it) * 4 + 1]);
+    if (p.kind == kStepSpmv) {
+      units = n_items * NG;
+      lg = lanes_log2(units, max_ent, S.consumers);
+    } else if (p.kind == kStepDense) {
+      units = p.aux1 * NG;
+      lg = lanes_log2(units, p.val_count / std::max(1, p.aux1), S.consumers);
+    }
+    if (p.kind == kStepSweep || p.kind == kStepSpmv)
+      for (int it = 0; it < n_items; ++it)
+        p.items[size_t(it) * 4] = panel_word(p.items[size_t(it) * 4], K);
+    if (p.kind == kStepSweep || p.kind == kStepSpmv || p.kind == kStepAcc)
+      for (int& c : p.col) c = panel_word(c, K);
+    const int warp0 = warp_rr;
+    if (units > 0) {
+      const int upw = 32 >> lg;
+      warp_rr = (warp_rr + (units + upw - 1) / upw) % (S.consumers / 32);
+    }
+    int hdr[kStepHeaderInts] = {p.kind, p.flags, n_items, n_col, p.aux0, p.aux1, p.val_count,
+                                par, lg, units, warp0, n_lev};
+    S.pat.insert(S.pat.end(), hdr, hdr + kStepHeaderInts);
+    S.pat.insert(S.pat.end(), p.levels.begin(), p.levels.end());
+    S.pat.insert(S.pat.end(), p.items.begin(), p.items.end());
+    S.pat.insert(S.pat.end(), p.col.begin(), p.col.end());
+    S.pat.resize(S.pat.size() + size_t(n_col - int(p.col.size())), 0);
+    is.val_arr = p.val_count > 0 ? p.val_arr : 0;
+    is.val_off = p.val_off;
+    is.val_count = p.val_count;
+    is.x_arr = p.x_count > 0 ? p.x_arr : 0;
+    is.x_off = p.x_off;
+    is.x_count = p.x_count;
+    S.issue.push_back(is);
+  }
+
+  // One triangular sweep (its levels, then optionally the tail gather as one
+  // more level).  Each level gets a team: the lowest T warps, T a power of two
+  // sized to its units x lanes; consecutive levels with the same team and
+  // diagonal mode share a step and are separated by team barriers (named
+  // barrier, or __syncwarp for one warp).  Values are appended to VS.
+  void sweep(const SweepPlan& sw, const std::vector<idx>& slot_of_t, bool diag, bool with_tail,
+             int tail_skip) {
+    const int K = S.K, NG = K > 8 ? K / 8 : 1;
+    struct Unit { idx row, b, e; };
+    std::vector<std::vector<Unit>> levels;
+    std::vector<char> level_diag;
+    const idx nl = idx(sw.lvl_ptr.size()) - 1;
+    for (idx l = 0; l < nl; ++l) {
+      std::vector<Unit> us;
+      for (idx it = sw.lvl_ptr[size_t(l)]; it < sw.lvl_ptr[size_t(l) + 1]; ++it) {
+        const idx row = sw.items[size_t(it) * 4], b = sw.items[size_t(it) * 4 + 1],
+                  e = sw.items[size_t(it) * 4 + 2];
+        if (!diag && e <= b) continue;  // nothing to subtract
+        us.push_back({row, b, e});
+      }
+      if (!us.empty()) {
+        levels.push_back(std::move(us));
+        level_diag.push_back(diag);
+      }
+    }
+    if (with_tail) {  // the tail rows are independent of each other
+      std::vector<Unit> us;
+      for (size_t it = 0; it < sw.tail_items.size() / 4; ++it) {
+        const idx row = sw.tail_items[it * 4], b = sw.tail_items[it * 4 + 1] + tail_skip,
+                  e = sw.tail_items[it * 4 + 2];
+        if (e > b) us.push_back({row, b, e});
+      }
+      if (!us.empty()) {
+        levels.push_back(std::move(us));
+        level_diag.push_back(false);
+      }
+    }
+    Pending p{kStepSweep, 0, 0, 0, {}, {}};
+    std::vector<idx> slots;
+    int cur_team = -1;
+    bool cur_diag = false;
+    auto flush = [&] {
+      if (p.items.empty()) return;
+      p.flags = (cur_diag ? kFlagDiag : 0) | (cur_team != last_team ? kFlagPre : 0);
+      p.aux0 = cur_team;
+      last_team = cur_team;
+      if (S.vs_src.size() & 1) S.vs_src.push_back(-1);
+      p.val_arr = kArrSweep;
+      p.val_off = int(S.vs_src.size());
+      p.val_count = int(p.col.size());
+      S.vs_src.insert(S.vs_src.end(), slots.begin(), slots.end());
+      emit(p);
+      ++S.n_sweep_steps;
+      p.items.clear();
+      p.col.clear();
+      p.levels.clear();
+      slots.clear();
+    };
+    for (size_t l = 0; l < levels.size(); ++l) {
+      const auto& us = levels[l];
+      const bool dg = level_diag[l];
+      int max_ent = 0;
+      for (const Unit& u : us) max_ent = std::max(max_ent, int(u.e - u.b) - (dg ? 1 : 0));
+      const int units = int(us.size()) * NG;
+      const int lg = lanes_log2(units, max_ent, S.consumers);
+      static const int min_team = [] {
+        const char* e = std::getenv("BIPM_MIN_TEAM");
+        return e ? std::max(1, std::atoi(e)) : 1;
+      }();
+      int team = min_team;
+      while (team < S.consumers / 32 && team * 32 < units * (1 << lg)) team *= 2;
+      if (!p.items.empty() && (team != cur_team || dg != cur_diag)) flush();
+      cur_team = team;
+      cur_diag = dg;
+      size_t u = 0;
+      while (u < us.size()) {
+        // as many of the level's units as fit in this step
+        const int ub = int(p.items.size() / 4);
+        while (u < us.size()) {
+          const int n_new = int(us[u].e - us[u].b);
+          if (!p.items.empty() &&
+              step_bytes(int(p.items.size() / 4) + 1, int(p.col.size()) + n_new,
+                         int(p.col.size()) + n_new, 0, int(p.levels.size() / 4) + 1) > max_bytes)
+            break;
+          const int beg = int(p.col.size());
+          for (idx t = us[u].b; t < us[u].e; ++t) {
+            p.col.push_back(sw.col[size_t(t)]);
+            slots.push_back(slot_of_t[size_t(t)]);
+          }
+          p.items.insert(p.items.end(), {us[u].row, beg, int(p.col.size()), 0});
+          ++u;
+        }
+        const int ue = int(p.items.size() / 4);
+        if (ue > ub)  // barrier after the level's last part
+          p.levels.insert(p.levels.end(), {ub * NG, ue * NG, lg, u == us.size() ? 1 : 0});
+        if (u < us.size()) flush();  // the step is full: the level continues in the next
+      }
+    }
+    flush();
+    last_team = 16;  // the steps after a sweep start with an all-consumer barrier
+  }
+};
+
+}  // namespace
+
+StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
+                                   idx n_u, int K, int consumers, int ring_bytes,
+                                   int lookahead_max) {
+  StreamProgram S;
+  S.K = K;
+  S.consumers = consumers;
+  S.ring_bytes = ring_bytes;
+  S.max_step_bytes = std::max(4096, std::min(ring_bytes / 4, 24 * 1024));
+  const idx n = L.n, t0 = L.t0, tl = L.tl;
+  S.stride[kArrDense] = 2LL * tl * tl;
+  S.stride[kArrKxx] = kxx.nnz();
+  S.stride[kArrKxuT] = kxu.nnz();
+  S.stride[kArrGuT] = gu.nnz();
+  S.stride[kArrSigma] = n;
+  // stride[kArrSweep] is fixed after the program is built (nnz_vs, even)
+  Builder B{S, S.max_step_bytes};
+  using P = Builder::Pending;
+
+  // factor slot of every entry of the four sweeps' direct value arrays
+  std::vector<idx> slot_L(size_t(L.nnz_l)), slot_U(size_t(L.nnz_f - L.nnz_l)),
+      slot_Ut(size_t(L.nnz_f - L.nnz_l)), slot_Lt(size_t(L.nnz_l));
+  for (idx t = 0; t < L.nnz_l; ++t) slot_L[size_t(t)] = t;
+  for (idx t = 0; t < L.nnz_f - L.nnz_l; ++t) slot_U[size_t(t)] = L.nnz_l + t;
+  for (idx t = 0; t < L.nnz_f - L.nnz_l; ++t) slot_Ut[size_t(t)] = L.ft_src[size_t(t)];
+  for (idx t = 0; t < L.nnz_l; ++t) slot_Lt[size_t(t)] = L.ft_src[size_t(L.nnz_f - L.nnz_l + t)];
+
+  auto dense = [&](int which) {
+    if (tl == 0) return;
+    const int rows = std::max(1, (S.max_step_bytes - 64) / (8 * int(tl)) - 1);
+    for (int r0 = 0; r0 < tl; r0 += rows) {
+      const int nr = std::min<int>(rows, int(tl) - r0);
+      const int fl = (r0 == 0 ? kFlagPre : 0) | (r0 + nr >= tl ? (kFlagCommit | kFlagBarrier) : 0);
+      P p{kStepDense, fl, r0, nr, {}, {}};
+      p.val_arr = kArrDense;
+      p.val_off = which * int(tl) * int(tl) + r0 * int(tl);
+      p.val_count = nr * int(tl);
+      B.emit(p);
+      ++S.n_dense_steps;
+    }
+  };
+  // accumulator rows: control u belongs to register q = (u K + c) / consumers
+  const int R = consumers / K;
+  S.nq = int((size_t(n_u) * K + consumers - 1) / consumers);
+  auto acc = [&](const Csr& A, std::vector<idx>& t_slot) {
+    bool first_acc = true;  // the accumulation reads the finished sweep
+    const Csr t = A.transpose_pattern();  // column u -> (state row, slot)
+    t_slot.resize(t.val.size());
+    for (size_t k = 0; k < t.val.size(); ++k) t_slot[k] = idx(t.val[k]);
+    for (int q = 0; q * R < n_u; ++q) {
+      const int ub = q * R, ue = std::min<int>(n_u, ub + R);
+      int u0 = ub;
+      while (u0 < ue) {
+        // grow the step while it fits
+        int u1 = u0;
+        int ents = 0;
+        while (u1 < ue) {
+          const int add = t.ptr[size_t(u1) + 1] - t.ptr[size_t(u1)];
+          if (u1 > u0 && Builder::step_bytes(u1 - u0 + 1, ents + add, ents + add, 0) > S.max_step_bytes)
+            break;
+          ents += add;
+          ++u1;
+        }
+        P p{kStepAcc, first_acc ? kFlagPre : 0, q, u0, {}, {}};
+        for (int u = u0; u < u1; ++u) {
+          const int beg = int(p.col.size());
+          for (idx k = t.ptr[size_t(u)]; k < t.ptr[size_t(u) + 1]; ++k)
+            p.col.push_back(L.iperm[size_t(t.ind[size_t(k)])]);
+          p.items.insert(p.items.end(), {u, beg, int(p.col.size()), 0});  // u: not a panel row
+        }
+        p.val_arr = (&t_slot == &S.kxu_t_slot) ? kArrKxuT : kArrGuT;
+        p.val_off = t.ptr[size_t(u0)];
+        p.val_count = t.ptr[size_t(u1)] - t.ptr[size_t(u0)];
+        if (p.val_count > 0) {  // an empty range contributes nothing
+          B.emit(p);
+          ++S.n_acc_steps;
+          first_acc = false;
+        }
+        u0 = u1;
+      }
+    }
+  };
+  auto spmv = [&] {
+    idx i0 = 0;
+    while (i0 < n) {
+      idx i1 = i0;
+      int ents = 0;
+      while (i1 < n) {
+        const int add = kxx.ptr[size_t(i1) + 1] - kxx.ptr[size_t(i1)];
+        if (i1 > i0 && Builder::step_bytes(int(i1 - i0) + 1, ents + add, ents + add,
+                                           int(i1 - i0) + 1) > S.max_step_bytes)
+          break;
+        ents += add;
+        ++i1;
+      }
+      P p{kStepSpmv, 0, 0, 0, {}, {}};
+      const idx e0 = kxx.ptr[size_t(i0)];
+      for (idx i = i0; i < i1; ++i) {
+        const int beg = int(p.col.size());
+        for (idx k = kxx.ptr[size_t(i)]; k < kxx.ptr[size_t(i) + 1]; ++k)
+          p.col.push_back(L.iperm[size_t(kxx.ind[size_t(k)])]);
+        p.items.insert(p.items.end(), {L.iperm[size_t(i)], beg, int(p.col.size()), int(i - i0)});
+      }
+      p.val_arr = kArrKxx;
+      p.val_off = e0;
+      p.val_count = kxx.ptr[size_t(i1)] - e0;
+      p.x_arr = kArrSigma;
+      p.x_off = i0;
+      p.x_count = i1 - i0;
+      B.emit(p);
+      ++S.n_spmv_steps;
+      i0 = i1;
+    }
+  };
+
+  // scatter and copy-back synchronise internally (before) and after
+  B.emit(P{kStepScatter, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+  B.sweep(L.sL, slot_L, false, true, 0);
+  dense(0);
+  B.sweep(L.sU, slot_U, true, false, 0);
+  acc(kxu, S.kxu_t_slot);
+  spmv();
+  B.emit(P{kStepCopyBack, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+  B.sweep(L.sUt, slot_Ut, true, true, 1);  // the diagonal is not part of the tail gather
+  dense(1);
+  B.sweep(L.sLt, slot_Lt, false, false, 0);
+  acc(gu, S.gu_t_slot);
+
+  if (S.vs_src.size() & 1) S.vs_src.push_back(-1);
+  if (S.vs_src.empty()) S.vs_src.assign(2, -1);
+  S.nnz_vs = idx(S.vs_src.size());
+  S.stride[kArrSweep] = S.nnz_vs;
+  // the VS parity bits were emitted with stride 0: VS offsets are even and its
+  // stride is even, so they are correct as written
+  S.steps = int(S.issue.size());
+
+  // ---- ring placement (sequential with wrap; every scenario starts at 0)
+  std::vector<int> beg(size_t(S.steps)), end(size_t(S.steps));
+  int off = 0;
+  for (int j = 0; j < S.steps; ++j) {
+    StepIssue& is = S.issue[size_t(j)];
+    const int bytes = is.pat_bytes + val_alloc(is.val_count) + val_alloc(is.x_count);
+    if (bytes > ring_bytes) throw Error(kInvalidArgument, "stream plan: step larger than the ring");
+    if (j == 0 || off + bytes > ring_bytes) off = 0;
+    is.ring_off = off;
+    is.val_ring = off + is.pat_bytes;
+    is.x_ring = is.val_ring + val_alloc(is.val_count);
+    beg[size_t(j)] = off;
+    end[size_t(j)] = off + bytes;
+    off += bytes;
+  }
+  // ---- producer waits: the latest earlier step (cyclically: the previous
+  // scenario's program) whose region overlaps; capped by the lookahead
+  S.ring_off.resize(size_t(S.steps));
+  for (int j = 0; j < S.steps; ++j) {
+    S.ring_off[size_t(j)] = S.issue[size_t(j)].ring_off;
+    int d = 1;
+    for (; d <= lookahead_max; ++d) {
+      const int k = ((j - d) % S.steps + S.steps) % S.steps;
+      if (beg[size_t(k)] < end[size_t(j)] && beg[size_t(j)] < end[size_t(k)]) break;
+    }
+    S.issue[size_t(j)].wait_delta = std::min(d, lookahead_max);
+  }
+  return S;
+}
+
+}  // namespace bipm

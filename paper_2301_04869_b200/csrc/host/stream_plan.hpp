@@ -1,0 +1,94 @@
+// Static step program of the streamed Schur reduction (kernels/reduce_stream.cu).
+//
+// The per-scenario work of one column tile of K_hat (reduce_group's tile loop,
+// kkt.cpp:385-462) is a fixed sequence of *steps*: the level-scheduled
+// triangular sweeps of G_x (L, U, U', L'), the dense separator tail, the
+// K_xu' T / G_u' Y accumulations and the K~_xx T product.  Every step's data
+// (a 32-byte header, its item list, its column indices and its values) is
+// laid out contiguously so that a producer warp can stage it into a shared
+// memory ring with one or two bulk (TMA) copies ahead of the consumers.  The
+// program, the ring placement and the producer's wait distances are computed
+// here once per solve; they are the same for every scenario and every tile.
+#pragma once
+
+#include <vector>
+
+#include "common.hpp"
+#include "plan.hpp"
+
+namespace bipm {
+
+// step kinds (header word 0)
+enum StepKind : int {
+  kStepScatter = 0,   // X = P G_u V (tile columns), acc += K_uu V
+  kStepSweep = 1,     // one level (or part) of a triangular sweep
+  kStepDense = 2,     // rows of the dense tail product X_T <- W X_T
+  kStepAcc = 3,       // acc -= (K_xu' or G_u') X over a range of control rows
+  kStepSpmv = 4,      // S = -(K~_xx X) over a range of state rows
+  kStepCopyBack = 5,  // X = S + K_xu V
+};
+// kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
+enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };
+
+// Step pattern block: a 64-byte header (16 ints)
+//   {kind, flags, n_items, n_col, aux0, aux1, vcount, par, lg, n_units, warp0, n_lev, 0...}
+// then n_lev int4 level records (sweep steps), n_items int4 items and n_col
+// column words.  All-warp steps (dense, spmv): a unit is (item, group of up to
+// 8 panel columns) served by 2^lg lanes, chunks of 32 >> lg units dealt to
+// the 16 consumer warps round robin from warp0.  Sweep steps: aux0 = T, the
+// team of the lowest T warps running them; level record = (unit begin, unit
+// end, lg, team barrier after it).
+constexpr int kStepHeaderInts = 16;
+
+// Shared-memory panel layout of the K right-hand-side columns: row r is K
+// doubles (K*8 bytes) split in 16-byte chunks, chunk c stored at position
+// c ^ sw(r) so that lanes gathering different rows spread over the banks.
+// word(r) = r*K*8 + 16*sw(r); element (r, c) lives at byte
+// (word(r) ^ ((c >> 1) << 4)) + 8 (c & 1)   (K = 1: r*8).
+inline int panel_swizzle(int r, int K) {
+  return K >= 16 ? (r & 7) : K == 8 ? ((r >> 1) & 3) : K == 4 ? ((r >> 2) & 1) : 0;
+}
+inline int panel_word(int r, int K) { return r * K * 8 + 16 * panel_swizzle(r, K); }
+
+// value arrays a step can read ([M][stride] scenario-major on the device)
+enum ValArray : int {
+  kArrSweep = 0,  // sweep-ordered factor values (VS), written by the refactor
+  kArrDense = 1,  // W, W' dense tail inverses
+  kArrKxx = 2,    // condensed K_xx (CSR slot order)
+  kArrKxuT = 3,   // K_xu values in column (control) order
+  kArrGuT = 4,    // G_u values in column (control) order
+  kArrSigma = 5,  // sigma_x
+  kNumValArrays = 6
+};
+
+// producer record of one step (12 ints)
+struct StepIssue {
+  int pat_off;     // int offset of the step's pattern block in `pat`
+  int pat_bytes;   // header + items + columns
+  int ring_off;    // byte offset of the step in the ring
+  int val_arr, val_off, val_count;  // values: array, offset within a scenario, count
+  int x_arr, x_off, x_count;        // extra values (sigma_x segment)
+  int val_ring, x_ring;             // byte offsets in the ring
+  int wait_delta;  // wait until step (j - wait_delta) has been consumed (0: none)
+};
+
+struct StreamProgram {
+  int K = 1, consumers = 512, ring_bytes = 0, steps = 0;
+  std::vector<int> pat;          // pattern blocks (16-byte aligned)
+  std::vector<StepIssue> issue;  // per step
+  std::vector<int> ring_off;     // per step (consumer lookup)
+  std::vector<idx> vs_src;       // VS position -> factor slot (F), -1: padding
+  idx nnz_vs = 0;
+  std::vector<idx> kxu_t_slot, gu_t_slot;  // column-order gathers of K_xu, G_u values
+  long long stride[kNumValArrays] = {0, 0, 0, 0, 0, 0};
+  int nq = 0;                    // accumulator registers per consumer thread
+  int max_step_bytes = 0;
+  // statistics
+  int n_sweep_steps = 0, n_dense_steps = 0, n_acc_steps = 0, n_spmv_steps = 0;
+};
+
+StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
+                                   idx n_u, int K, int consumers, int ring_bytes,
+                                   int lookahead_max);
+
+}  // namespace bipm

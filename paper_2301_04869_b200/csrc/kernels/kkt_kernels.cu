@@ -75,7 +75,8 @@ template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const double* __restrict__ gx,
                                                             int nnz_gx, double* F, double* FT,
                                                             double* D, int* status,
-                                                            double piv_tol) {
+                                                            double piv_tol, const int* vs_src,
+                                                            int nnz_vs, double* VS) {
   const int s = blockIdx.x;
   const double* __restrict__ A = gx + size_t(s) * nnz_gx;
   double* Fs = F + size_t(s) * P.nnz_f;
@@ -130,6 +131,14 @@ __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const doubl
   // solve layouts: transposed copy ...
   double* FTs = FT + size_t(s) * P.nnz_f;
   for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
+  // ... and the sweep-ordered copy streamed by the Schur reduction
+  if (VS) {
+    double* VSs = VS + size_t(s) * nnz_vs;
+    for (int q = threadIdx.x; q < nnz_vs; q += BLOCK) {
+      const int src = vs_src[q];
+      VSs[q] = src >= 0 ? Fs[src] : 0.0;
+    }
+  }
   // ... and W = (L_TT U_TT)^{-1}: stage the tail triangles in shared memory,
   // thread j solves L U w = e_j for column j (written row-major to W and W')
   const int tl = P.tl;
@@ -539,12 +548,14 @@ size_t single_rhs_smem(int n_x) {
 }  // namespace
 
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
-                        double* FT, double* D, int* status, double piv_tol, cudaStream_t st) {
+                        double* FT, double* D, int* status, double piv_tol, const int* vs_src,
+                        int nnz_vs, double* VS, cudaStream_t st) {
   if (M <= 0) return;
   const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
   cudaFuncSetAttribute(lu_refactor_kernel<kLuBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(smem));
-  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol);
+  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol,
+                                                          vs_src, nnz_vs, VS);
   note_launch();
   check_launch("lu_refactor");
 }

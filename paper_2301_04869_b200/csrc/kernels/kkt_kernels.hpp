@@ -14,8 +14,11 @@ namespace bipm {
 // finite), mirroring SingularBlockError (linalg.cpp:69-73).
 // Also writes the transposed copy FT [M][nnz_f] and the dense tail blocks
 // D [M][4 tl tl] used by the solve kernels.
+// VS (optional, [M][nnz_vs]): VS[s][q] = F[s][vs_src[q]] (0 where -1), the
+// sweep-ordered factor values of the streamed reduction (reduce_stream.cu).
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
-                        double* FT, double* D, int* status, double piv_tol, cudaStream_t st);
+                        double* FT, double* D, int* status, double piv_tol, const int* vs_src,
+                        int nnz_vs, double* VS, cudaStream_t st);
 
 struct ReduceLaunch {
   DevLu lu;
