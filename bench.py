@@ -5,8 +5,11 @@ reduced-space KKT path, B200 (this repo) vs the reference CPU implementation.
 A *step* is one interior-point iteration of the solve (AD of the bundle,
 condensation, batched G_x refactor, Schur reduction + inertia loop, dense
 Cholesky, recovery, refinement, globalisation), iterations warmup..warmup+steps-1
-of a fresh solve (a converged solve restarts).  Workload: BASELINE.json
-configs[1] = case118, 64 scenarios, one B200 (override with --case/--scenarios).
+of a fresh solve (a converged solve restarts).  Workload: case1354pegase with
+256 scenarios, the configuration north_star's target is stated on (BASELINE.json
+configs[2]); it fits one B200 (~0.6 GB resident), so N=1 runs it whole and
+--gpus N shards its scenarios (override with --case/--scenarios, e.g. configs[1]
+= case118 / 64).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -290,15 +293,16 @@ def bench_reference(a, rank, world):
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--case", default="case118")
-    ap.add_argument("--scenarios", type=int, default=64)
+    ap.add_argument("--case", default="case1354pegase")
+    ap.add_argument("--scenarios", type=int, default=256)
     ap.add_argument("--sigma", type=float, default=0.05)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-iters", type=int, default=300,
-                    help="iteration cap of the CPU baseline sample")
+    ap.add_argument("--cpu-iters", type=int, default=4,
+                    help="iteration cap of the CPU baseline sample (bounded: ~10-30 s of "
+                         "host work at the default workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)

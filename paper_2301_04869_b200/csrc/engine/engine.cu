@@ -77,7 +77,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
     lu_arrays.back().upload(v);
     return lu_arrays.back().get();
   };
-  lu_arrays.reserve(80);
+  lu_arrays.reserve(120);
   lu.n = L.n;
   lu.nnz_l = L.nnz_l;
   lu.nnz_f = L.nnz_f;
@@ -110,6 +110,17 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   lu.mul_ptr = up(L.mul_ptr);
   lu.mul_l = up(L.mul_l);
   lu.mul_u = up(L.mul_u);
+  auto up0 = [&](const std::vector<idx>& v) { return up(v.empty() ? std::vector<idx>{0} : v); };
+  lu.n_nt = idx(L.nt_lvl_u_ptr.size()) - 1;
+  lu.n_tail_ent = idx(L.tail_slot.size());
+  lu.nt_lvl_u_ptr = up(L.nt_lvl_u_ptr);
+  lu.nt_lvl_u_slot = up0(L.nt_lvl_u_slot);
+  lu.nt_lvl_l_ptr = up(L.nt_lvl_l_ptr);
+  lu.nt_lvl_l_slot = up0(L.nt_lvl_l_slot);
+  lu.tail_slot = up0(L.tail_slot);
+  lu.tail_mul_ptr = up(L.tail_mul_ptr);
+  lu.tail_mul_l = up0(L.tail_mul_l);
+  lu.tail_mul_u = up0(L.tail_mul_u);
   lu.t0 = L.t0;
   lu.tl = L.tl;
   lu.ft_src = up(L.ft_src);

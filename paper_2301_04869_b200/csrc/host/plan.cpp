@@ -551,6 +551,41 @@ LuPlan make_lu_plan(const Csr& A) {
     P.lvl_u_ptr.push_back(idx(P.lvl_u_slot.size()));
     P.lvl_l_ptr.push_back(idx(P.lvl_l_slot.size()));
   }
+  // split at the dense tail
+  const idx t0 = P.t0;
+  P.nt_lvl_u_ptr.assign(1, 0);
+  P.nt_lvl_l_ptr.assign(1, 0);
+  for (idx l = 0; l < nf; ++l) {
+    bool any = false;
+    for (idx t = P.fwd_ptr[size_t(l)]; t < P.fwd_ptr[size_t(l) + 1]; ++t) {
+      const idx j = P.fwd_rows[size_t(t)];
+      if (j >= t0) continue;
+      any = true;
+      P.nt_lvl_u_slot.push_back(P.diag[size_t(j)]);
+      for (idx q = P.u_ptr[size_t(j)]; q < P.u_ptr[size_t(j) + 1]; ++q)
+        P.nt_lvl_u_slot.push_back(P.u_slot[size_t(q)]);
+      for (idx r : urow[size_t(j)]) P.nt_lvl_l_slot.push_back(l_slot_of(r, j));
+    }
+    if (!any) continue;
+    P.nt_lvl_u_ptr.push_back(idx(P.nt_lvl_u_slot.size()));
+    P.nt_lvl_l_ptr.push_back(idx(P.nt_lvl_l_slot.size()));
+  }
+  P.tail_mul_ptr.assign(1, 0);
+  auto add_tail = [&](idx slot) {
+    P.tail_slot.push_back(slot);
+    for (idx t = P.mul_ptr[size_t(slot)]; t < P.mul_ptr[size_t(slot) + 1]; ++t)
+      if (P.l_col[size_t(P.mul_l[size_t(t)])] < t0) {
+        P.tail_mul_l.push_back(P.mul_l[size_t(t)]);
+        P.tail_mul_u.push_back(P.mul_u[size_t(t)]);
+      }
+    P.tail_mul_ptr.push_back(idx(P.tail_mul_l.size()));
+  };
+  for (idx i = t0; i < n; ++i) {
+    for (idx q = P.l_ptr[size_t(i)]; q < P.l_ptr[size_t(i) + 1]; ++q)
+      if (P.l_col[size_t(q)] >= t0) add_tail(q);  // L(i, j), t0 <= j < i
+    add_tail(P.diag[size_t(i)]);
+    for (idx q = P.u_ptr[size_t(i)]; q < P.u_ptr[size_t(i) + 1]; ++q) add_tail(P.u_slot[size_t(q)]);
+  }
   return P;
 }
 

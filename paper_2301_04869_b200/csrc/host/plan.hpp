@@ -87,6 +87,12 @@ struct LuPlan {
   // e: value = A[a_src[e]] (or 0) - sum_t F[mul_l[t]] * F[mul_u[t]]
   // over t in [mul_ptr[e], mul_ptr[e+1]); L entries then divide by the pivot.
   std::vector<idx> lvl_u_ptr, lvl_u_slot, lvl_l_ptr, lvl_l_slot;
+  // the same program split at the dense tail (refactor_levels_kernel /
+  // refactor_tail_kernel): levels of the pivots j < t0 only, then for every
+  // factor slot of the tail block the terms k < t0 of its sum (the tail block
+  // is then factorised densely)
+  std::vector<idx> nt_lvl_u_ptr, nt_lvl_u_slot, nt_lvl_l_ptr, nt_lvl_l_slot;
+  std::vector<idx> tail_slot, tail_mul_ptr, tail_mul_l, tail_mul_u;
   std::vector<idx> a_src;       // per factor slot: G_x slot or -1 (fill)
   std::vector<idx> piv_of;      // per factor slot: pivot slot for L entries, -1 for U
   std::vector<idx> mul_ptr, mul_l, mul_u;

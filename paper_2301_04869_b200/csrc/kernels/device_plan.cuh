@@ -27,6 +27,10 @@ struct DevLu {
   const int *fwd_ptr, *fwd_rows, *bwd_ptr, *bwd_rows;
   const int *lvl_u_ptr, *lvl_u_slot, *lvl_l_ptr, *lvl_l_slot;
   const int *a_src, *piv_of, *mul_ptr, *mul_l, *mul_u;
+  // split refactor: non-tail levels, tail-block partial sums (k < t0)
+  int n_nt, n_tail_ent;
+  const int *nt_lvl_u_ptr, *nt_lvl_u_slot, *nt_lvl_l_ptr, *nt_lvl_l_slot;
+  const int *tail_slot, *tail_mul_ptr, *tail_mul_l, *tail_mul_u;
   // solve layouts: transposed factor copy and dense tail blocks
   int t0, tl;
   const int* ft_src;     // [nnz_f]

@@ -71,67 +71,131 @@ __device__ __forceinline__ int find_in_row(const int* ptr, const int* ind, int r
 }
 
 // ---------------------------------------------------------------- LU refactor
+// Two kernels (BlockDiagFactor::factor, linalg.cpp:51-89, with one static
+// symbolic pattern):
+//  refactor_levels_kernel  the level-scheduled Crout program of the pivots
+//    j < t0 (no shared memory, so several scenarios share an SM and hide each
+//    other's memory latency), then for every factor slot of the dense tail
+//    block its partial sum A - sum_{k < t0} L(i,k) U(k,j);
+//  refactor_tail_kernel    right-looking dense LU of that tail block in shared
+//    memory (static pivots), W = (L_TT U_TT)^{-1}, the pivot guard and the
+//    sweep layouts (FT, VS) of the solve kernels.
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const double* __restrict__ gx,
-                                                            int nnz_gx, double* F, double* FT,
-                                                            double* D, int* status,
-                                                            double piv_tol, const int* vs_src,
-                                                            int nnz_vs, double* VS) {
+__global__ void __launch_bounds__(BLOCK) refactor_levels_kernel(DevLu P,
+                                                                const double* __restrict__ gx,
+                                                                int nnz_gx, double* F,
+                                                                double* scale_out) {
   const int s = blockIdx.x;
   const double* __restrict__ A = gx + size_t(s) * nnz_gx;
   double* Fs = F + size_t(s) * P.nnz_f;
   double mx = 0.0;
   for (int i = threadIdx.x; i < nnz_gx; i += BLOCK) mx = fmax(mx, fabs(A[i]));
   const double scale = block_reduce<BLOCK>(mx, true);
+  if (threadIdx.x == 0) scale_out[s] = scale;
 
-  for (int lv = 0; lv < P.n_fwd; ++lv) {
+  for (int lv = 0; lv < P.n_nt; ++lv) {
     {
-      const int b0 = P.lvl_u_ptr[lv];
+      const int b0 = P.nt_lvl_u_ptr[lv];
       group_dot<BLOCK>(
-          P.lvl_u_ptr[lv + 1] - b0,
+          P.nt_lvl_u_ptr[lv + 1] - b0,
           [&](int it, int& b, int& e) {
-            const int slot = P.lvl_u_slot[b0 + it];
+            const int slot = P.nt_lvl_u_slot[b0 + it];
             b = P.mul_ptr[slot];
             e = P.mul_ptr[slot + 1];
           },
           [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
           [&](int it, double acc) {
-            const int slot = P.lvl_u_slot[b0 + it];
+            const int slot = P.nt_lvl_u_slot[b0 + it];
             const int src = P.a_src[slot];
             Fs[slot] = (src >= 0 ? A[src] : 0.0) - acc;
           });
     }
     __syncthreads();
     {
-      const int b0 = P.lvl_l_ptr[lv];
+      const int b0 = P.nt_lvl_l_ptr[lv];
       group_dot<BLOCK>(
-          P.lvl_l_ptr[lv + 1] - b0,
+          P.nt_lvl_l_ptr[lv + 1] - b0,
           [&](int it, int& b, int& e) {
-            const int slot = P.lvl_l_slot[b0 + it];
+            const int slot = P.nt_lvl_l_slot[b0 + it];
             b = P.mul_ptr[slot];
             e = P.mul_ptr[slot + 1];
           },
           [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
           [&](int it, double acc) {
-            const int slot = P.lvl_l_slot[b0 + it];
+            const int slot = P.nt_lvl_l_slot[b0 + it];
             const int src = P.a_src[slot];
             Fs[slot] = ((src >= 0 ? A[src] : 0.0) - acc) / Fs[P.piv_of[slot]];
           });
     }
     __syncthreads();
   }
+  // tail block: A - sum over the non-tail pivots (independent entries)
+  group_dot<BLOCK>(
+      P.n_tail_ent,
+      [&](int it, int& b, int& e) {
+        b = P.tail_mul_ptr[it];
+        e = P.tail_mul_ptr[it + 1];
+      },
+      [&](int, int t) { return Fs[P.tail_mul_l[t]] * Fs[P.tail_mul_u[t]]; },
+      [&](int it, double acc) {
+        const int slot = P.tail_slot[it];
+        const int src = P.a_src[slot];
+        Fs[slot] = (src >= 0 ? A[src] : 0.0) - acc;
+      });
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F, double* FT,
+                                                              double* D,
+                                                              const double* __restrict__ scale_in,
+                                                              int* status, double piv_tol,
+                                                              const int* vs_src, int nnz_vs,
+                                                              double* VS) {
+  const int s = blockIdx.x;
+  double* Fs = F + size_t(s) * P.nnz_f;
+  const int tl = P.tl, tt = tl * tl;
+  extern __shared__ double sm[];
+  double* T = sm;       // tail block, column-major; L strict lower + U upper after the LU
+  double* Wm = sm + tt;  // W column j solved by thread j
+  if (tl > 0) {
+    for (int q = threadIdx.x; q < tt; q += BLOCK) {
+      const int a = q % tl, b = q / tl;
+      const int src = a > b ? P.dense_src[q] : P.dense_src[tt + q];
+      T[q] = src >= 0 ? Fs[src] : 0.0;
+    }
+    __syncthreads();
+    // right-looking LU without pivoting (the static pivot order)
+    for (int k = 0; k < tl - 1; ++k) {
+      const double piv = T[k * tl + k];
+      for (int i = k + 1 + threadIdx.x; i < tl; i += BLOCK) T[k * tl + i] /= piv;
+      __syncthreads();
+      const int m = tl - 1 - k;
+      for (int q = threadIdx.x; q < m * m; q += BLOCK) {
+        const int i = k + 1 + q % m, j = k + 1 + q / m;
+        T[j * tl + i] -= T[k * tl + i] * T[j * tl + k];
+      }
+      __syncthreads();
+    }
+    // back into the factor (structural slots only)
+    for (int q = threadIdx.x; q < tt; q += BLOCK) {
+      const int a = q % tl, b = q / tl;
+      const int src = a > b ? P.dense_src[q] : P.dense_src[tt + q];
+      if (src >= 0) Fs[src] = T[q];
+    }
+  }
+  __syncthreads();
+  // pivot guard (linalg.cpp:69-73): every diagonal of U against max |G_x|
   double bad = 0.0;
-  const double floor_ = piv_tol * fmax(scale, 1e-300);
+  const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
   for (int j = threadIdx.x; j < P.n; j += BLOCK) {
     const double d = Fs[P.diag[j]];
     if (!(fabs(d) >= floor_) || !isfinite(d)) bad = 1.0;
   }
   bad = block_reduce<BLOCK>(bad, true);
   if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
-  // solve layouts: transposed copy ...
+  // solve layouts: transposed copy and the sweep-ordered copy
   double* FTs = FT + size_t(s) * P.nnz_f;
   for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
-  // ... and the sweep-ordered copy streamed by the Schur reduction
   if (VS) {
     double* VSs = VS + size_t(s) * nnz_vs;
     for (int q = threadIdx.x; q < nnz_vs; q += BLOCK) {
@@ -139,37 +203,28 @@ __global__ void __launch_bounds__(BLOCK) lu_refactor_kernel(DevLu P, const doubl
       VSs[q] = src >= 0 ? Fs[src] : 0.0;
     }
   }
-  // ... and W = (L_TT U_TT)^{-1}: stage the tail triangles in shared memory,
-  // thread j solves L U w = e_j for column j (written row-major to W and W')
-  const int tl = P.tl;
   if (tl == 0) return;
-  extern __shared__ double tri[];  // [L_TT | U_TT], column-major
-  const int tt = tl * tl;
-  for (int q = threadIdx.x; q < 2 * tt; q += BLOCK) {
-    const int src = P.dense_src[q];
-    tri[q] = src >= 0 ? Fs[src] : 0.0;
+  // W = (L_TT U_TT)^{-1}: thread j solves L U w = e_j for column j
+  for (int j = threadIdx.x; j < tl; j += BLOCK) {
+    for (int i = 0; i < j; ++i) Wm[i * tl + j] = 0.0;
+    Wm[j * tl + j] = 1.0;
+    for (int i = j + 1; i < tl; ++i) {  // y = L^{-1} e_j
+      double acc = 0.0;
+      for (int k = j; k < i; ++k) acc += T[k * tl + i] * Wm[k * tl + j];
+      Wm[i * tl + j] = -acc;
+    }
+    for (int i = tl - 1; i >= 0; --i) {  // w = U^{-1} y
+      double acc = Wm[i * tl + j];
+      for (int k = i + 1; k < tl; ++k) acc -= T[k * tl + i] * Wm[k * tl + j];
+      Wm[i * tl + j] = acc / T[i * tl + i];
+    }
   }
   __syncthreads();
-  const double* Lt = tri;
-  const double* Ut = tri + tt;
+  // D = [W row-major | W' row-major]
   double* W = D + size_t(s) * 2 * tt;
-  double* Wt = W + tt;
-  for (int j = threadIdx.x; j < tl; j += BLOCK) {
-    // forward: y = L^{-1} e_j (y_i = 0 for i < j), kept in W[:, j]
-    for (int i = 0; i < j; ++i) W[i * tl + j] = 0.0;
-    W[j * tl + j] = 1.0;
-    for (int i = j + 1; i < tl; ++i) {
-      double acc = 0.0;
-      for (int k = j; k < i; ++k) acc += Lt[k * tl + i] * W[k * tl + j];
-      W[i * tl + j] = -acc;
-    }
-    // backward: w = U^{-1} y
-    for (int i = tl - 1; i >= 0; --i) {
-      double acc = W[i * tl + j];
-      for (int k = i + 1; k < tl; ++k) acc -= Ut[k * tl + i] * W[k * tl + j];
-      W[i * tl + j] = acc / Ut[i * tl + i];
-    }
-    for (int i = 0; i < tl; ++i) Wt[j * tl + i] = W[i * tl + j];
+  for (int q = threadIdx.x; q < tt; q += BLOCK) {
+    W[q] = Wm[q];
+    W[tt + q] = Wm[(q % tl) * tl + q / tl];
   }
 }
 
@@ -551,13 +606,23 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
                         int nnz_vs, double* VS, cudaStream_t st) {
   if (M <= 0) return;
-  const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
-  cudaFuncSetAttribute(lu_refactor_kernel<kLuBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(smem));
-  lu_refactor_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, gx, nnz_gx, F, FT, D, status, piv_tol,
-                                                          vs_src, nnz_vs, VS);
+  static double* scale = nullptr;
+  static int scale_n = 0;
+  if (scale_n < M) {
+    if (scale) cudaFree(scale);
+    cudaMalloc(&scale, size_t(M) * sizeof(double));
+    scale_n = M;
+  }
+  refactor_levels_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
-  check_launch("lu_refactor");
+  check_launch("refactor_levels");
+  const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
+  cudaFuncSetAttribute(refactor_tail_kernel<kLuBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status, piv_tol,
+                                                            vs_src, nnz_vs, VS);
+  note_launch();
+  check_launch("refactor_tail");
 }
 
 void plan_reduce_launch(ReduceLaunch& a, int smem_budget, int sm_count) {
