@@ -207,30 +207,51 @@ void Engine::setup_stream() {
   const DerivPlan& D = pb.D;
   const LuPlan& L = pb.LU;
   const int n_x = pb.M.n_x, n_u = pb.M.n_u;
-  // widest power-of-two tile whose panel leaves a useful ring (>= 40 KB)
+  // Configuration: tile width K, consumers C per CTA and CTAs per SM.  Among
+  // the configurations with a useful ring (>= 16 KB) keep the most panel
+  // columns in flight per SM (K x CTAs), then the widest tile: measured at
+  // 1354/256, one CTA of 512 consumers with K = 8 (47.8 ms) beats two CTAs
+  // with K = 4 (62 ms) and four with K = 1 (100 ms) -- each level step costs
+  // the same latency whatever its width, and smaller rings mean more steps.
   int cap = 1;
   while (cap < 32 && cap < n_u) cap *= 2;
   const Csr gut = D.g.u.transpose_pattern(), kxut = D.kxu.out.transpose_pattern();
   if (const char* e = std::getenv("BIPM_STREAM_K")) cap = std::max(1, std::min(cap, std::atoi(e)));
-  int K = cap;
-  int ring = 0, list_cap = 0;
-  for (; K >= 1; K /= 2) {
-    if ((size_t(n_u) * K + kStreamConsumers - 1) / kStreamConsumers > kStreamMaxQ) continue;
-    list_cap = 0;
+  int force_c = 0;
+  if (const char* e = std::getenv("BIPM_STREAM_C")) force_c = std::atoi(e);
+  auto list_cap_of = [&](int K) {
+    int lc = 0;
     for (int j0 = 0; j0 < n_u; j0 += K) {
       const int j1 = std::min(n_u, j0 + K);
       const int a = gut.ptr[size_t(j1)] - gut.ptr[size_t(j0)];
       const int b = kxut.ptr[size_t(j1)] - kxut.ptr[size_t(j0)];
-      list_cap = std::max(list_cap, ((a + 1) & ~1) + ((b + 1) & ~1));
+      lc = std::max(lc, ((a + 1) & ~1) + ((b + 1) & ~1));
     }
-    ring = stream_ring_capacity(n_x, K, L.tl, 4096, list_cap);
-    if (ring >= 40 * 1024) break;
+    return lc;
+  };
+  struct Cfg { int K, C, ctas, ring, list_cap; };
+  Cfg best{0, 0, 0, 0, 0};
+  for (int C : {512, 256, 128}) {
+    if (force_c && C != force_c) continue;
+    const int ctas = 512 / C;
+    for (int K = cap; K >= 1; K /= 2) {
+      if (C < 512 && K > (C == 256 ? 8 : 4)) continue;  // instantiated kernels
+      if ((size_t(n_u) * K + C - 1) / C > size_t(kStreamMaxQ)) continue;
+      const int lc = list_cap_of(K);
+      const int ring = stream_ring_capacity(n_x, K, L.tl, 4096, lc, ctas);
+      if (ring < 16 * 1024) continue;
+      const bool better = K * ctas > best.K * best.ctas ||
+                          (K * ctas == best.K * best.ctas && K > best.K);
+      if (better) best = Cfg{K, C, ctas, ring, lc};
+      break;  // widest K that fits for this C
+    }
   }
-  if (K < 1) {
+  if (best.K < 1) {
     use_stream = false;  // panel does not fit: tile kernel with a global panel
     return;
   }
-  sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, kStreamConsumers, ring,
+  const int K = best.K, ring = best.ring, list_cap = best.list_cap;
+  sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, best.C, ring,
                                kStreamLookahead);
   sp_pat.upload(sprog.pat);
   {
@@ -272,6 +293,8 @@ void Engine::setup_stream() {
   sl.t0 = L.t0;
   sl.tl = L.tl;
   sl.list_cap = list_cap;
+  sl.consumers = best.C;
+  sl.ctas_per_sm = best.ctas;
   plan_stream_chunks(sl, sm_count);
   sl.pat = sp_pat.get();
   sl.issue = sp_issue.get();

@@ -27,8 +27,6 @@ namespace bipm {
 
 namespace {
 
-constexpr int kC = kStreamConsumers;
-constexpr int kThreads = kC + 32;
 constexpr int kNB = 32;  // mbarrier slots (> producer lookahead)
 constexpr int kMaxQ = kStreamMaxQ;
 
@@ -73,8 +71,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+template <int C>
 __device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kC) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(C) : "memory");
 }
 
 // ---------------------------------------------------------------- panel
@@ -189,8 +188,8 @@ enum : int { kFDiag = 1, kFCommit = 2, kFBarrier = 4, kFPre = 8 };
     const int lane_ = (tid) & 31, warp_ = (tid) >> 5;                            \
     const int upw_ = 32 >> lg_;                                                   \
     const int nch_ = ((h).n_units + upw_ - 1) >> (5 - lg_);                      \
-    for (int c_ = (warp_ - (h).warp0 + kC / 32) & (kC / 32 - 1); c_ < nch_;      \
-         c_ += kC / 32) {                                                         \
+    for (int c_ = (warp_ - (h).warp0 + C / 32) & (C / 32 - 1); c_ < nch_;      \
+         c_ += C / 32) {                                                         \
       const int unit = c_ * upw_ + (lane_ >> lg_);                                \
       const int sub = lane_ & (g_ - 1);                                           \
       const bool active = unit < (h).n_units;                                     \
@@ -201,10 +200,15 @@ enum : int { kFDiag = 1, kFCommit = 2, kFBarrier = 4, kFPre = 8 };
 
 // one level (or part of one) of a triangular sweep: x_r -= sum v x_col, then
 // divided by the diagonal (the item's first entry) with kFlagDiag
-// barrier of the team of the lowest T consumer warps (T = 1: the warp itself)
+// barrier of the team of the lowest T consumer warps (T = C/32: all of them,
+// barrier 1; T = 1: the warp itself)
+template <int C>
 __device__ __forceinline__ void team_sync(int T) {
+  if (T == C / 32) {
+    consumer_sync<C>();
+    return;
+  }
   switch (T) {
-    case 16: asm volatile("bar.sync 1, 512;" ::: "memory"); break;
     case 8: asm volatile("bar.sync 2, 256;" ::: "memory"); break;
     case 4: asm volatile("bar.sync 3, 128;" ::: "memory"); break;
     case 2: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
@@ -212,11 +216,8 @@ __device__ __forceinline__ void team_sync(int T) {
   }
 }
 
-// levels of a triangular sweep run by the team of the lowest T = aux0 warps:
-// per level, chunks of 32 >> lg units (2^lg lanes each) are dealt to the team
-// round robin; x_r -= sum v x_col, then divided by the diagonal (the item's
-// first entry) with kFlagDiag; a team barrier closes each finished level
-// debug trace (CTA (0,0), thread 0, first scenario): (code, clock64) pairs
+// debug trace (CTA (0,0), thread 0, first scenario): (code, clock64) pairs,
+// compiled in with -DBIPM_TRACE (tools/trace_reduce.py)
 struct Tracer {
   long long* buf = nullptr;
   int n = 0;
@@ -227,11 +228,13 @@ struct Tracer {
       buf[2 * n + 1] = clock64();
       ++n;
     }
+#else
+    (void)code;
 #endif
   }
 };
 
-template <int K>
+template <int K, int C>
 __device__ __forceinline__ void step_sweep(const Hdr& h, unsigned lev, unsigned items,
                                            unsigned col, unsigned v, unsigned xb, int tid,
                                            Tracer& tr, int dbg) {
@@ -282,14 +285,14 @@ __device__ __forceinline__ void step_sweep(const Hdr& h, unsigned lev, unsigned 
       }
     }
     tr(200 + L);
-    if (e.w && !(dbg & 2)) team_sync(T);
+    if (e.w && !(dbg & 2)) team_sync<C>(T);
     tr(300 + L);
   }
 }
 
 // rows [r0, r0 + nr) of X_T <- W X_T (W row-major tl x tl in the ring) into
 // temp (row-major, K per row)
-template <int K>
+template <int K, int C>
 __device__ __forceinline__ void step_dense(const Hdr& h, unsigned W, unsigned xb, double* temp,
                                            int t0, int tl, int tid) {
   using Pn = Panel<K>;
@@ -320,7 +323,7 @@ _Pragma("unroll")
 
 // S_p = -(sum_t kxx_t X_col + (sigma_x,i + dw) X_p) over a range of state rows;
 // S (global scratch) uses the panel layout
-template <int K>
+template <int K, int C>
 __device__ __forceinline__ void step_spmv(const Hdr& h, unsigned items, unsigned col, unsigned v,
                                           unsigned sig, unsigned xb, char* S, double dw,
                                           int tid) {
@@ -362,11 +365,11 @@ _Pragma("unroll")
 
 // acc -= A' X over controls [u0, u0 + n_items) of accumulator register q; the
 // consumer owning (u, c) is (u K + c) mod 512
-template <int K>
+template <int K, int C>
 __device__ __forceinline__ void step_acc(const Hdr& h, unsigned items, unsigned col, unsigned v,
                                          unsigned xb, double (&acc)[kMaxQ], int tid) {
   const int q = h.aux0, u0 = h.aux1;
-  const int u = q * (kC / K) + tid / K, c = tid % K;
+  const int u = q * (C / K) + tid / K, c = tid % K;
   const int it = u - u0;
   if (it >= 0 && it < h.n_items) {
     const int4 m = ldsi4(items + 16 * it);
@@ -383,8 +386,9 @@ __device__ __forceinline__ void step_acc(const Hdr& h, unsigned items, unsigned 
   }
 }
 
-template <int K>
-__global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch a) {
+template <int K, int C>
+__global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLaunch a) {
+  constexpr int kThreads = C + 32;
   using Pn = Panel<K>;
   extern __shared__ __align__(1024) unsigned char smem[];
   // layout: X panel (offset 0, 256-byte aligned rows) | temp | barriers |
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch
   if (tid == 0) {
     for (int b = 0; b < kNB; ++b) {
       mbar_init(&full[b], 1);
-      mbar_init(&empty[b], kC / 32);
+      mbar_init(&empty[b], C / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -433,8 +437,8 @@ __global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch
   }
   __syncthreads();
 
-  if (tid >= kC) {  // ------------------------------------------- producer warp
-    const int lane = tid - kC;
+  if (tid >= C) {  // ------------------------------------------- producer warp
+    const int lane = tid - C;
     for (int jb = 0; jb < total; jb += 32) {
       int rec[12];
       {
@@ -513,53 +517,53 @@ __global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch
     const int vshift = (h.par & 1) ^ ((h.par >> 1) & s & 1);
     const unsigned v = vals + 8 * vshift;
     tr(3);
-    if (h.flags & kFPre) consumer_sync();
+    if (h.flags & kFPre) consumer_sync<C>();
     tr(4);
     switch (h.kind) {
       case kScatter: {
         if constexpr (K == 1) {
-          for (int i = tid; i < a.n_x; i += kC) sts1(xb + 8 * i, 0.0);
+          for (int i = tid; i < a.n_x; i += C) sts1(xb + 8 * i, 0.0);
         } else {
-          for (int i = tid; i < nxk2; i += kC) sts2(xb + 16 * i, 0.0, 0.0);
+          for (int i = tid; i < nxk2; i += C) sts2(xb + 16 * i, 0.0, 0.0);
         }
-        consumer_sync();
+        consumer_sync<C>();
         const double* gu = a.gu_v + size_t(s) * a.gu.nnz;
-        for (int e = tid; e < n_gu; e += kC) sts1(xb + gu_list[e].x, gu[gu_list[e].y]);
+        for (int e = tid; e < n_gu; e += C) sts1(xb + gu_list[e].x, gu[gu_list[e].y]);
         break;
       }
       case kSweep:
-        step_sweep<K>(h, lev, items, col, v, xb, tid, tr, a.debug);
+        step_sweep<K, C>(h, lev, items, col, v, xb, tid, tr, a.debug);
         break;
       case kDense:
-        step_dense<K>(h, v, xb, temp, a.t0, a.tl, tid);
+        step_dense<K, C>(h, v, xb, temp, a.t0, a.tl, tid);
         if (h.flags & 2) {
-          consumer_sync();
-          for (int e = tid; e < a.tl * K; e += kC)
+          consumer_sync<C>();
+          for (int e = tid; e < a.tl * K; e += C)
             sts1(xb + Pn::elem(a.t0 + e / K, e % K), temp[e]);
         }
         break;
       case kAcc:
-        step_acc<K>(h, items, col, v, xb, acc, tid);
+        step_acc<K, C>(h, items, col, v, xb, acc, tid);
         break;
       case kSpmv: {
         const int xoff = h.vcount > 0 ? ((h.vcount + 1) * 8 + 15) & ~15 : 0;
         const int xshift = ((h.par >> 2) & 1) ^ ((h.par >> 3) & s & 1);
-        step_spmv<K>(h, items, col, v, vals + xoff + 8 * xshift, xb, S, a.dw, tid);
+        step_spmv<K, C>(h, items, col, v, vals + xoff + 8 * xshift, xb, S, a.dw, tid);
         break;
       }
       case kCopyBack: {
         if constexpr (K == 1) {
-          for (int i = tid; i < a.n_x; i += kC)
+          for (int i = tid; i < a.n_x; i += C)
             sts1(xb + 8 * i, reinterpret_cast<const double*>(S)[i]);
         } else {
-          for (int i = tid; i < nxk2; i += kC) {
+          for (int i = tid; i < nxk2; i += C) {
             const double2 t = reinterpret_cast<const double2*>(S)[i];
             sts2(xb + 16 * i, t.x, t.y);
           }
         }
-        consumer_sync();
+        consumer_sync<C>();
         const double* kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
-        for (int e = tid; e < n_kxu; e += kC)
+        for (int e = tid; e < n_kxu; e += C)
           sts1(xb + kxu_list[e].x, lds1(xb + kxu_list[e].x) + kxu[kxu_list[e].y]);
         break;
       }
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch
         break;
     }
     tr(5);
-    if (h.flags & kFBarrier) consumer_sync();
+    if (h.flags & kFBarrier) consumer_sync<C>();
     tr(6);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[j & (kNB - 1)]);
@@ -584,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) reduce_stream_kernel(StreamLaunch
   double* out = a.partial + size_t(chunk) * a.n_u * a.n_u;
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) {
-    const int it = tid + q * kC;
+    const int it = tid + q * C;
     if (q < a.nq && it < a.n_u * K) {
       const int u = it / K, c = it % K;
       if (c < k) out[size_t(j0 + c) * a.n_u + u] = acc[q];
@@ -628,14 +632,16 @@ size_t stream_smem_bytes(int n_x, int K, int tl, int steps, int list_cap, int ri
          size_t((steps + 3) & ~3) * 4 + size_t(list_cap) * 8 + 16 + ring_bytes;
 }
 
-int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap) {
-  const long long cap =
-      227LL * 1024 - (long long)stream_smem_bytes(n_x, K, tl, steps, list_cap, 0);
+int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap, int ctas_per_sm) {
+  // 228 KB of shared memory per SM, 1 KB of it reserved per resident CTA
+  const long long per_cta = std::min(227LL * 1024, 228LL * 1024 / ctas_per_sm - 1024);
+  const long long cap = per_cta - (long long)stream_smem_bytes(n_x, K, tl, steps, list_cap, 0);
   return cap > 0 ? int(cap & ~15LL) : 0;
 }
 
 void plan_stream_chunks(StreamLaunch& a, int sm_count) {
-  // minimise waves x scenarios per CTA (one CTA per SM)
+  // minimise waves x scenarios per CTA (ctas_per_sm CTAs resident per SM)
+  sm_count *= std::max(1, a.ctas_per_sm);
   const int tiles = (a.n_u + a.K - 1) / a.K;
   long long best = -1;
   int best_n = 1;
@@ -653,27 +659,35 @@ void plan_stream_chunks(StreamLaunch& a, int sm_count) {
   a.nchunks = (a.M + a.chunk - 1) / a.chunk;
 }
 
-template <int K>
+template <int K, int C>
 static void launch_k(const StreamLaunch& a, cudaStream_t st) {
   const int tiles = (a.n_u + K - 1) / K;
   const size_t smem = stream_smem_bytes(a.n_x, K, a.tl, a.steps, a.list_cap, a.ring_bytes);
-  cudaFuncSetAttribute(reduce_stream_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(reduce_stream_kernel<K, C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(smem));
-  reduce_stream_kernel<K><<<dim3(tiles, a.nchunks), kThreads, smem, st>>>(a);
+  reduce_stream_kernel<K, C><<<dim3(tiles, a.nchunks), C + 32, smem, st>>>(a);
   note_launch();
 }
 
 void launch_reduce_stream(const StreamLaunch& a, cudaStream_t st) {
   if (a.M <= 0) return;
   if (a.nq > kMaxQ) throw std::runtime_error("reduce_stream: too many accumulator registers");
-  switch (a.K) {
-    case 1: launch_k<1>(a, st); break;
-    case 2: launch_k<2>(a, st); break;
-    case 4: launch_k<4>(a, st); break;
-    case 8: launch_k<8>(a, st); break;
-    case 16: launch_k<16>(a, st); break;
-    case 32: launch_k<32>(a, st); break;
-    default: throw std::runtime_error("reduce_stream: unsupported tile width");
+  const int code = a.K * 1000 + a.consumers;
+  switch (code) {
+    case 1512: launch_k<1, 512>(a, st); break;
+    case 2512: launch_k<2, 512>(a, st); break;
+    case 4512: launch_k<4, 512>(a, st); break;
+    case 8512: launch_k<8, 512>(a, st); break;
+    case 16512: launch_k<16, 512>(a, st); break;
+    case 32512: launch_k<32, 512>(a, st); break;
+    case 1256: launch_k<1, 256>(a, st); break;
+    case 2256: launch_k<2, 256>(a, st); break;
+    case 4256: launch_k<4, 256>(a, st); break;
+    case 8256: launch_k<8, 256>(a, st); break;
+    case 1128: launch_k<1, 128>(a, st); break;
+    case 2128: launch_k<2, 128>(a, st); break;
+    case 4128: launch_k<4, 128>(a, st); break;
+    default: throw std::runtime_error("reduce_stream: unsupported tile width / consumer count");
   }
   check_launch("reduce_stream");
 }

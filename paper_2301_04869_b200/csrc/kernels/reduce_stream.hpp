@@ -16,6 +16,8 @@ constexpr int kStreamArrays = 6;
 struct StreamLaunch {
   int n_x, n_u, M, K, nq, steps, ring_bytes, t0, tl;
   int chunk, nchunks;
+  int consumers;        // consumer threads per CTA (128, 256 or 512; + one producer warp)
+  int ctas_per_sm;      // co-resident CTAs the shared memory plan allows
   int list_cap;         // tile list entries (G_u + K_xu columns, each rounded to even)
   const int* pat;       // pattern blocks
   const int* issue;     // StepIssue records (12 ints each)
@@ -32,7 +34,7 @@ struct StreamLaunch {
   int debug;         // timing experiments only (BIPM_STREAM_DEBUG): 1 skip sweeps, 2 no team barriers
 };
 
-// consumers per CTA (one producer warp is added)
+// largest consumer count per CTA (one producer warp is added)
 constexpr int kStreamConsumers = 512;
 // producer lookahead cap in steps (< the kernel's 32 mbarrier slots)
 constexpr int kStreamLookahead = 24;
@@ -41,7 +43,7 @@ constexpr int kStreamMaxQ = 10;
 
 size_t stream_smem_bytes(int n_x, int K, int tl, int steps, int list_cap, int ring_bytes);
 // largest ring that fits next to the panel (0 when the panel does not fit)
-int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap);
+int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap, int ctas_per_sm);
 void plan_stream_chunks(StreamLaunch& a, int sm_count);
 void launch_reduce_stream(const StreamLaunch& a, cudaStream_t st);
 // out[col q][row q] = sum_s kuu[s][q] (the K_uu V terms of K_hat)
