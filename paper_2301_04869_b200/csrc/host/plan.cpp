@@ -1,6 +1,7 @@
 #include "plan.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <numeric>
 #include <set>
 
@@ -241,32 +242,68 @@ std::vector<idx> min_degree_order(const Csr& S) {
 
 namespace {
 
-// Trailing block solved densely: the run of narrow forward levels (<= 2 rows)
-// at the end of the schedule, capped at kMaxTail rows (the refactor stages
-// L_TT and U_TT in shared memory to form W = (L_TT U_TT)^{-1}).
-constexpr idx kMaxTail = 112;
-idx choose_tail(const std::vector<idx>& fwd_level, idx n) {
-  idx nlev = 0;
-  for (idx v : fwd_level) nlev = std::max(nlev, v + 1);
-  std::vector<idx> width(size_t(nlev), 0);
-  for (idx v : fwd_level) ++width[size_t(v)];
-  idx t0 = n;
-  for (idx i = n - 1; i >= 0; --i) {
-    if (width[size_t(fwd_level[size_t(i)])] > 2) break;
-    if (n - i > kMaxTail) break;
-    t0 = i;
+// symbolic factorisation of B = P A P' by row subtrees of the etree: the
+// sorted strict-lower column pattern of every row
+std::vector<std::vector<idx>> symbolic_rows(const Csr& A, const std::vector<idx>& perm,
+                                            const std::vector<idx>& iperm) {
+  const idx n = A.rows;
+  std::vector<std::vector<idx>> lrow(static_cast<size_t>(n));
+  std::vector<idx> parent(size_t(n), -1), mark(size_t(n), -1);
+  for (idx i = 0; i < n; ++i) {
+    mark[size_t(i)] = i;
+    const idx oi = perm[size_t(i)];
+    for (idx k = A.ptr[size_t(oi)]; k < A.ptr[size_t(oi) + 1]; ++k) {
+      idx j = iperm[size_t(A.ind[size_t(k)])];
+      if (j >= i) continue;
+      while (mark[size_t(j)] != i) {
+        lrow[size_t(i)].push_back(j);
+        mark[size_t(j)] = i;
+        if (parent[size_t(j)] < 0) parent[size_t(j)] = i;
+        j = parent[size_t(j)];
+      }
+    }
+    std::sort(lrow[size_t(i)].begin(), lrow[size_t(i)].end());
   }
-  // rows in the tail must come after every non-tail row of their levels
-  return (n - t0) >= 8 ? t0 : n;
+  return lrow;
 }
 
+// Dense tail: the rows of the top forward levels of the elimination tree,
+// from the first level after which every level holds at most `width` rows,
+// capped at `max_rows`.  The set is closed under etree ancestors (levels grow
+// towards the root), so moving it to the end of the order keeps the fill.
+// Each level it absorbs is one dependent step less in every triangular sweep;
+// its cost is the dense W = (L_TT U_TT)^{-1} product.
+std::vector<char> choose_tail_rows(const std::vector<std::vector<idx>>& lrow, idx width,
+                                   idx max_rows) {
+  const idx n = idx(lrow.size());
+  std::vector<idx> fl(size_t(n), 0);
+  idx nlev = 0;
+  for (idx i = 0; i < n; ++i) {
+    idx lv = 0;
+    for (idx j : lrow[size_t(i)]) lv = std::max(lv, fl[size_t(j)] + 1);
+    fl[size_t(i)] = lv;
+    nlev = std::max(nlev, lv + 1);
+  }
+  std::vector<idx> cnt(size_t(nlev) + 1, 0);
+  for (idx v : fl) ++cnt[size_t(v)];
+  idx ls = nlev, rows = 0;
+  for (idx l = nlev - 1; l >= 0; --l) {
+    if (cnt[size_t(l)] > width || rows + cnt[size_t(l)] > max_rows) break;
+    rows += cnt[size_t(l)];
+    ls = l;
+  }
+  std::vector<char> tail(size_t(n), 0);
+  if (rows < 8) return tail;
+  for (idx i = 0; i < n; ++i) tail[size_t(i)] = fl[size_t(i)] >= ls;
+  return tail;
+}
 
 }  // namespace
 
 void build_sweeps(LuPlan& P, const std::vector<std::vector<idx>>& lrow,
                   const std::vector<std::vector<idx>>& urow, const std::vector<idx>& fl) {
   const idx n = P.n;
-  P.t0 = choose_tail(fl, n);
+  (void)fl;
   P.tl = n - P.t0;
   const idx t0 = P.t0;
   // --- CSR layouts with direct value indexing
@@ -392,25 +429,25 @@ LuPlan make_lu_plan(const Csr& A) {
   P.perm = min_degree_order(A);
   P.iperm.assign(size_t(n), 0);
   for (idx k = 0; k < n; ++k) P.iperm[size_t(P.perm[size_t(k)])] = k;
-
-  // symbolic factorisation of B = P A P' by row subtrees of the etree
-  std::vector<std::vector<idx>> lrow(static_cast<size_t>(n));
+  std::vector<std::vector<idx>> lrow = symbolic_rows(A, P.perm, P.iperm);
+  // dense tail: move the top levels of the etree to the end of the order
+  // (same elimination tree, same fill) and redo the symbolic pass
   {
-    std::vector<idx> parent(size_t(n), -1), mark(size_t(n), -1);
-    for (idx i = 0; i < n; ++i) {
-      mark[size_t(i)] = i;
-      const idx oi = P.perm[size_t(i)];
-      for (idx k = A.ptr[size_t(oi)]; k < A.ptr[size_t(oi) + 1]; ++k) {
-        idx j = P.iperm[size_t(A.ind[size_t(k)])];
-        if (j >= i) continue;
-        while (mark[size_t(j)] != i) {
-          lrow[size_t(i)].push_back(j);
-          mark[size_t(j)] = i;
-          if (parent[size_t(j)] < 0) parent[size_t(j)] = i;
-          j = parent[size_t(j)];
-        }
-      }
-      std::sort(lrow[size_t(i)].begin(), lrow[size_t(i)].end());
+    idx width = kTailWidth, max_rows = kMaxTail;
+    if (const char* e = std::getenv("BIPM_TAIL_WIDTH")) width = std::atoi(e);
+    if (const char* e = std::getenv("BIPM_TAIL_MAX")) max_rows = std::atoi(e);
+    const std::vector<char> tail = choose_tail_rows(lrow, width, max_rows);
+    std::vector<idx> perm2;
+    perm2.reserve(size_t(n));
+    for (idx k = 0; k < n; ++k)
+      if (!tail[size_t(k)]) perm2.push_back(P.perm[size_t(k)]);
+    P.t0 = idx(perm2.size());
+    for (idx k = 0; k < n; ++k)
+      if (tail[size_t(k)]) perm2.push_back(P.perm[size_t(k)]);
+    if (perm2 != P.perm) {
+      P.perm = perm2;
+      for (idx k = 0; k < n; ++k) P.iperm[size_t(P.perm[size_t(k)])] = k;
+      lrow = symbolic_rows(A, P.perm, P.iperm);
     }
   }
   // U strict upper rows = transpose of the L pattern

@@ -111,6 +111,11 @@ struct LuPlan {
   SweepPlan sL, sU, sUt, sLt;
 };
 
+// dense tail selection (make_lu_plan): top etree levels of at most
+// kTailWidth rows, at most kMaxTail rows (env BIPM_TAIL_WIDTH / BIPM_TAIL_MAX)
+constexpr idx kTailWidth = 6;
+constexpr idx kMaxTail = 320;
+
 std::vector<idx> min_degree_order(const Csr& sym_pattern);
 LuPlan make_lu_plan(const Csr& gx_pattern);
 void build_sweeps(LuPlan& P, const std::vector<std::vector<idx>>& lrow,

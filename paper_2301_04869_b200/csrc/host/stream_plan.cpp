@@ -153,7 +153,15 @@ struct Builder {
       int max_ent = 0;
       for (const Unit& u : us) max_ent = std::max(max_ent, int(u.e - u.b) - (dg ? 1 : 0));
       const int units = int(us.size()) * NG;
-      const int lg = lanes_log2(units, max_ent, S.consumers);
+      int lg = lanes_log2(units, max_ent, S.consumers);
+      // a level whose units fit one warp runs on that warp alone (no team
+      // barrier, __syncwarp between levels): fewer lanes per unit if needed
+      static const int solo_max = [] {
+        const char* e = std::getenv("BIPM_SOLO_UNITS");
+        return e ? std::atoi(e) : 0;
+      }();
+      if (units <= solo_max)
+        while (lg > 0 && units * (1 << lg) > 32) --lg;
       static const int min_team = [] {
         const char* e = std::getenv("BIPM_MIN_TEAM");
         return e ? std::max(1, std::atoi(e)) : 1;
@@ -226,19 +234,14 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   for (idx t = 0; t < L.nnz_f - L.nnz_l; ++t) slot_Ut[size_t(t)] = L.ft_src[size_t(t)];
   for (idx t = 0; t < L.nnz_l; ++t) slot_Lt[size_t(t)] = L.ft_src[size_t(L.nnz_f - L.nnz_l + t)];
 
+  // the dense tail product: one all-warp step; W (tl x tl per scenario) is
+  // read straight from global memory (L2: the 65 column tiles of a scenario
+  // run close together), not staged through the ring
   auto dense = [&](int which) {
     if (tl == 0) return;
-    const int rows = std::max(1, (S.max_step_bytes - 64) / (8 * int(tl)) - 1);
-    for (int r0 = 0; r0 < tl; r0 += rows) {
-      const int nr = std::min<int>(rows, int(tl) - r0);
-      const int fl = (r0 == 0 ? kFlagPre : 0) | (r0 + nr >= tl ? (kFlagCommit | kFlagBarrier) : 0);
-      P p{kStepDense, fl, r0, nr, {}, {}};
-      p.val_arr = kArrDense;
-      p.val_off = which * int(tl) * int(tl) + r0 * int(tl);
-      p.val_count = nr * int(tl);
-      B.emit(p);
-      ++S.n_dense_steps;
-    }
+    P p{kStepDenseG, kFlagPre | kFlagCommit | kFlagBarrier, which, 0, {}, {}};
+    B.emit(p);
+    ++S.n_dense_steps;
   };
   // accumulator rows: control u belongs to register q = (u K + c) / consumers
   const int R = consumers / K;

@@ -26,6 +26,7 @@ enum StepKind : int {
   kStepAcc = 3,       // acc -= (K_xu' or G_u') X over a range of control rows
   kStepSpmv = 4,      // S = -(K~_xx X) over a range of state rows
   kStepCopyBack = 5,  // X = S + K_xu V
+  kStepDenseG = 6,    // X_T <- W X_T with W read from global memory (L2), one step
 };
 // kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
 enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };

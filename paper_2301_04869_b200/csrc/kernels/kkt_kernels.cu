@@ -228,6 +228,94 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F
   }
 }
 
+// Large tails (2 tl^2 doubles beyond shared memory): Gauss-Jordan inversion
+// of the tail block S = L_TT U_TT in place in D's W slot (row-major, global
+// memory, L2-resident), static pivots; W = S^{-1} directly.  The pivots of
+// the elimination are U_TT's diagonal: they go to the factor's diagonal
+// slots for the guard.  The tail block's L/U values themselves are never read
+// by the sweeps (the tail is applied through W), so F keeps S there.
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double* F, double* FT,
+                                                                 double* D,
+                                                                 const double* __restrict__ scale_in,
+                                                                 int* status, double piv_tol,
+                                                                 const int* vs_src, int nnz_vs,
+                                                                 double* VS) {
+  constexpr int kMaxTl = 320;
+  __shared__ double rowk[kMaxTl], colk[kMaxTl];
+  const int s = blockIdx.x;
+  double* Fs = F + size_t(s) * P.nnz_f;
+  const int tl = P.tl, tt = tl * tl, t0 = P.t0;
+  double* W = D + size_t(s) * 2 * tt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int kWarps = BLOCK / 32;
+  for (int i = warp; i < tl; i += kWarps)
+    for (int j = lane; j < tl; j += 32) {
+      const int src = i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
+      W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
+    }
+  __syncthreads();
+  for (int k = 0; k < tl; ++k) {
+    for (int j = threadIdx.x; j < tl; j += BLOCK) {
+      rowk[j] = W[k * tl + j];
+      colk[j] = W[j * tl + k];
+    }
+    __syncthreads();
+    const double piv = rowk[k];
+    const double rp = 1.0 / piv;
+    if (threadIdx.x == 0) Fs[P.diag[t0 + k]] = piv;
+    // rows of this warp, two at a time with all their loads in flight (the
+    // block lives in L2)
+    constexpr int kJ = kMaxTl / 32;
+    for (int i0 = warp; i0 < tl; i0 += 2 * kWarps) {
+      double v0[kJ], v1[kJ];
+      const int i1 = i0 + kWarps;
+      double* w0 = W + size_t(i0) * tl;
+      double* w1 = W + size_t(i1 < tl ? i1 : i0) * tl;
+#pragma unroll
+      for (int c = 0; c < kJ; ++c) {
+        const int j = lane + 32 * c;
+        if (j < tl) {
+          v0[c] = w0[j];
+          v1[c] = w1[j];
+        }
+      }
+      const double f0 = colk[i0] * rp, f1 = i1 < tl ? colk[i1] * rp : 0.0;
+#pragma unroll
+      for (int c = 0; c < kJ; ++c) {
+        const int j = lane + 32 * c;
+        if (j < tl) {
+          const double r = rowk[j];
+          w0[j] = i0 == k ? (j == k ? rp : r * rp) : (j == k ? -f0 : v0[c] - f0 * r);
+          if (i1 < tl) w1[j] = i1 == k ? (j == k ? rp : r * rp) : (j == k ? -f1 : v1[c] - f1 * r);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // pivot guard (linalg.cpp:69-73) over every diagonal of U
+  double bad = 0.0;
+  const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
+  for (int j = threadIdx.x; j < P.n; j += BLOCK) {
+    const double d = Fs[P.diag[j]];
+    if (!(fabs(d) >= floor_) || !isfinite(d)) bad = 1.0;
+  }
+  bad = block_reduce<BLOCK>(bad, true);
+  if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
+  double* FTs = FT + size_t(s) * P.nnz_f;
+  for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
+  if (VS) {
+    double* VSs = VS + size_t(s) * nnz_vs;
+    for (int q = threadIdx.x; q < nnz_vs; q += BLOCK) {
+      const int src = vs_src[q];
+      VSs[q] = src >= 0 ? Fs[src] : 0.0;
+    }
+  }
+  // W' (row-major transpose)
+  for (int i = warp; i < tl; i += kWarps)
+    for (int j = lane; j < tl; j += 32) W[tt + j * tl + i] = W[i * tl + j];
+}
+
 // ----------------------------------------------------------- Schur reduction
 __device__ __forceinline__ FactorView factor_of(const DevLu& P, const double* F, const double* FT,
                                                 const double* D, int s) {
@@ -617,10 +705,16 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
   note_launch();
   check_launch("refactor_levels");
   const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
-  cudaFuncSetAttribute(refactor_tail_kernel<kLuBlock>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       int(smem));
-  refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status, piv_tol,
-                                                            vs_src, nnz_vs, VS);
+  if (smem <= 200 * 1024) {
+    cudaFuncSetAttribute(refactor_tail_kernel<kLuBlock>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status,
+                                                              piv_tol, vs_src, nnz_vs, VS);
+  } else {
+    if (P.tl > 320) throw std::runtime_error("lu refactor: dense tail larger than 320 rows");
+    refactor_tail_gj_kernel<1024><<<M, 1024, 0, st>>>(P, F, FT, D, scale, status, piv_tol,
+                                                      vs_src, nnz_vs, VS);
+  }
   note_launch();
   check_launch("refactor_tail");
 }

@@ -35,8 +35,10 @@ void check_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5 };
+enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5,
+             kDenseG = 6 };
 constexpr int kStepHeaderIntsDev = 16;  // host/stream_plan.hpp kStepHeaderInts
+constexpr int kArrDenseDev = 1;         // host/stream_plan.hpp kArrDense
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -321,6 +323,59 @@ _Pragma("unroll")
   })
 }
 
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// temp = W X_T for the whole tail on the FP64 tensor pipe (DMMA m8n8k4):
+// warp = 8 output rows x all K columns; A = W rows from global memory (L2,
+// eight k-steps of loads in flight), B = X_T from the panel in shared memory
+template <int K, int C>
+__device__ __forceinline__ void step_dense_global(const double* __restrict__ W, unsigned xb,
+                                                  double* temp, int t0, int tl, int tid) {
+  using Pn = Panel<K>;
+  constexpr int NT = K >= 8 ? K / 8 : 1;  // 8-column tiles
+  const int lane = tid & 31, warp = tid >> 5;
+  const int gm = lane >> 2, gk = lane & 3;
+  const int mtiles = (tl + 7) >> 3;
+  for (int mt = warp; mt < mtiles; mt += C / 32) {
+    const int i = mt * 8 + gm;
+    const double* __restrict__ wr = W + size_t(i < tl ? i : 0) * tl;
+    double acc[NT][2];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
+    for (int k0 = 0; k0 < tl; k0 += 32) {
+      double af[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + 4 * u + gk;
+        af[u] = (i < tl && k < tl) ? __ldg(wr + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + 4 * u + gk;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int c = n * 8 + gm;
+          const double bf = (k < tl && c < K) ? lds1(xb + Pn::elem(t0 + k, c)) : 0.0;
+          dmma884(acc[n][0], acc[n][1], af[u], bf);
+        }
+      }
+    }
+    if (i < tl) {
+#pragma unroll
+      for (int n = 0; n < NT; ++n)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int c = n * 8 + 2 * gk + v;
+          if (c < K) temp[i * K + c] = acc[n][v];
+        }
+    }
+  }
+}
+
 // S_p = -(sum_t kxx_t X_col + (sigma_x,i + dw) X_p) over a range of state rows;
 // S (global scratch) uses the panel layout
 template <int K, int C>
@@ -542,6 +597,14 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
             sts1(xb + Pn::elem(a.t0 + e / K, e % K), temp[e]);
         }
         break;
+      case kDenseG: {
+        const double* W = a.arr[kArrDenseDev] + size_t(s) * a.stride[kArrDenseDev] +
+                          size_t(h.aux0) * a.tl * a.tl;
+        step_dense_global<K, C>(W, xb, temp, a.t0, a.tl, tid);
+        consumer_sync<C>();
+        for (int e = tid; e < a.tl * K; e += C) sts1(xb + Pn::elem(a.t0 + e / K, e % K), temp[e]);
+        break;
+      }
       case kAcc:
         step_acc<K, C>(h, items, col, v, xb, acc, tid);
         break;
