@@ -228,11 +228,12 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F
   }
 }
 
-// Large tails (2 tl^2 doubles beyond shared memory): Gauss-Jordan inversion
-// of the tail block S = L_TT U_TT in place in D's W slot (row-major, global
-// memory, L2-resident), static pivots; W = S^{-1} directly.  The pivots of
-// the elimination are U_TT's diagonal: they go to the factor's diagonal
-// slots for the guard.  The tail block's L/U values themselves are never read
+// Large tails (2 tl^2 doubles beyond shared memory): blocked Gauss-Jordan
+// inversion of the tail block S = L_TT U_TT in place in D's W slot
+// (row-major, global memory, L2-resident), static pivots, 16 pivots per pass
+// so the block is streamed tl/16 times instead of tl times; W = S^{-1}.  The
+// pivots of the elimination are U_TT's diagonal: they go to the factor's
+// diagonal slots for the guard.  The tail block's L/U values are never read
 // by the sweeps (the tail is applied through W), so F keeps S there.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double* F, double* FT,
@@ -241,11 +242,15 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
                                                                  int* status, double piv_tol,
                                                                  const int* vs_src, int nnz_vs,
                                                                  double* VS) {
-  constexpr int kMaxTl = 320;
-  __shared__ double rowk[kMaxTl], colk[kMaxTl];
+  constexpr int kB = 16;
+  extern __shared__ double gj[];
   const int s = blockIdx.x;
   double* Fs = F + size_t(s) * P.nnz_f;
   const int tl = P.tl, tt = tl * tl, t0 = P.t0;
+  double* Cb = gj;                      // [tl][kB]   W[:, P]
+  double* Rb = Cb + size_t(tl) * kB;    // [kB][tl]   W[P, :]
+  double* R2 = Rb + size_t(tl) * kB;    // [kB][tl]   A11^{-1} W[P, :]
+  double* Ai = R2 + size_t(tl) * kB;    // [kB][kB]   A11^{-1}
   double* W = D + size_t(s) * 2 * tt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = BLOCK / 32;
@@ -255,40 +260,79 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
     }
   __syncthreads();
-  for (int k = 0; k < tl; ++k) {
-    for (int j = threadIdx.x; j < tl; j += BLOCK) {
-      rowk[j] = W[k * tl + j];
-      colk[j] = W[j * tl + k];
+  for (int k0 = 0; k0 < tl; k0 += kB) {
+    const int bb = min(kB, tl - k0);
+    for (int q = threadIdx.x; q < tl * kB; q += BLOCK) {
+      const int i = q / kB, p = q % kB;
+      Cb[q] = p < bb ? W[size_t(i) * tl + k0 + p] : 0.0;
+      const int pr = q / tl, j = q % tl;
+      Rb[q] = pr < bb ? W[size_t(k0 + pr) * tl + j] : 0.0;
     }
     __syncthreads();
-    const double piv = rowk[k];
-    const double rp = 1.0 / piv;
-    if (threadIdx.x == 0) Fs[P.diag[t0 + k]] = piv;
-    // rows of this warp, two at a time with all their loads in flight (the
-    // block lives in L2)
-    constexpr int kJ = kMaxTl / 32;
-    for (int i0 = warp; i0 < tl; i0 += 2 * kWarps) {
-      double v0[kJ], v1[kJ];
-      const int i1 = i0 + kWarps;
-      double* w0 = W + size_t(i0) * tl;
-      double* w1 = W + size_t(i1 < tl ? i1 : i0) * tl;
+    // A11^{-1} by Gauss-Jordan in one warp (lane = column), pivots to the factor
+    if (warp == 0) {
+      double col[kB];  // lane's column of the working matrix
 #pragma unroll
-      for (int c = 0; c < kJ; ++c) {
-        const int j = lane + 32 * c;
-        if (j < tl) {
-          v0[c] = w0[j];
-          v1[c] = w1[j];
+      for (int r = 0; r < kB; ++r) col[r] = (lane < bb && r < bb) ? Rb[r * tl + k0 + lane] : 0.0;
+      double inv[kB];  // lane's column of the identity being transformed
+#pragma unroll
+      for (int r = 0; r < kB; ++r) inv[r] = (r == lane) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        if (k >= bb) break;
+        const double piv = __shfl_sync(0xffffffffu, col[k], k);
+        if (lane == 0) Fs[P.diag[t0 + k0 + k]] = piv;
+        const double rp = 1.0 / piv;
+        col[k] *= rp;
+        inv[k] *= rp;
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+          const double f = __shfl_sync(0xffffffffu, col[r], k);  // A(r, k)
+          if (r != k) {
+            col[r] -= f * col[k];
+            inv[r] -= f * inv[k];
+          }
         }
       }
-      const double f0 = colk[i0] * rp, f1 = i1 < tl ? colk[i1] * rp : 0.0;
+      if (lane < kB)
 #pragma unroll
-      for (int c = 0; c < kJ; ++c) {
-        const int j = lane + 32 * c;
-        if (j < tl) {
-          const double r = rowk[j];
-          w0[j] = i0 == k ? (j == k ? rp : r * rp) : (j == k ? -f0 : v0[c] - f0 * r);
-          if (i1 < tl) w1[j] = i1 == k ? (j == k ? rp : r * rp) : (j == k ? -f1 : v1[c] - f1 * r);
+        for (int r = 0; r < kB; ++r) Ai[r * kB + lane] = inv[r];
+    }
+    __syncthreads();
+    // R2 = A11^{-1} W[P, :]
+    for (int q = threadIdx.x; q < kB * tl; q += BLOCK) {
+      const int r = q / tl, j = q % tl;
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < kB; ++p) acc += Ai[r * kB + p] * Rb[p * tl + j];
+      R2[q] = acc;
+    }
+    __syncthreads();
+    // rank-bb update of every other row; the pivot rows / columns take the
+    // Gauss-Jordan values
+    for (int i = warp; i < tl; i += kWarps) {
+      const bool ip = i >= k0 && i < k0 + bb;
+      double c[kB];
+#pragma unroll
+      for (int p = 0; p < kB; ++p) c[p] = Cb[i * kB + p];
+      double* wi = W + size_t(i) * tl;
+      for (int j = lane; j < tl; j += 32) {
+        const bool jp = j >= k0 && j < k0 + bb;
+        double v;
+        if (ip) {
+          v = jp ? Ai[(i - k0) * kB + (j - k0)] : R2[(i - k0) * tl + j];
+        } else if (jp) {
+          double acc = 0.0;
+#pragma unroll
+          for (int p = 0; p < kB; ++p) acc += c[p] * Ai[p * kB + (j - k0)];
+          v = -acc;
+        } else {
+          double acc = 0.0;
+#pragma unroll
+          for (int p = 0; p < kB; ++p) acc += c[p] * R2[p * tl + j];
+          v = wi[j] - acc;
         }
+        wi[j] = v;
       }
     }
     __syncthreads();
@@ -711,8 +755,10 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status,
                                                               piv_tol, vs_src, nnz_vs, VS);
   } else {
-    if (P.tl > 320) throw std::runtime_error("lu refactor: dense tail larger than 320 rows");
-    refactor_tail_gj_kernel<1024><<<M, 1024, 0, st>>>(P, F, FT, D, scale, status, piv_tol,
+    const size_t gsm = (size_t(3) * P.tl * 16 + 16 * 16) * sizeof(double);
+    cudaFuncSetAttribute(refactor_tail_gj_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(gsm));
+    refactor_tail_gj_kernel<512><<<M, 512, gsm, st>>>(P, F, FT, D, scale, status, piv_tol,
                                                       vs_src, nnz_vs, VS);
   }
   note_launch();
