@@ -188,6 +188,12 @@ int bipm_ctx_info(bipm_ctx* c, int64_t out[12]);
 /* debug: (step kind, clock64 before its data wait, after it) of every step of
    the streamed reduction's first scenario in CTA (0,0) from the previous
    reduction; n_out triples written */
+/* host only: build the streamed reduction's step program for tile width K,
+   `consumers` threads and a ring of ring_bytes, and validate it (sweep value
+   coverage, ring placement).  out = {violations, steps, nnz_vs, sweep steps,
+   dense steps, acc steps, spmv steps, accumulator registers, t0, tl} */
+int bipm_problem_stream_check(const bipm_problem* p, int32_t K, int32_t consumers,
+                              int32_t ring_bytes, int64_t out[10]);
 /* debug: raw copy of the reduction's stamp/trace buffer */
 int bipm_ctx_debug_buffer(bipm_ctx* c, int64_t* out, int64_t cap, int64_t* n_out);
 int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap, int32_t* n_out);

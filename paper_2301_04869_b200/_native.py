@@ -86,6 +86,8 @@ SIGNATURES = {
                                          ctypes.c_int32]),
     "bipm_ctx_set_host_comm": (ctypes.c_int, [_P, _P, _P, ctypes.c_int32, ctypes.c_int32]),
     "bipm_ctx_phase_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_problem_stream_check": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
+                                                 ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_debug_buffer": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
                                              ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_step_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
@@ -184,6 +186,14 @@ class Problem:
         ct = ctypes.c_int32 if is_int.value else ctypes.c_double
         buf = (ct * n.value).from_address(data.value)
         return np.array(buf, copy=True)
+
+    def stream_check(self, K: int, consumers: int = 512, ring_bytes: int = 48 * 1024) -> dict:
+        """Host-only build + validation of the streamed reduction's step program."""
+        out = (ctypes.c_int64 * 10)()
+        check(lib().bipm_problem_stream_check(self._h, K, consumers, ring_bytes, out))
+        keys = ("violations", "steps", "nnz_vs", "sweep_steps", "dense_steps", "acc_steps",
+                "spmv_steps", "nq", "t0", "tl")
+        return dict(zip(keys, list(out)))
 
     def csr(self, name: str):
         return self.array(name + "_rowptr"), self.array(name + "_colind")

@@ -1,3 +1,4 @@
+#include <algorithm>
 // extern "C" boundary (include/bipm_gpu.h): exceptions become status codes.
 #include "../../include/bipm_gpu.h"
 
@@ -377,6 +378,62 @@ int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap,
     } else {
       e.phase.resize(0);
     }
+  });
+}
+
+int bipm_problem_stream_check(const bipm_problem* bp, int32_t K, int32_t consumers,
+                              int32_t ring_bytes, int64_t out[10]) {
+  return guarded([&] {
+    const Problem& P = *bp->p;
+    const LuPlan& L = P.LU;
+    const StreamProgram S = build_stream_program(L, P.D.g.u, P.D.kxx.out, P.D.kxu.out,
+                                                 P.M.n_u, K, consumers, ring_bytes,
+                                                 kStreamLookahead);
+    int64_t bad = 0;
+    // (1) every factor entry a sweep reads appears in VS, once per sweep: each
+    // L slot twice (L, L'), each U slot twice (U, U'), less the entries the
+    // dense tail covers (both row and column in the tail)
+    std::vector<int> seen(size_t(L.nnz_f), 0);
+    for (idx v : S.vs_src) {
+      if (v < -1 || v >= L.nnz_f) ++bad;
+      if (v >= 0) ++seen[size_t(v)];
+    }
+    auto row_of_l = [&](idx t) { return idx(std::upper_bound(L.l_ptr.begin(), L.l_ptr.end(), t) - L.l_ptr.begin()) - 1; };
+    for (idx t = 0; t < L.nnz_l; ++t) {
+      const bool in_tail = row_of_l(t) >= L.t0 && L.l_col[size_t(t)] >= L.t0;
+      if (seen[size_t(t)] != (in_tail ? 0 : 2)) ++bad;
+    }
+    for (idx i = 0; i < L.n; ++i) {
+      const int want = i >= L.t0 ? 0 : 2;  // U rows of the tail live in W
+      if (seen[size_t(L.diag[size_t(i)])] != want) ++bad;
+      for (idx q = L.u_ptr[size_t(i)]; q < L.u_ptr[size_t(i) + 1]; ++q)
+        if (seen[size_t(L.u_slot[size_t(q)])] != want) ++bad;
+    }
+    // (2) ring placement: a step's region never overlaps a step the producer
+    // may still be ahead of (within its wait distance), cyclically
+    const int n = S.steps;
+    auto size_of = [&](const StepIssue& is) {
+      auto va = [](int c) { return c > 0 ? ((c + 1) * 8 + 15) & ~15 : 0; };
+      return is.pat_bytes + va(is.val_count) + va(is.x_count);
+    };
+    for (int j = 0; j < n; ++j) {
+      const StepIssue& a = S.issue[size_t(j)];
+      if (a.ring_off < 0 || a.ring_off + size_of(a) > ring_bytes) ++bad;
+      for (int d = 1; d < a.wait_delta; ++d) {
+        const StepIssue& b = S.issue[size_t(((j - d) % n + n) % n)];
+        if (a.ring_off < b.ring_off + size_of(b) && b.ring_off < a.ring_off + size_of(a)) ++bad;
+      }
+    }
+    out[0] = bad;
+    out[1] = S.steps;
+    out[2] = S.nnz_vs;
+    out[3] = S.n_sweep_steps;
+    out[4] = S.n_dense_steps;
+    out[5] = S.n_acc_steps;
+    out[6] = S.n_spmv_steps;
+    out[7] = S.nq;
+    out[8] = L.t0;
+    out[9] = L.tl;
   });
 }
 

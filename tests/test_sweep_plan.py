@@ -86,3 +86,36 @@ def test_sweeps_solve_the_factor_pattern(case):
         assert np.abs(x - ref).max() <= 1e-9 * max(1.0, np.abs(ref).max())
     if case == "case1354pegase":
         assert tl >= 64  # the separator chain goes to the dense tail
+
+
+@pytest.mark.parametrize("case", ["case9", "case118", "case1354pegase"])
+@pytest.mark.parametrize("K", [1, 8])
+def test_stream_program_is_valid(case, K):
+    """The streamed reduction's static step program (host/stream_plan.cpp):
+    every factor entry a sweep reads is staged exactly once per sweep, the
+    dense tail's entries never, and no step's ring region overlaps a region the
+    producer may still be refilling (checked on the host, bipm_problem_stream_check)."""
+    p = nat.Problem(case_path(case), 2, 0.05, 0)
+    for ring in (24 * 1024, 48 * 1024):
+        st = p.stream_check(K, 512, ring)
+        assert st["violations"] == 0, st
+        assert st["dense_steps"] == (2 if st["tl"] else 0)
+        assert st["t0"] + st["tl"] == p.n_x
+
+
+def test_dense_tail_keeps_the_fill(monkeypatch):
+    """Moving the top etree levels to the end of the order (the dense tail)
+    keeps the elimination tree, hence the factor's fill, and cuts the levels
+    every triangular sweep walks (make_lu_plan)."""
+    case = case_path("case1354pegase")
+    monkeypatch.setenv("BIPM_TAIL_WIDTH", "0")
+    p0 = nat.Problem(case, 2, 0.05, 0)
+    monkeypatch.delenv("BIPM_TAIL_WIDTH")
+    p1 = nat.Problem(case, 2, 0.05, 0)
+    s0, s1 = p0.array("lu_shape"), p1.array("lu_shape")
+    assert s0[1] == s1[1] and s0[2] == s1[2]  # nnz_l, nnz_f
+    assert s0[4] == 0 and s1[4] > 100          # tail rows
+    lev0 = len(p0.array("lu_sL_lvl_ptr")) - 1
+    lev1 = len(p1.array("lu_sL_lvl_ptr")) - 1
+    assert lev1 < lev0 / 3, (lev0, lev1)
+    assert sorted(p1.array("lu_perm")) == list(range(p1.n_x))
