@@ -153,7 +153,11 @@ struct Builder {
       int max_ent = 0;
       for (const Unit& u : us) max_ent = std::max(max_ent, int(u.e - u.b) - (dg ? 1 : 0));
       const int units = int(us.size()) * NG;
-      int lg = lanes_log2(units, max_ent, S.consumers);
+      static const int max_lanes = [] {
+        const char* e = std::getenv("BIPM_MAX_LANES");
+        return e ? std::atoi(e) : 0;
+      }();
+      int lg = lanes_log2(units, max_ent, max_lanes > 0 ? max_lanes : S.consumers);
       // a level whose units fit one warp runs on that warp alone (no team
       // barrier, __syncwarp between levels): fewer lanes per unit if needed
       static const int solo_max = [] {
