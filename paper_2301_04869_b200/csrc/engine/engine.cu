@@ -121,6 +121,11 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   lu.tail_mul_ptr = up(L.tail_mul_ptr);
   lu.tail_mul_l = up0(L.tail_mul_l);
   lu.tail_mul_u = up0(L.tail_mul_u);
+  lu.rf_nphase = idx(L.rf_phase_ptr.size()) - 1;
+  lu.rf_phase_ptr = up(L.rf_phase_ptr);
+  lu.rf_rec = reinterpret_cast<const int4*>(up(L.rf_rec.empty() ? std::vector<idx>{0, 0, 0, -1} : L.rf_rec));
+  lu.rf_piv = up0(L.rf_piv);
+  lu.rf_pair = reinterpret_cast<const int2*>(up(L.rf_pair.empty() ? std::vector<idx>{0, 0} : L.rf_pair));
   lu.t0 = L.t0;
   lu.tl = L.tl;
   lu.ft_src = up(L.ft_src);

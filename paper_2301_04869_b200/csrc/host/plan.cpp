@@ -623,6 +623,36 @@ LuPlan make_lu_plan(const Csr& A) {
     add_tail(P.diag[size_t(i)]);
     for (idx q = P.u_ptr[size_t(i)]; q < P.u_ptr[size_t(i) + 1]; ++q) add_tail(P.u_slot[size_t(q)]);
   }
+  // flattened phases
+  P.rf_phase_ptr.assign(1, 0);
+  auto rec = [&](idx slot, idx mb, idx me, bool divide) {
+    P.rf_rec.insert(P.rf_rec.end(), {slot, idx(P.rf_pair.size() / 2) + 0, 0, P.a_src[size_t(slot)]});
+    const size_t at = P.rf_rec.size() - 4;
+    for (idx t = mb; t < me; ++t) P.rf_pair.insert(P.rf_pair.end(), {P.mul_l[size_t(t)], P.mul_u[size_t(t)]});
+    P.rf_rec[at + 2] = idx(P.rf_pair.size() / 2);
+    P.rf_piv.push_back(divide ? P.piv_of[size_t(slot)] : -1);
+  };
+  for (size_t lv = 0; lv + 1 < P.nt_lvl_u_ptr.size(); ++lv) {
+    for (idx q = P.nt_lvl_u_ptr[lv]; q < P.nt_lvl_u_ptr[lv + 1]; ++q) {
+      const idx slot = P.nt_lvl_u_slot[size_t(q)];
+      rec(slot, P.mul_ptr[size_t(slot)], P.mul_ptr[size_t(slot) + 1], false);
+    }
+    P.rf_phase_ptr.push_back(idx(P.rf_piv.size()));
+    for (idx q = P.nt_lvl_l_ptr[lv]; q < P.nt_lvl_l_ptr[lv + 1]; ++q) {
+      const idx slot = P.nt_lvl_l_slot[size_t(q)];
+      rec(slot, P.mul_ptr[size_t(slot)], P.mul_ptr[size_t(slot) + 1], true);
+    }
+    P.rf_phase_ptr.push_back(idx(P.rf_piv.size()));
+  }
+  for (size_t it = 0; it < P.tail_slot.size(); ++it) {
+    const idx slot = P.tail_slot[it];
+    P.rf_rec.insert(P.rf_rec.end(), {slot, idx(P.rf_pair.size() / 2), 0, P.a_src[size_t(slot)]});
+    for (idx t = P.tail_mul_ptr[it]; t < P.tail_mul_ptr[it + 1]; ++t)
+      P.rf_pair.insert(P.rf_pair.end(), {P.tail_mul_l[size_t(t)], P.tail_mul_u[size_t(t)]});
+    P.rf_rec[P.rf_rec.size() - 2] = idx(P.rf_pair.size() / 2);
+    P.rf_piv.push_back(-1);
+  }
+  if (!P.tail_slot.empty()) P.rf_phase_ptr.push_back(idx(P.rf_piv.size()));
   return P;
 }
 

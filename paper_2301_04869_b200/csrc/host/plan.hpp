@@ -93,6 +93,11 @@ struct LuPlan {
   // is then factorised densely)
   std::vector<idx> nt_lvl_u_ptr, nt_lvl_u_slot, nt_lvl_l_ptr, nt_lvl_l_slot;
   std::vector<idx> tail_slot, tail_mul_ptr, tail_mul_l, tail_mul_u;
+  // the same split program flattened for refactor_levels_kernel: phases (U
+  // entries of a level, L entries of a level, ..., tail block), one record per
+  // factor slot {slot, pair begin, pair end, G_x slot or -1} + its pivot slot
+  // (-1: no division), multiply pairs (L position, U slot) contiguous
+  std::vector<idx> rf_phase_ptr, rf_rec, rf_piv, rf_pair;
   std::vector<idx> a_src;       // per factor slot: G_x slot or -1 (fill)
   std::vector<idx> piv_of;      // per factor slot: pivot slot for L entries, -1 for U
   std::vector<idx> mul_ptr, mul_l, mul_u;

@@ -31,6 +31,11 @@ struct DevLu {
   int n_nt, n_tail_ent;
   const int *nt_lvl_u_ptr, *nt_lvl_u_slot, *nt_lvl_l_ptr, *nt_lvl_l_slot;
   const int *tail_slot, *tail_mul_ptr, *tail_mul_l, *tail_mul_u;
+  int rf_nphase;
+  const int* rf_phase_ptr;
+  const int4* rf_rec;   // {slot, pair begin, pair end, G_x slot or -1}
+  const int* rf_piv;    // pivot slot or -1
+  const int2* rf_pair;  // (L position, U slot)
   // solve layouts: transposed factor copy and dense tail blocks
   int t0, tl;
   const int* ft_src;     // [nnz_f]

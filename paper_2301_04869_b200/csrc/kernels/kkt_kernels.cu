@@ -92,56 +92,49 @@ __global__ void __launch_bounds__(BLOCK) refactor_levels_kernel(DevLu P,
   for (int i = threadIdx.x; i < nnz_gx; i += BLOCK) mx = fmax(mx, fabs(A[i]));
   const double scale = block_reduce<BLOCK>(mx, true);
   if (threadIdx.x == 0) scale_out[s] = scale;
-
-  for (int lv = 0; lv < P.n_nt; ++lv) {
-    {
-      const int b0 = P.nt_lvl_u_ptr[lv];
-      group_dot<BLOCK>(
-          P.nt_lvl_u_ptr[lv + 1] - b0,
-          [&](int it, int& b, int& e) {
-            const int slot = P.nt_lvl_u_slot[b0 + it];
-            b = P.mul_ptr[slot];
-            e = P.mul_ptr[slot + 1];
-          },
-          [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
-          [&](int it, double acc) {
-            const int slot = P.nt_lvl_u_slot[b0 + it];
-            const int src = P.a_src[slot];
-            Fs[slot] = (src >= 0 ? A[src] : 0.0) - acc;
-          });
-    }
-    __syncthreads();
-    {
-      const int b0 = P.nt_lvl_l_ptr[lv];
-      group_dot<BLOCK>(
-          P.nt_lvl_l_ptr[lv + 1] - b0,
-          [&](int it, int& b, int& e) {
-            const int slot = P.nt_lvl_l_slot[b0 + it];
-            b = P.mul_ptr[slot];
-            e = P.mul_ptr[slot + 1];
-          },
-          [&](int, int t) { return Fs[P.mul_l[t]] * Fs[P.mul_u[t]]; },
-          [&](int it, double acc) {
-            const int slot = P.nt_lvl_l_slot[b0 + it];
-            const int src = P.a_src[slot];
-            Fs[slot] = ((src >= 0 ? A[src] : 0.0) - acc) / Fs[P.piv_of[slot]];
-          });
+  constexpr int kWarps = BLOCK / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int ph = 0; ph < P.rf_nphase; ++ph) {
+    const int b0 = P.rf_phase_ptr[ph], items = P.rf_phase_ptr[ph + 1] - b0;
+    int g = 1;
+    while (g < 32 && items * (g * 2) <= BLOCK) g *= 2;
+    const int per_warp = 32 / g, sub = lane & (g - 1), gid = lane / g;
+    for (int base = warp * per_warp; base < items; base += kWarps * per_warp) {
+      const int item = base + gid;
+      double acc = 0.0;
+      int4 r = make_int4(0, 0, 0, -1);
+      if (item < items) {
+        r = P.rf_rec[b0 + item];
+        // four multiply pairs (and their eight factor values) in flight
+        int t = r.y + sub;
+        for (; t + 3 * g < r.z; t += 4 * g) {
+          int2 pr[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pr[u] = P.rf_pair[t + u * g];
+          double l[4], uu[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            l[u] = Fs[pr[u].x];
+            uu[u] = Fs[pr[u].y];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acc += l[u] * uu[u];
+        }
+        for (; t < r.z; t += g) {
+          const int2 pr = P.rf_pair[t];
+          acc += Fs[pr.x] * Fs[pr.y];
+        }
+      }
+      for (int off = g >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (item < items && sub == 0) {
+        double v = (r.w >= 0 ? A[r.w] : 0.0) - acc;
+        const int piv = P.rf_piv[b0 + item];
+        if (piv >= 0) v /= Fs[piv];
+        Fs[r.x] = v;
+      }
     }
     __syncthreads();
   }
-  // tail block: A - sum over the non-tail pivots (independent entries)
-  group_dot<BLOCK>(
-      P.n_tail_ent,
-      [&](int it, int& b, int& e) {
-        b = P.tail_mul_ptr[it];
-        e = P.tail_mul_ptr[it + 1];
-      },
-      [&](int, int t) { return Fs[P.tail_mul_l[t]] * Fs[P.tail_mul_u[t]]; },
-      [&](int it, double acc) {
-        const int slot = P.tail_slot[it];
-        const int src = P.a_src[slot];
-        Fs[slot] = (src >= 0 ? A[src] : 0.0) - acc;
-      });
 }
 
 template <int BLOCK>
@@ -310,13 +303,23 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     __syncthreads();
     // rank-bb update of every other row; the pivot rows / columns take the
     // Gauss-Jordan values
+    constexpr int kJ = 10;  // tl <= 320: the lane's columns of a row in registers
     for (int i = warp; i < tl; i += kWarps) {
       const bool ip = i >= k0 && i < k0 + bb;
       double c[kB];
 #pragma unroll
       for (int p = 0; p < kB; ++p) c[p] = Cb[i * kB + p];
       double* wi = W + size_t(i) * tl;
-      for (int j = lane; j < tl; j += 32) {
+      double old[kJ];
+#pragma unroll
+      for (int q = 0; q < kJ; ++q) {  // all of the row's loads in flight at once
+        const int j = lane + 32 * q;
+        old[q] = j < tl ? wi[j] : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kJ; ++q) {
+        const int j = lane + 32 * q;
+        if (j >= tl) break;
         const bool jp = j >= k0 && j < k0 + bb;
         double v;
         if (ip) {
@@ -330,7 +333,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
           double acc = 0.0;
 #pragma unroll
           for (int p = 0; p < kB; ++p) acc += c[p] * R2[p * tl + j];
-          v = wi[j] - acc;
+          v = old[q] - acc;
         }
         wi[j] = v;
       }
@@ -346,18 +349,35 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   }
   bad = block_reduce<BLOCK>(bad, true);
   if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
-  double* FTs = FT + size_t(s) * P.nnz_f;
-  for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
-  if (VS) {
-    double* VSs = VS + size_t(s) * nnz_vs;
-    for (int q = threadIdx.x; q < nnz_vs; q += BLOCK) {
-      const int src = vs_src[q];
-      VSs[q] = src >= 0 ? Fs[src] : 0.0;
+}
+
+// the solve layouts after the Gauss-Jordan tail, spread over the whole GPU:
+// FT and VS gathers from F, W' = transpose(W)
+__global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, double* FT,
+                                        double* D, const int* __restrict__ vs_src, int nnz_vs,
+                                        double* VS, int M) {
+  const long long n1 = (long long)M * P.nnz_f, n2 = (long long)M * nnz_vs;
+  const int tl = P.tl, tt = tl * tl;
+  const long long n3 = (long long)M * tt;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n1 + n2 + n3;
+       q += stride) {
+    if (q < n1) {
+      const int s = int(q / P.nnz_f), e = int(q % P.nnz_f);
+      FT[q] = F[size_t(s) * P.nnz_f + P.ft_src[e]];
+    } else if (q < n1 + n2) {
+      const long long r = q - n1;
+      const int s = int(r / nnz_vs), e = int(r % nnz_vs);
+      const int src = vs_src[e];
+      VS[r] = src >= 0 ? F[size_t(s) * P.nnz_f + src] : 0.0;
+    } else {
+      const long long r = q - n1 - n2;
+      const int s = int(r / tt), e = int(r % tt);
+      const int i = e / tl, j = e % tl;  // W'(i, j) = W(j, i)
+      double* W = D + size_t(s) * 2 * tt;
+      W[tt + e] = W[j * tl + i];
     }
   }
-  // W' (row-major transpose)
-  for (int i = warp; i < tl; i += kWarps)
-    for (int j = lane; j < tl; j += 32) W[tt + j * tl + i] = W[i * tl + j];
 }
 
 // ----------------------------------------------------------- Schur reduction
@@ -745,7 +765,7 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     cudaMalloc(&scale, size_t(M) * sizeof(double));
     scale_n = M;
   }
-  refactor_levels_kernel<kLuBlock><<<M, kLuBlock, 0, st>>>(P, gx, nnz_gx, F, scale);
+  refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
   check_launch("refactor_levels");
   const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
@@ -760,6 +780,10 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                          int(gsm));
     refactor_tail_gj_kernel<512><<<M, 512, gsm, st>>>(P, F, FT, D, scale, status, piv_tol,
                                                       vs_src, nnz_vs, VS);
+    note_launch();
+    check_launch("refactor_tail_gj");
+    refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
+                                                     M);
   }
   note_launch();
   check_launch("refactor_tail");
