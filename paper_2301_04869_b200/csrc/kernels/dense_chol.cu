@@ -54,11 +54,13 @@ __global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
   __shared__ double A[kNb][kNb + 1];
   __shared__ int fail;
   if (*info) return;
-  const int w = min(kNb, n - c0), r = threadIdx.x;
-  if (r < w)
-    for (int c = 0; c <= r; ++c) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
+  const int w = min(kNb, n - c0), r = threadIdx.x;  // one warp: lane = row
+  // column by column: each load is one coalesced column segment, all in flight
+#pragma unroll
+  for (int c = 0; c < kNb; ++c)
+    if (c < w && r < w && c <= r) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
   if (r == 0) fail = 0;
-  __syncthreads();
+  __syncwarp();
   for (int j = 0; j < w; ++j) {
     if (r == j) {
       const double ajj = A[j][j];
@@ -67,20 +69,21 @@ __global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
       else
         A[j][j] = sqrt(ajj);
     }
-    __syncthreads();
+    __syncwarp();
     if (fail) break;
     if (r > j && r < w) A[r][j] /= A[j][j];
-    __syncthreads();
+    __syncwarp();
     if (r > j && r < w)
       for (int k = j + 1; k <= r; ++k) A[r][k] -= A[r][j] * A[k][j];
-    __syncthreads();
+    __syncwarp();
   }
   if (fail) {
     if (r == 0) *info = fail;
     return;
   }
-  if (r < w)
-    for (int c = 0; c <= r; ++c) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
+#pragma unroll
+  for (int c = 0; c < kNb; ++c)
+    if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
 }
 
 // (2) L21 = A21 L11^{-T}: one thread per row below the panel
@@ -169,22 +172,30 @@ __global__ void __launch_bounds__(128) panel_update_kernel(double* K, int n, int
       }
 }
 
-// L L' x = b, blocked by 32 rows: one warp solves each diagonal triangle by
-// shuffles, the CTA updates the remaining rows.
+// L L' x = b, blocked by 32 rows: the CTA stages each 32 x 32 diagonal block
+// in shared memory, one warp solves it by shuffles, the CTA updates the
+// remaining rows.
 __global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __restrict__ L, int n,
                                                             double* b) {
   extern __shared__ double x[];  // n
+  __shared__ double Dg[32][33];  // diagonal block, Dg[r][c] = L(c0 + r, c0 + c)
   for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
-  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  auto stage = [&](int c0, int w) {
+    __syncthreads();
+    const int r = threadIdx.x & 31, c = threadIdx.x >> 5;
+    if (c < 32) Dg[r][c] = (r < w && c < w) ? L[size_t(c0 + c) * n + c0 + r] : 0.0;
+    __syncthreads();
+  };
   for (int c0 = 0; c0 < n; c0 += 32) {  // forward
     const int w = min(32, n - c0);
+    stage(c0, w);
     if (warp == 0) {
       double xv = lane < w ? x[c0 + lane] : 0.0;
       for (int j = 0; j < w; ++j) {
-        if (lane == j) xv /= L[size_t(c0 + j) * n + c0 + j];
+        if (lane == j) xv /= Dg[j][j];
         const double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane > j && lane < w) xv -= L[size_t(c0 + j) * n + c0 + lane] * xj;
+        if (lane > j && lane < w) xv -= Dg[lane][j] * xj;
       }
       if (lane < w) x[c0 + lane] = xv;
     }
@@ -194,16 +205,16 @@ __global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __res
       for (int j = 0; j < w; ++j) acc += L[size_t(c0 + j) * n + i] * x[c0 + j];
       x[i] -= acc;
     }
-    __syncthreads();
   }
   for (int c0 = ((n - 1) / 32) * 32; c0 >= 0; c0 -= 32) {  // backward with L'
     const int w = min(32, n - c0);
+    stage(c0, w);
     if (warp == 0) {
       double xv = lane < w ? x[c0 + lane] : 0.0;
       for (int j = w - 1; j >= 0; --j) {
-        if (lane == j) xv /= L[size_t(c0 + j) * n + c0 + j];
+        if (lane == j) xv /= Dg[j][j];
         const double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane < j) xv -= L[size_t(c0 + lane) * n + c0 + j] * xj;
+        if (lane < j) xv -= Dg[j][lane] * xj;
       }
       if (lane < w) x[c0 + lane] = xv;
     }
@@ -213,8 +224,8 @@ __global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __res
       for (int j = 0; j < w; ++j) acc += L[size_t(i) * n + c0 + j] * x[c0 + j];
       x[i] -= acc;
     }
-    __syncthreads();
   }
+  __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = x[i];
 }
 
