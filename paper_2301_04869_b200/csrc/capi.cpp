@@ -470,7 +470,7 @@ int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, in
     cudaStream_t st;
     cuda_check(cudaStreamCreate(&st), "stream");
     DArr<double> K, b;
-    DArr<int> info(1);
+    DArr<int> info(4);
     K.upload(k_colmajor, size_t(n) * n, st);
     b.upload(rhs, size_t(n), st);
     launch_shift_cholesky(K.get(), n, info.get(), nullptr, st);

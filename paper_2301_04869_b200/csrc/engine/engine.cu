@@ -184,7 +184,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));
   rhs_part.resize(Ms * size_t(Mo.n_u));
-  chol_info.resize(1);
+  chol_info.resize(4);  // status + an 8-byte |K|_inf slot (dense_chol.cu)
 
   red.lu = lu;
   red.gu = gu_p.v;

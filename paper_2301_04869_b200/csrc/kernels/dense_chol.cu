@@ -11,7 +11,10 @@
 // Per panel of kNb = 32 columns: (1) factor the diagonal block in shared
 // memory, (2) L21 = A21 L11^{-T} row-parallel, (3) A22 -= L21 L21' on the lower
 // triangle in 64 x 64 tiles, four warps of 32 x 32 DMMA fragments each.
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <algorithm>
 #include <stdexcept>
 #include <string>
 
@@ -172,6 +175,162 @@ __global__ void __launch_bounds__(128) panel_update_kernel(double* K, int n, int
       }
 }
 
+// The whole blocked factorisation in one cooperative launch (no per-panel
+// launch gaps): per panel, CTA 0 factors the diagonal block, the grid solves
+// the panel rows, the grid updates the trailing lower tiles on DMMA; grid-wide
+// barriers between the phases.  A failed pivot stops every CTA consistently.
+__global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, int* info) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double buf[2 * kTile * (kNb + 1)];
+  __shared__ int fail;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // shift (kkt.cpp:965-968): |K|_inf over the grid, CTA 0 applies it
+  {
+    double mx = 0.0;
+    for (long long i = blockIdx.x * 128LL + tid; i < (long long)n * n; i += gridDim.x * 128LL)
+      mx = fmax(mx, fabs(K[i]));
+    for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+    if (lane == 0) buf[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      double v = fmax(fmax(buf[0], buf[1]), fmax(buf[2], buf[3]));
+      // max of non-negative doubles: compare as integers
+      atomicMax(reinterpret_cast<unsigned long long*>(info) + 1,
+                static_cast<unsigned long long>(__double_as_longlong(v)));
+    }
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    const double kinf = __longlong_as_double(
+        static_cast<long long>(reinterpret_cast<unsigned long long*>(info)[1]));
+    const double shift = 1e-13 * fmax(1.0, kinf);
+    for (int i = tid; i < n; i += 128) K[size_t(i) * n + i] += shift;
+    if (tid == 0) info[0] = 0;
+  }
+  grid.sync();
+  for (int c0 = 0; c0 < n; c0 += kNb) {
+    const int w = min(kNb, n - c0);
+    // (1) diagonal block on CTA 0, warp 0
+    if (blockIdx.x == 0 && warp == 0) {
+      double(*A)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
+      const int r = lane;
+#pragma unroll
+      for (int c = 0; c < kNb; ++c)
+        if (c < w && r < w && c <= r) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
+      if (r == 0) fail = 0;
+      __syncwarp();
+      for (int j = 0; j < w; ++j) {
+        if (r == j) {
+          const double ajj = A[j][j];
+          if (!(ajj > 0.0) || isnan(ajj))
+            fail = c0 + j + 1;
+          else
+            A[j][j] = sqrt(ajj);
+        }
+        __syncwarp();
+        if (fail) break;
+        if (r > j && r < w) A[r][j] /= A[j][j];
+        __syncwarp();
+        if (r > j && r < w)
+          for (int k = j + 1; k <= r; ++k) A[r][k] -= A[r][j] * A[k][j];
+        __syncwarp();
+      }
+      if (fail) {
+        if (r == 0) info[0] = fail;
+      } else {
+#pragma unroll
+        for (int c = 0; c < kNb; ++c)
+          if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
+      }
+    }
+    grid.sync();
+    if (*(volatile int*)info) return;
+    const int rows = n - c0 - w;
+    if (rows <= 0) break;
+    // (2) L21 = A21 L11^{-T}, one thread per row
+    {
+      double(*L)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
+      for (int q = tid; q < w * w; q += 128) {
+        const int rr = q / w, cc = q % w;
+        L[rr][cc] = cc <= rr ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
+      }
+      __syncthreads();
+      for (int rb = blockIdx.x * 128; rb < rows; rb += gridDim.x * 128) {
+        const int r = c0 + w + rb + tid;
+        if (r < n) {
+          double x[kNb];
+#pragma unroll
+          for (int j = 0; j < kNb; ++j) x[j] = j < w ? K[size_t(c0 + j) * n + r] : 0.0;
+#pragma unroll
+          for (int j = 0; j < kNb; ++j) {
+            if (j >= w) break;
+            double v = x[j];
+#pragma unroll
+            for (int k = 0; k < j; ++k) v -= x[k] * L[j][k];
+            x[j] = v / L[j][j];
+          }
+#pragma unroll
+          for (int j = 0; j < kNb; ++j)
+            if (j < w) K[size_t(c0 + j) * n + r] = x[j];
+        }
+      }
+    }
+    grid.sync();
+    // (3) A22 -= L21 L21' on the lower 64 x 64 tiles
+    {
+      double(*sa)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
+      double(*sb)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf + kTile * (kNb + 1));
+      const int t0 = c0 + kNb;
+      const int nt = (rows + kTile - 1) / kTile;
+      for (int tile = blockIdx.x; tile < nt * (nt + 1) / 2; tile += gridDim.x) {
+        int I = int((sqrt(8.0 * tile + 1.0) - 1.0) / 2.0);
+        while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+        while (I * (I + 1) / 2 > tile) --I;
+        const int J = tile - I * (I + 1) / 2;
+        const int r0 = t0 + I * kTile, s0 = t0 + J * kTile;
+        __syncthreads();
+        for (int q = tid; q < kTile * kNb; q += 128) {
+          const int rr = q % kTile, kk = q / kTile;
+          const int ra = r0 + rr, rb = s0 + rr;
+          sa[rr][kk] = ra < n ? K[size_t(c0 + kk) * n + ra] : 0.0;
+          sb[rr][kk] = rb < n ? K[size_t(c0 + kk) * n + rb] : 0.0;
+        }
+        __syncthreads();
+        const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+        double acc[4][4][2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2) acc[a][b2][0] = acc[a][b2][1] = 0.0;
+        const int gm = lane >> 2, gk = lane & 3;
+#pragma unroll
+        for (int k = 0; k < kNb; k += 4) {
+          double af[4], bf[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) af[a] = sa[wm + a * 8 + gm][k + gk];
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2) bf[b2] = sb[wn + b2 * 8 + gm][k + gk];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b2 = 0; b2 < 4; ++b2) dmma(acc[a][b2][0], acc[a][b2][1], af[a], bf[b2]);
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int r = r0 + wm + a * 8 + gm, c = s0 + wn + b2 * 8 + 2 * gk + v;
+              if (r < n && c < n && c <= r) K[size_t(c) * n + r] -= acc[a][b2][v];
+            }
+      }
+    }
+    grid.sync();
+  }
+}
+
 // L L' x = b, blocked by 32 rows: the CTA stages each 32 x 32 diagonal block
 // in shared memory, one warp solves it by shuffles, the CTA updates the
 // remaining rows.
@@ -232,6 +391,30 @@ __global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __res
 }  // namespace
 
 void launch_blocked_cholesky(double* K, int n, int* info, cudaStream_t st) {
+  // one cooperative launch when the grid fits co-resident (info holds two
+  // 8-byte slots: the status and the |K|_inf scratch)
+  static int coop_blocks = -1;
+  if (coop_blocks < 0) {
+    int dev = 0, sms = 0, per = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cholesky_coop_kernel, 128, 0);
+    coop_blocks = coop ? sms * per : 0;
+  }
+  const int rows0 = n - kNb;
+  const int nt0 = (rows0 + kTile - 1) / kTile;
+  const int want = std::max(nt0 * (nt0 + 1) / 2, (rows0 + 127) / 128);
+  const int grid = std::min(want, coop_blocks);
+  if (grid >= 1 && coop_blocks > 0) {
+    cudaMemsetAsync(info, 0, 16, st);
+    void* args[] = {&K, &n, &info};
+    const cudaError_t e = cudaLaunchCooperativeKernel(
+        reinterpret_cast<void*>(cholesky_coop_kernel), dim3(grid), dim3(128), args, 0, st);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("cholesky_coop: ") + cudaGetErrorString(e));
+    note_launch();
+    return;
+  }
   shift_kernel<<<1, 1024, 0, st>>>(K, n, info);
   note_launch();
   for (int c0 = 0; c0 < n; c0 += kNb) {
