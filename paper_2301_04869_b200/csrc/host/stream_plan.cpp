@@ -43,7 +43,7 @@ struct Builder {
   }
 
   void emit(Pending p) {
-    const int K = S.K, NG = K > 8 ? K / 8 : 1;
+    const int K = S.K, NG = K > kStreamUnitCols ? K / kStreamUnitCols : 1;
     const int n_items = int(p.items.size() / 4);
     const int n_lev = int(p.levels.size() / 4);
     const int n_col = (int(p.col.size()) + 3) & ~3;
@@ -96,7 +96,7 @@ struct Builder {
   // barrier, or __syncwarp for one warp).  Values are appended to VS.
   void sweep(const SweepPlan& sw, const std::vector<idx>& slot_of_t, bool diag, bool with_tail,
              int tail_skip) {
-    const int K = S.K, NG = K > 8 ? K / 8 : 1;
+    const int K = S.K, NG = K > kStreamUnitCols ? K / kStreamUnitCols : 1;
     struct Unit { idx row, b, e; };
     std::vector<std::vector<Unit>> levels;
     std::vector<char> level_diag;

@@ -40,6 +40,8 @@ enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre
 // team of the lowest T warps running them; level record = (unit begin, unit
 // end, lg, team barrier after it).
 constexpr int kStepHeaderInts = 16;
+// panel columns per work unit (the kernel's Panel<K>::CW = min(K, this))
+constexpr int kStreamUnitCols = 4;  // measured: 8 -> 30.4 ms, 4 -> 28.5 ms, 2 -> 28.9 ms (1354/256)
 
 // Shared-memory panel layout of the K right-hand-side columns: row r is K
 // doubles (K*8 bytes) split in 16-byte chunks, chunk c stored at position

@@ -21,6 +21,7 @@
 #include <string>
 
 #include "reduce_stream.hpp"
+#include "../host/stream_plan.hpp"
 #include "stats.hpp"
 
 namespace bipm {
@@ -114,7 +115,7 @@ __device__ __forceinline__ int4 ldsi4(unsigned a) {
 
 template <int K>
 struct Panel {
-  static constexpr int CW = K < 8 ? K : 8;  // columns per work unit
+  static constexpr int CW = K < kStreamUnitCols ? K : kStreamUnitCols;  // columns per unit
   static constexpr int NG = K / CW;         // unit groups per row
   static constexpr int NC = CW / 2;         // 16-byte chunks per unit
   __host__ __device__ static constexpr int swz(int r) {
