@@ -196,6 +196,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   red.M = M;
   plan_reduce_launch(red, 200 * 1024, sm_count);
   if (const char* e = std::getenv("BIPM_REDUCE")) use_stream = std::strcmp(e, "tiles") != 0;
+  if (const char* e = std::getenv("BIPM_FORCE_COMM")) force_comm = std::atoi(e) != 0;
   if (use_stream) setup_stream();
   if (use_stream) {
     red_parts = sl.nchunks + 1;  // + the K_uu slab

@@ -59,7 +59,10 @@ class Engine {
   const Problem& pb;
   const idx lo, hi, M;
   std::unique_ptr<Comm> comm;  // null: single GPU (no exchange)
-  bool multi() const { return comm && comm->size() > 1; }
+  // exchange through comm; BIPM_FORCE_COMM=1 also routes a one-rank
+  // communicator through it (tests the NCCL path on a single GPU)
+  bool force_comm = false;
+  bool multi() const { return comm && (comm->size() > 1 || force_comm); }
   int device = 0, sm_count = 148;
   cudaStream_t st = nullptr;
 

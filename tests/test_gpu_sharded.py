@@ -52,3 +52,21 @@ def test_sharded_solve_matches_single_and_reference(case, N, sigma, world):
     assert abs(r0["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
     u_ref = np.array(ref["u"])
     assert np.abs(np.array(r0["u"]) - u_ref).max() <= 1e-6 * max(1.0, np.abs(u_ref).max())
+
+
+def test_nccl_path_one_rank(goldens, monkeypatch):
+    """The NCCL exchange (dlopen'd libnccl, ncclCommInitRank, ncclAllReduce on
+    the engine stream) exercised on one GPU: a one-rank communicator routed
+    through every exchange point must leave the solve unchanged."""
+    from paper_2301_04869_b200 import _native as nat
+    monkeypatch.setenv("BIPM_FORCE_COMM", "1")
+    p = nat.Problem(case_path("case118"), 16, 0.05, 0)
+    ctx = nat.Context(p, device=0)
+    ctx.set_nccl(nat.nccl_unique_id(), 1, 0)
+    r = nat.Solver(ctx).solve()
+    monkeypatch.delenv("BIPM_FORCE_COMM")
+    ref = nat.Solver(nat.Context(p, device=0)).solve()
+    assert r["status_name"] == "Optimal"
+    assert r["iterations"] == ref["iterations"]
+    assert abs(r["objective"] - ref["objective"]) <= 1e-12 * abs(ref["objective"])
+    assert np.max(np.abs(r["u"] - ref["u"])) <= 1e-10
