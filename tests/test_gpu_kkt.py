@@ -74,7 +74,7 @@ def synthetic_condensed(p, N, seed):
     }
 
 
-@pytest.mark.parametrize("case,N", [("case118", 16), ("case1354pegase", 3)])
+@pytest.mark.parametrize("case,N", [("case118", 16), ("case1354pegase", 3), ("case2869pegase", 2)])
 def test_reduce_matches_oracle_on_grid_patterns(case, N):
     p = nat.Problem(case_path(case), N, 0.05, 0)
     v = synthetic_condensed(p, N, seed=7)
