@@ -52,41 +52,50 @@ __global__ void shift_kernel(double* K, int n, int* info) {
   if (threadIdx.x == 0) *info = 0;
 }
 
-// (1) diagonal block [c0, c0+w) in shared memory, one thread per row
+// Cholesky of the w x w diagonal block held in one warp's registers (lane r
+// holds row r, a[c] = A(r, c) for c <= r); column values travel by shuffle.
+// The block is padded to 32 x 32 with the identity so the loop is branch-free
+// and the shuffles stay warp-converged.  Returns 0, or 1 + the first failing
+// column (pivot not > 0 or NaN).
+__device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane) {
+  if (lane >= w) {
+#pragma unroll
+    for (int c = 0; c < kNb; ++c) a[c] = (c == lane) ? 1.0 : 0.0;
+  }
+  int fail = 0;
+#pragma unroll
+  for (int j = 0; j < kNb; ++j) {
+    const double ajj = __shfl_sync(0xffffffffu, a[j], j);
+    const bool bad = !(ajj > 0.0) || isnan(ajj);
+    fail = (fail == 0 && bad) ? j + 1 : fail;
+    const double d = sqrt(bad ? 1.0 : ajj);
+    const double rd = 1.0 / d;  // one reciprocal per pivot (all lanes alike)
+    a[j] = lane == j ? d : (lane > j ? a[j] * rd : a[j]);  // L(r, j)
+#pragma unroll
+    for (int k = j + 1; k < kNb; ++k) {
+      const double lkj = __shfl_sync(0xffffffffu, a[j], k);  // L(k, j)
+      a[k] = lane >= k ? a[k] - a[j] * lkj : a[k];
+    }
+  }
+  return fail;
+}
+
+// (1) diagonal block [c0, c0+w), one warp, lane = row
 __global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
-  __shared__ double A[kNb][kNb + 1];
-  __shared__ int fail;
   if (*info) return;
-  const int w = min(kNb, n - c0), r = threadIdx.x;  // one warp: lane = row
-  // column by column: each load is one coalesced column segment, all in flight
+  const int w = min(kNb, n - c0), r = threadIdx.x;
+  double a[kNb];
 #pragma unroll
   for (int c = 0; c < kNb; ++c)
-    if (c < w && r < w && c <= r) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
-  if (r == 0) fail = 0;
-  __syncwarp();
-  for (int j = 0; j < w; ++j) {
-    if (r == j) {
-      const double ajj = A[j][j];
-      if (!(ajj > 0.0) || isnan(ajj))
-        fail = c0 + j + 1;
-      else
-        A[j][j] = sqrt(ajj);
-    }
-    __syncwarp();
-    if (fail) break;
-    if (r > j && r < w) A[r][j] /= A[j][j];
-    __syncwarp();
-    if (r > j && r < w)
-      for (int k = j + 1; k <= r; ++k) A[r][k] -= A[r][j] * A[k][j];
-    __syncwarp();
-  }
+    a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
+  const int fail = warp_chol32(a, w, r);
   if (fail) {
-    if (r == 0) *info = fail;
+    if (r == 0) *info = c0 + fail;
     return;
   }
 #pragma unroll
   for (int c = 0; c < kNb; ++c)
-    if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
+    if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = a[c];
 }
 
 // (2) L21 = A21 L11^{-T}: one thread per row below the panel
@@ -179,11 +188,17 @@ __global__ void __launch_bounds__(128) panel_update_kernel(double* K, int n, int
 // launch gaps): per panel, CTA 0 factors the diagonal block, the grid solves
 // the panel rows, the grid updates the trailing lower tiles on DMMA; grid-wide
 // barriers between the phases.  A failed pivot stops every CTA consistently.
+__device__ long long* g_chol_stamps = nullptr;  // debug: per-panel phase clocks of CTA 0
+
 __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, int* info) {
   namespace cg = cooperative_groups;
+  long long* stamps = (blockIdx.x == 0 && threadIdx.x == 0) ? g_chol_stamps : nullptr;
+  int ns = 0;
+  auto stamp = [&] {
+    if (stamps && ns < 256) stamps[ns++] = clock64();
+  };
   cg::grid_group grid = cg::this_grid();
   __shared__ double buf[2 * kTile * (kNb + 1)];
-  __shared__ int fail;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // shift (kkt.cpp:965-968): |K|_inf over the grid, CTA 0 applies it
   {
@@ -211,40 +226,27 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
   grid.sync();
   for (int c0 = 0; c0 < n; c0 += kNb) {
     const int w = min(kNb, n - c0);
+    stamp();
     // (1) diagonal block on CTA 0, warp 0
     if (blockIdx.x == 0 && warp == 0) {
-      double(*A)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
       const int r = lane;
+      double a[kNb];
 #pragma unroll
       for (int c = 0; c < kNb; ++c)
-        if (c < w && r < w && c <= r) A[r][c] = K[size_t(c0 + c) * n + c0 + r];
-      if (r == 0) fail = 0;
-      __syncwarp();
-      for (int j = 0; j < w; ++j) {
-        if (r == j) {
-          const double ajj = A[j][j];
-          if (!(ajj > 0.0) || isnan(ajj))
-            fail = c0 + j + 1;
-          else
-            A[j][j] = sqrt(ajj);
-        }
-        __syncwarp();
-        if (fail) break;
-        if (r > j && r < w) A[r][j] /= A[j][j];
-        __syncwarp();
-        if (r > j && r < w)
-          for (int k = j + 1; k <= r; ++k) A[r][k] -= A[r][j] * A[k][j];
-        __syncwarp();
-      }
-      if (fail) {
-        if (r == 0) info[0] = fail;
+        a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
+      stamp();
+      const int f = warp_chol32(a, w, r);
+      if (f) {
+        if (r == 0) info[0] = c0 + f;
       } else {
 #pragma unroll
         for (int c = 0; c < kNb; ++c)
-          if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = A[r][c];
+          if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = a[c];
       }
     }
+    stamp();
     grid.sync();
+    stamp();
     if (*(volatile int*)info) return;
     const int rows = n - c0 - w;
     if (rows <= 0) break;
@@ -265,10 +267,17 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
 #pragma unroll
           for (int j = 0; j < kNb; ++j) {
             if (j >= w) break;
-            double v = x[j];
+            double v0 = x[j], v1 = 0.0, v2 = 0.0, v3 = 0.0;  // four independent chains
 #pragma unroll
-            for (int k = 0; k < j; ++k) v -= x[k] * L[j][k];
-            x[j] = v / L[j][j];
+            for (int k = 0; k + 3 < j; k += 4) {
+              v0 -= x[k] * L[j][k];
+              v1 -= x[k + 1] * L[j][k + 1];
+              v2 -= x[k + 2] * L[j][k + 2];
+              v3 -= x[k + 3] * L[j][k + 3];
+            }
+#pragma unroll
+            for (int k = j & ~3; k < j; ++k) v0 -= x[k] * L[j][k];
+            x[j] = ((v0 + v1) + (v2 + v3)) / L[j][j];
           }
 #pragma unroll
           for (int j = 0; j < kNb; ++j)
@@ -276,7 +285,9 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
         }
       }
     }
+    stamp();
     grid.sync();
+    stamp();
     // (3) A22 -= L21 L21' on the lower 64 x 64 tiles
     {
       double(*sa)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
@@ -290,11 +301,23 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
         const int J = tile - I * (I + 1) / 2;
         const int r0 = t0 + I * kTile, s0 = t0 + J * kTile;
         __syncthreads();
-        for (int q = tid; q < kTile * kNb; q += 128) {
-          const int rr = q % kTile, kk = q / kTile;
-          const int ra = r0 + rr, rb = s0 + rr;
-          sa[rr][kk] = ra < n ? K[size_t(c0 + kk) * n + ra] : 0.0;
-          sb[rr][kk] = rb < n ? K[size_t(c0 + kk) * n + rb] : 0.0;
+        {
+          // all 32 loads of this thread in flight, then the shared-memory stores
+          constexpr int kPer = kTile * kNb / 128;
+          double va[kPer], vb[kPer];
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const int q = tid + u * 128, rr = q % kTile, kk = q / kTile;
+            const int ra = r0 + rr, rb = s0 + rr;
+            va[u] = ra < n ? K[size_t(c0 + kk) * n + ra] : 0.0;
+            vb[u] = rb < n ? K[size_t(c0 + kk) * n + rb] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < kPer; ++u) {
+            const int q = tid + u * 128, rr = q % kTile, kk = q / kTile;
+            sa[rr][kk] = va[u];
+            sb[rr][kk] = vb[u];
+          }
         }
         __syncthreads();
         const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
@@ -327,6 +350,7 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
             }
       }
     }
+    stamp();
     grid.sync();
   }
 }
