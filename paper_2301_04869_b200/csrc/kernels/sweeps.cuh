@@ -127,6 +127,45 @@ template <int BLOCK, int K>
 __device__ void dense_tail_gemm(const DevLu& P, const double* __restrict__ W, double* X) {
   const int tl = P.tl, t0 = P.t0;
   if (tl == 0) return;
+  if constexpr (K == 1) {
+    // single right-hand side: a warp per output row, lanes split the row of W
+    // (coalesced), four rows' loads in flight per warp, shuffle reduction;
+    // result j of a warp (row warp*4 + (j/4)*stride + j%4) is kept by lane j%32
+    constexpr int kWarps = BLOCK / 32, kRows = 4, kStride = kWarps * kRows;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double res0 = 0.0, res1 = 0.0;
+    int j = 0;
+    for (int i0 = warp * kRows; i0 < tl; i0 += kStride) {
+      double acc[kRows];
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) acc[q] = 0.0;
+      for (int k = lane; k < tl; k += 32) {
+        const double xk = X[t0 + k];
+#pragma unroll
+        for (int q = 0; q < kRows; ++q)
+          if (i0 + q < tl) acc[q] += __ldg(W + size_t(i0 + q) * tl + k) * xk;
+      }
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        for (int off = 16; off > 0; off >>= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], off);
+        if (lane == ((j + q) & 31)) {
+          if ((j + q) >> 5)
+            res1 = acc[q];
+          else
+            res0 = acc[q];
+        }
+      }
+      j += kRows;
+    }
+    __syncthreads();
+    for (int slot = 0; slot < 2; ++slot) {
+      const int jj = slot * 32 + lane;
+      const int row = warp * kRows + (jj / kRows) * kStride + (jj % kRows);
+      if (jj < j && row < tl) X[t0 + row] = slot ? res1 : res0;
+    }
+    __syncthreads();
+    return;
+  }
   constexpr int kMaxOut = 8;
   const int n = tl * K;
   double r[kMaxOut];
