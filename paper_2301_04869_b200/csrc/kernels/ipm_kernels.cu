@@ -478,32 +478,23 @@ __global__ void __launch_bounds__(kB) aug_residual_kernel(AugResidualArgs a, dou
   block_partial<1>(vmax, ops, partial);
 }
 
-__global__ void aug_residual_u_kernel(AugResidualArgs a, double* o1u, double* out) {
-  constexpr int ops[1] = {kMax};
-  double vmax[1] = {0.0};
-  const IpmDims& d = a.d;
-  for (int i = threadIdx.x; i < d.n_u; i += kB) {
-    dd_pair t{a.r1u[i], 0.0};
-    t = dd_add_d(t, (a.sigma_u[i] + a.dw) * a.p.pu[i]);
-    for (int s = 0; s < d.M; ++s) {
-      const size_t k = (size_t(s) * d.n_u + i) * 2;
-      t = dd_add(t, dd_pair{a.o1u_part[k], a.o1u_part[k + 1]});
-    }
-    const double o = t.hi + t.lo;
-    o1u[i] = o;
-    vmax[0] = fmax(vmax[0], fabs(o));
-  }
-  block_partial<1>(vmax, ops, out);
-}
-
+// per control: the double-double sum over the scenarios, one warp per
+// control, lanes over scenarios, then a fixed xor tree (deterministic order)
 __global__ void aug_residual_u_local_kernel(AugResidualArgs a, double* dd) {
   const IpmDims& d = a.d;
-  for (int i = threadIdx.x + blockIdx.x * kB; i < d.n_u; i += kB * gridDim.x) {
-    dd_pair t{0.0, 0.0};
-    for (int s = 0; s < d.M; ++s) {
-      const size_t k = (size_t(s) * d.n_u + i) * 2;
-      t = dd_add(t, dd_pair{a.o1u_part[k], a.o1u_part[k + 1]});
-    }
+  const int lane = threadIdx.x & 31;
+  const int i = (blockIdx.x * kB + threadIdx.x) >> 5;
+  if (i >= d.n_u) return;  // whole warps exit together
+  dd_pair t{0.0, 0.0};
+  for (int s = lane; s < d.M; s += 32) {
+    const size_t k = (size_t(s) * d.n_u + i) * 2;
+    t = dd_add(t, dd_pair{a.o1u_part[k], a.o1u_part[k + 1]});
+  }
+  for (int off = 16; off > 0; off >>= 1) {
+    const dd_pair o{__shfl_xor_sync(0xffffffffu, t.hi, off), __shfl_xor_sync(0xffffffffu, t.lo, off)};
+    t = (lane & off) ? dd_add(o, t) : dd_add(t, o);  // same operand order on both lanes
+  }
+  if (lane == 0) {
     dd[2 * i] = t.hi;
     dd[2 * i + 1] = t.lo;
   }
@@ -923,14 +914,9 @@ void launch_aug_residual(const AugResidualArgs& a, double* partial, double* out1
   check("aug_residual");
 }
 
-void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st) {
-  aug_residual_u_kernel<<<1, kB, 0, st>>>(a, o1u, out1);
-  note_launch();
-  check("aug_residual_u");
-}
-
 void launch_aug_residual_u_local(const AugResidualArgs& a, double* dd, cudaStream_t st) {
-  aug_residual_u_local_kernel<<<ew_blocks(a.d.n_u), kB, 0, st>>>(a, dd);
+  const long long threads = (long long)a.d.n_u * 32;
+  aug_residual_u_local_kernel<<<int((threads + kB - 1) / kB), kB, 0, st>>>(a, dd);
   note_launch();
   check("aug_residual_u_local");
 }
@@ -941,6 +927,21 @@ void launch_aug_residual_u_finish(const AugResidualArgs& a, const double* dd, do
   note_launch();
   check("aug_residual_u_finish");
 }
+
+// the scenario sums spread over the GPU (warp per control), then one CTA
+// adds r1u + (sigma_u + dw) p_u and reduces the max
+void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st) {
+  static double* dd = nullptr;
+  static int dd_n = 0;
+  if (dd_n < a.d.n_u) {
+    if (dd) cudaFree(dd);
+    cudaMalloc(&dd, size_t(2) * a.d.n_u * sizeof(double));
+    dd_n = a.d.n_u;
+  }
+  launch_aug_residual_u_local(a, dd, st);
+  launch_aug_residual_u_finish(a, dd, o1u, out1, st);
+}
+
 
 void launch_rhs_scale(const IpmDims& d, const double* r1x, const double* r1u, const double* r2,
                       const double* r3, const double* r4, double* partial, double* out1,
