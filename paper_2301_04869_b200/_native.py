@@ -112,6 +112,18 @@ def lib():
     return _lib
 
 
+def _destroy(obj, fn_name: str) -> None:
+    """Release a C-ABI handle; quiet at interpreter shutdown (module globals gone)."""
+    h = getattr(obj, "_h", None)
+    if not h:
+        return
+    obj._h = None
+    try:
+        getattr(_lib, fn_name)(h)
+    except Exception:  # noqa: BLE001
+        pass
+
+
 def check(code: int) -> None:
     if code != 0:
         msg = lib().bipm_last_error().decode()
@@ -199,9 +211,7 @@ class Problem:
         return self.array(name + "_rowptr"), self.array(name + "_colind")
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().bipm_problem_destroy(self._h)
-            self._h = None
+        _destroy(self, "bipm_problem_destroy")
 
 
 class Context:
@@ -305,9 +315,7 @@ class Context:
         return dict(zip(keys, list(out)))
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().bipm_ctx_destroy(self._h)
-            self._h = None
+        _destroy(self, "bipm_ctx_destroy")
 
 
 class Solver:
@@ -356,9 +364,7 @@ class Solver:
         return self.result()
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            lib().bipm_solver_destroy(self._h)
-            self._h = None
+        _destroy(self, "bipm_solver_destroy")
 
 
 def counters() -> dict:
