@@ -264,17 +264,19 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     __syncthreads();
     // A11^{-1} by Gauss-Jordan in one warp (lane = column), pivots to the factor
     if (warp == 0) {
+      // padded with the identity beyond bb: a branch-free loop keeps the
+      // shuffles warp-converged
       double col[kB];  // lane's column of the working matrix
 #pragma unroll
-      for (int r = 0; r < kB; ++r) col[r] = (lane < bb && r < bb) ? Rb[r * tl + k0 + lane] : 0.0;
+      for (int r = 0; r < kB; ++r)
+        col[r] = (lane < bb && r < bb) ? Rb[r * tl + k0 + lane] : (r == lane ? 1.0 : 0.0);
       double inv[kB];  // lane's column of the identity being transformed
 #pragma unroll
       for (int r = 0; r < kB; ++r) inv[r] = (r == lane) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
-        if (k >= bb) break;
         const double piv = __shfl_sync(0xffffffffu, col[k], k);
-        if (lane == 0) Fs[P.diag[t0 + k0 + k]] = piv;
+        if (lane == 0 && k < bb) Fs[P.diag[t0 + k0 + k]] = piv;
         const double rp = 1.0 / piv;
         col[k] *= rp;
         inv[k] *= rp;
