@@ -53,11 +53,12 @@ __global__ void shift_kernel(double* K, int n, int* info) {
 }
 
 // Cholesky of the w x w diagonal block held in one warp's registers (lane r
-// holds row r, a[c] = A(r, c) for c <= r); column values travel by shuffle.
-// The block is padded to 32 x 32 with the identity so the loop is branch-free
-// and the shuffles stay warp-converged.  Returns 0, or 1 + the first failing
+// holds row r, a[c] = A(r, c) for c <= r); each pivot's column L(:, j) is
+// broadcast through a 32-double shared buffer (shuffles of a whole column
+// would keep 31 doubles live per step and spill).  Padded to 32 x 32 with the
+// identity so the loop is branch-free.  Returns 0, or 1 + the first failing
 // column (pivot not > 0 or NaN).
-__device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane) {
+__device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane, double* colbuf) {
   if (lane >= w) {
 #pragma unroll
     for (int c = 0; c < kNb; ++c) a[c] = (c == lane) ? 1.0 : 0.0;
@@ -69,13 +70,13 @@ __device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane) {
     const bool bad = !(ajj > 0.0) || isnan(ajj);
     fail = (fail == 0 && bad) ? j + 1 : fail;
     const double d = sqrt(bad ? 1.0 : ajj);
-    const double rd = 1.0 / d;  // one reciprocal per pivot (all lanes alike)
+    const double rd = 1.0 / d;
     a[j] = lane == j ? d : (lane > j ? a[j] * rd : a[j]);  // L(r, j)
+    colbuf[lane] = a[j];
+    __syncwarp();
 #pragma unroll
-    for (int k = j + 1; k < kNb; ++k) {
-      const double lkj = __shfl_sync(0xffffffffu, a[j], k);  // L(k, j)
-      a[k] = lane >= k ? a[k] - a[j] * lkj : a[k];
-    }
+    for (int k = j + 1; k < kNb; ++k) a[k] = lane >= k ? a[k] - a[j] * colbuf[k] : a[k];
+    __syncwarp();
   }
   return fail;
 }
@@ -84,11 +85,12 @@ __device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane) {
 __global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
   if (*info) return;
   const int w = min(kNb, n - c0), r = threadIdx.x;
+  __shared__ double colbuf[kNb];
   double a[kNb];
 #pragma unroll
   for (int c = 0; c < kNb; ++c)
     a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
-  const int fail = warp_chol32(a, w, r);
+  const int fail = warp_chol32(a, w, r, colbuf);
   if (fail) {
     if (r == 0) *info = c0 + fail;
     return;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
       for (int c = 0; c < kNb; ++c)
         a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
       stamp();
-      const int f = warp_chol32(a, w, r);
+      const int f = warp_chol32(a, w, r, buf);
       if (f) {
         if (r == 0) info[0] = c0 + f;
       } else {

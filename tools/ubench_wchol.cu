@@ -5,6 +5,7 @@
 namespace bipm {
 __global__ void wchol(double* out, long long* cyc, int reps) {
   const int lane = threadIdx.x;
+  __shared__ double colbuf[kNb];
   double a[kNb];
   long long t0 = 0, t1 = 0;
   int f = 0;
@@ -13,7 +14,7 @@ __global__ void wchol(double* out, long long* cyc, int reps) {
     for (int c = 0; c < kNb; ++c) a[c] = c <= lane ? (c == lane ? 40.0 + r : 1.0 / (1 + c + lane)) : 0.0;
     __syncwarp();
     if (r == 1) t0 = clock64();
-    f += warp_chol32(a, 32, lane);
+    f += warp_chol32(a, 32, lane, colbuf);
     __syncwarp();
     if (r == reps - 1) t1 = clock64();
   }
