@@ -255,9 +255,16 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
     // (2) L21 = A21 L11^{-T}, one thread per row
     {
       double(*L)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
+      double* rdiag = buf + kNb * (kNb + 1);  // reciprocals of the diagonal
       for (int q = tid; q < w * w; q += 128) {
         const int rr = q / w, cc = q % w;
         L[rr][cc] = cc <= rr ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
+      }
+      __syncthreads();
+      if (tid < kNb) rdiag[tid] = tid < w ? 1.0 / L[tid][tid] : 1.0;
+      for (int q = tid; q < kNb * kNb; q += 128) {  // zero the padding of L
+        const int rr = q / kNb, cc = q % kNb;
+        if (rr >= w || cc >= w) L[rr][cc] = 0.0;
       }
       __syncthreads();
       for (int rb = blockIdx.x * 128; rb < rows; rb += gridDim.x * 128) {
@@ -266,20 +273,14 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
           double x[kNb];
 #pragma unroll
           for (int j = 0; j < kNb; ++j) x[j] = j < w ? K[size_t(c0 + j) * n + r] : 0.0;
+          // column-oriented substitution: after x_j is final, every later
+          // x_k is updated independently (one multiply-add deep per step);
+          // L is zero-padded beyond w, rdiag to 1
 #pragma unroll
           for (int j = 0; j < kNb; ++j) {
-            if (j >= w) break;
-            double v0 = x[j], v1 = 0.0, v2 = 0.0, v3 = 0.0;  // four independent chains
+            x[j] *= rdiag[j];
 #pragma unroll
-            for (int k = 0; k + 3 < j; k += 4) {
-              v0 -= x[k] * L[j][k];
-              v1 -= x[k + 1] * L[j][k + 1];
-              v2 -= x[k + 2] * L[j][k + 2];
-              v3 -= x[k + 3] * L[j][k + 3];
-            }
-#pragma unroll
-            for (int k = j & ~3; k < j; ++k) v0 -= x[k] * L[j][k];
-            x[j] = ((v0 + v1) + (v2 + v3)) / L[j][j];
+            for (int k = j + 1; k < kNb; ++k) x[k] -= L[k][j] * x[j];
           }
 #pragma unroll
           for (int j = 0; j < kNb; ++j)
@@ -341,6 +342,8 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
 #pragma unroll
             for (int b2 = 0; b2 < 4; ++b2) dmma(acc[a][b2][0], acc[a][b2][1], af[a], bf[b2]);
         }
+        // read-modify-write of the tile: all 32 loads in flight first
+        double old[4][4][2];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -348,7 +351,16 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
               const int r = r0 + wm + a * 8 + gm, c = s0 + wn + b2 * 8 + 2 * gk + v;
-              if (r < n && c < n && c <= r) K[size_t(c) * n + r] -= acc[a][b2][v];
+              old[a][b2][v] = (r < n && c < n && c <= r) ? K[size_t(c) * n + r] : 0.0;
+            }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b2 = 0; b2 < 4; ++b2)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int r = r0 + wm + a * 8 + gm, c = s0 + wn + b2 * 8 + 2 * gk + v;
+              if (r < n && c < n && c <= r) K[size_t(c) * n + r] = old[a][b2][v] - acc[a][b2][v];
             }
       }
     }
