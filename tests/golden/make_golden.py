@@ -7,6 +7,8 @@ from /root/reference) and stores compressed fixtures:
   case118_N4_s005_it5.npz   case118, 4 scenarios, sigma 0.05, seed 0, iterate 5
   case118_N4_s005_it20.npz  same problem, iterate 20 (near convergence)
   solves.json               full reference solves (iterations, objective, logs)
+  solves_large.json         case1354pegase / 256 full solve; case2869pegase / 512
+                            capped at 4 iterations (per-iteration logs), 8 threads
 
 Each .npz holds the model maps, patterns, the iterate, the derivative bundle,
 the augmented and condensed systems, K_hat / rhs at delta_w in {0, 1e-4}
@@ -42,6 +44,32 @@ SOLVES = [
 ]
 
 
+LARGE = [  # (case, N, sigma, seed, max_iter); run with --large (hours of CPU)
+    ("case1354pegase", 256, 0.05, 0, 300),
+    ("case2869pegase", 512, 0.05, 0, 4),
+]
+
+
+def large():
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1")
+    path = os.path.join(HERE, "solves_large.json")
+    out = json.load(open(path)) if os.path.exists(path) else {}
+    threads = str(min(8, os.cpu_count() or 1))
+    for case, N, sigma, seed, max_iter in LARGE:
+        key = f"{case}_N{N}_s{sigma}_seed{seed}" + (f"_it{max_iter}" if max_iter < 300 else "")
+        if key in out:
+            continue
+        r = subprocess.run([REF, "solve", "--case", f"{DATA}/{case}.m", "--N", str(N), "--sigma",
+                            str(sigma), "--seed", str(seed), "--groups", threads, "--workers",
+                            threads, "--max-iter", str(max_iter)],
+                           check=True, env=env, capture_output=True, text=True)
+        j = json.loads(r.stdout)
+        out[key] = j
+        print(key, j["status"], j["iterations"], j["objective"])
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def main():
     env = dict(os.environ, OPENBLAS_NUM_THREADS="1")
     for case, N, sigma, seed, it in DUMPS:
@@ -72,4 +100,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    large() if "--large" in sys.argv else main()

@@ -68,3 +68,18 @@ def test_case1354_N256_matches_reference_at_scale():
     assert abs(r["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
     u_ref = np.array(ref["u"])
     assert np.abs(r["u"] - u_ref).max() <= 1e-6 * max(1.0, np.abs(u_ref).max())
+
+
+def test_case2869_N512_first_iterations_match_reference():
+    """BASELINE configs[3] workload (one GPU): the first four interior-point
+    iterations match the reference's per-iteration log (objective, primal and
+    dual infeasibility, step lengths) — the whole solve takes the reference
+    CPU about two hours, so the golden is capped (tests/golden/make_golden.py)."""
+    ref = json.load(open(os.path.join(GOLDEN, "solves_large.json")))[
+        "case2869pegase_N512_s0.05_seed0_it4"]
+    p = nat.Problem(case_path("case2869pegase"), 512, 0.05, 0)
+    r = nat.Solver(nat.Context(p), max_iter=4).solve()
+    assert r["status_name"] == "MaxIter" and r["iterations"] == ref["iterations"] == 4
+    for k, (g, c) in enumerate(zip(r["logs"], ref["logs"])):
+        for key in ("objective", "inf_pr", "inf_du", "alpha_p", "alpha_d", "mu"):
+            assert abs(g[key] - c[key]) <= 1e-6 * max(1.0, abs(c[key])), (k, key, g[key], c[key])
