@@ -80,7 +80,10 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
   const std::map<std::string, const std::vector<idx>*> ivecs = {
       {"lu_perm", &P.LU.perm},       {"lu_fwd_ptr", &P.LU.fwd_ptr}, {"lu_bwd_ptr", &P.LU.bwd_ptr},
       {"lu_l_ptr", &P.LU.l_ptr},     {"lu_l_col", &P.LU.l_col},     {"lu_u_ptr", &P.LU.u_ptr},
-      {"lu_u_col", &P.LU.u_col},     {"lu_mul_ptr", &P.LU.mul_ptr}};
+      {"lu_u_col", &P.LU.u_col},     {"lu_mul_ptr", &P.LU.mul_ptr},
+      {"lu_rf_phase_ptr", &P.LU.rf_phase_ptr}, {"lu_rf_rec", &P.LU.rf_rec},
+      {"lu_rf_piv", &P.LU.rf_piv},   {"lu_rf_pair", &P.LU.rf_pair},
+      {"lu_u_slot", &P.LU.u_slot},   {"lu_diag", &P.LU.diag}};
   if (auto it = ivecs.find(name); it != ivecs.end()) return ints(*it->second);
   static thread_local std::vector<idx> scalars;
   if (name == "lu_shape") {
@@ -88,7 +91,7 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
     return ints(scalars);
   }
   const std::map<std::string, const std::vector<idx>*> lu_more = {
-      {"lu_ft_src", &P.LU.ft_src},     {"lu_diag", &P.LU.diag},     {"lu_a_src", &P.LU.a_src},
+      {"lu_ft_src", &P.LU.ft_src},     {"lu_a_src", &P.LU.a_src},
       {"lu_dense_src0", &P.LU.dense_src[0]}, {"lu_dense_src1", &P.LU.dense_src[1]}};
   if (auto it = lu_more.find(name); it != lu_more.end()) return ints(*it->second);
   const std::map<std::string, const SweepPlan*> sweeps = {

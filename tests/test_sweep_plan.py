@@ -119,3 +119,68 @@ def test_dense_tail_keeps_the_fill(monkeypatch):
     lev1 = len(p1.array("lu_sL_lvl_ptr")) - 1
     assert lev1 < lev0 / 3, (lev0, lev1)
     assert sorted(p1.array("lu_perm")) == list(range(p1.n_x))
+
+
+@pytest.mark.parametrize("case", ["case118", "case1354pegase"])
+def test_split_refactor_program_factors_the_pattern(case):
+    """The flattened refactor program (refactor_levels_kernel: Crout phases of
+    the pivots before the dense tail, then the tail block's partial sums)
+    followed by a dense LU of the tail block (refactor_tail_* kernels),
+    executed in numpy on a random diagonally dominant matrix with G_x's
+    pattern, reproduces P A P' = L U."""
+    p = nat.Problem(case_path(case), 2, 0.05, 0)
+    n, nnz_l, nnz_f, t0, tl = p.array("lu_shape")
+    rp, ci = p.array("gx_p_rowptr"), p.array("gx_p_colind")
+    rng = np.random.default_rng(5)
+    A = np.zeros((n, n))
+    for i in range(n):
+        for k in range(rp[i], rp[i + 1]):
+            A[i, ci[k]] = rng.normal()
+        A[i, i] = 10.0 + abs(A[i]).sum()
+    vals = np.array([A[i, ci[k]] for i in range(n) for k in range(rp[i], rp[i + 1])])
+    phase = p.array("lu_rf_phase_ptr")
+    rec = p.array("lu_rf_rec").reshape(-1, 4)
+    piv = p.array("lu_rf_piv")
+    pair = p.array("lu_rf_pair").reshape(-1, 2)
+    F = np.zeros(nnz_f)
+    for ph in range(len(phase) - 1):
+        new = {}
+        for it in range(phase[ph], phase[ph + 1]):
+            slot, b, e, src = rec[it]
+            acc = sum(F[pair[t, 0]] * F[pair[t, 1]] for t in range(b, e))
+            v = (vals[src] if src >= 0 else 0.0) - acc
+            if piv[it] >= 0:
+                v /= F[piv[it]]
+            new[slot] = v
+        for k, v in new.items():  # a phase's entries are independent
+            F[k] = v
+    # dense LU of the tail block (what the tail kernels do), written back
+    src0, src1 = p.array("lu_dense_src0"), p.array("lu_dense_src1")
+    T = np.zeros((tl, tl))
+    for q in range(tl * tl):
+        a, b = q % tl, q // tl
+        s = src0[q] if a > b else src1[q]
+        T[a, b] = F[s] if s >= 0 else 0.0
+    for k in range(tl - 1):
+        T[k + 1:, k] /= T[k, k]
+        T[k + 1:, k + 1:] -= np.outer(T[k + 1:, k], T[k, k + 1:])
+    for q in range(tl * tl):
+        a, b = q % tl, q // tl
+        s = src0[q] if a > b else src1[q]
+        if s >= 0:
+            F[s] = T[a, b]
+    # assemble L, U and compare with P A P'
+    perm = p.array("lu_perm")
+    l_ptr, l_col = p.array("lu_l_ptr"), p.array("lu_l_col")
+    u_ptr, u_col, u_slot, diag = (p.array("lu_u_ptr"), p.array("lu_u_col"), p.array("lu_u_slot"),
+                                  p.array("lu_diag"))
+    L = np.eye(n)
+    U = np.zeros((n, n))
+    for i in range(n):
+        for t in range(l_ptr[i], l_ptr[i + 1]):
+            L[i, l_col[t]] = F[t]
+        U[i, i] = F[diag[i]]
+        for t in range(u_ptr[i], u_ptr[i + 1]):
+            U[i, u_col[t]] = F[u_slot[t]]
+    PA = A[np.ix_(perm, perm)]
+    assert np.abs(L @ U - PA).max() <= 1e-10 * np.abs(PA).max()
