@@ -12,14 +12,18 @@
 //   launch_recover_slack   recover_slack_dual          kkt.cpp:172-188
 //   launch_condense        condense / run_condense     kkt.cpp:123-170, sparse.cpp:208-214
 //   launch_shift_cholesky  solve_reduced shift+factor  kkt.cpp:965-971, linalg.cpp:129-145
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kkt_kernels.hpp"
 #include "sweeps.cuh"
 
 #include "stats.hpp"
+
+namespace cg = cooperative_groups;
 
 namespace bipm {
 
@@ -222,12 +226,17 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F
 }
 
 // Large tails (2 tl^2 doubles beyond shared memory): blocked Gauss-Jordan
-// inversion of the tail block S = L_TT U_TT in place in D's W slot
-// (row-major, global memory, L2-resident), static pivots, 16 pivots per pass
-// so the block is streamed tl/16 times instead of tl times; W = S^{-1}.  The
-// pivots of the elimination are U_TT's diagonal: they go to the factor's
-// diagonal slots for the guard.  The tail block's L/U values are never read
-// by the sweeps (the tail is applied through W), so F keeps S there.
+// inversion of the tail block S = L_TT U_TT into D's W slot (row-major,
+// global memory, L2-resident), static pivots, 16 pivots per pass so the block
+// is streamed tl/16 times instead of tl times; W = S^{-1}.  Passes ping-pong
+// between D's two tt slots (the W' slot is scratch until the layouts kernel)
+// and end in the W slot.  A thread-block cluster of CL CTAs may share one
+// scenario (small M: the GPU would otherwise idle): every CTA forms the 16x16
+// pivot inverse redundantly and updates the rows r = rank (mod CL), one
+// cluster barrier per pass.  The pivots of the elimination are U_TT's
+// diagonal: they go to the factor's diagonal slots for the guard.  The tail
+// block's L/U values are never read by the sweeps (the tail is applied
+// through W), so F keeps S there.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double* F, double* FT,
                                                                  double* D,
@@ -237,24 +246,33 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
                                                                  double* VS) {
   constexpr int kB = 16;
   extern __shared__ double gj[];
-  const int s = blockIdx.x;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int ncl = int(cluster.num_blocks()), crank = int(cluster.block_rank());
+  const int s = blockIdx.x / ncl;
   double* Fs = F + size_t(s) * P.nnz_f;
   const int tl = P.tl, tt = tl * tl, t0 = P.t0;
   double* Cb = gj;                      // [tl][kB]   W[:, P]
   double* Rb = Cb + size_t(tl) * kB;    // [kB][tl]   W[P, :]
   double* R2 = Rb + size_t(tl) * kB;    // [kB][tl]   A11^{-1} W[P, :]
   double* Ai = R2 + size_t(tl) * kB;    // [kB][kB]   A11^{-1}
-  double* W = D + size_t(s) * 2 * tt;
+  const int npass = (tl + kB - 1) / kB;
+  double* const Wbase = D + size_t(s) * 2 * tt;  // slot b at Wbase + b tt
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   constexpr int kWarps = BLOCK / 32;
-  for (int i = warp; i < tl; i += kWarps)
-    for (int j = lane; j < tl; j += 32) {
-      const int src = i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
-      W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
-    }
-  __syncthreads();
-  for (int k0 = 0; k0 < tl; k0 += kB) {
+  const int row0 = crank * kWarps + warp, rstep = kWarps * ncl;
+  {
+    double* W = Wbase + (npass & 1) * tt;
+    for (int i = row0; i < tl; i += rstep)
+      for (int j = lane; j < tl; j += 32) {
+        const int src = i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
+        W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
+      }
+  }
+  cluster.sync();
+  for (int k0 = 0, pass = 0; k0 < tl; k0 += kB, ++pass) {
     const int bb = min(kB, tl - k0);
+    const double* W = Wbase + ((npass - pass) & 1) * tt;
+    double* Wn = Wbase + ((npass - pass - 1) & 1) * tt;
     for (int q = threadIdx.x; q < tl * kB; q += BLOCK) {
       const int i = q / kB, p = q % kB;
       Cb[q] = p < bb ? W[size_t(i) * tl + k0 + p] : 0.0;
@@ -276,7 +294,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
         const double piv = __shfl_sync(0xffffffffu, col[k], k);
-        if (lane == 0 && k < bb) Fs[P.diag[t0 + k0 + k]] = piv;
+        if (crank == 0 && lane == 0 && k < bb) Fs[P.diag[t0 + k0 + k]] = piv;
         const double rp = 1.0 / piv;
         col[k] *= rp;
         inv[k] *= rp;
@@ -303,15 +321,16 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       R2[q] = acc;
     }
     __syncthreads();
-    // rank-bb update of every other row; the pivot rows / columns take the
+    // rank-bb update of this CTA's rows; the pivot rows / columns take the
     // Gauss-Jordan values
     constexpr int kJ = 10;  // tl <= 320: the lane's columns of a row in registers
-    for (int i = warp; i < tl; i += kWarps) {
+    for (int i = row0; i < tl; i += rstep) {
       const bool ip = i >= k0 && i < k0 + bb;
       double c[kB];
 #pragma unroll
       for (int p = 0; p < kB; ++p) c[p] = Cb[i * kB + p];
-      double* wi = W + size_t(i) * tl;
+      const double* wi = W + size_t(i) * tl;
+      double* wn = Wn + size_t(i) * tl;
       double old[kJ];
 #pragma unroll
       for (int q = 0; q < kJ; ++q) {  // all of the row's loads in flight at once
@@ -337,11 +356,12 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
           for (int p = 0; p < kB; ++p) acc += c[p] * R2[p * tl + j];
           v = old[q] - acc;
         }
-        wi[j] = v;
+        wn[j] = v;
       }
     }
-    __syncthreads();
+    cluster.sync();  // every CTA's rows of Wn written before the next pass reads them
   }
+  if (crank != 0) return;
   // pivot guard (linalg.cpp:69-73) over every diagonal of U
   double bad = 0.0;
   const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
@@ -780,8 +800,46 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     const size_t gsm = (size_t(3) * P.tl * 16 + 16 * 16) * sizeof(double);
     cudaFuncSetAttribute(refactor_tail_gj_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(gsm));
-    refactor_tail_gj_kernel<512><<<M, 512, gsm, st>>>(P, F, FT, D, scale, status, piv_tol,
-                                                      vs_src, nnz_vs, VS);
+    // small M: a cluster of CL CTAs per scenario so the grid covers the GPU
+    static int max_cl = -1;
+    if (max_cl < 0) {
+      max_cl = 1;
+      for (int c = 8; c > 1 && max_cl == 1; c /= 2) {
+        cudaLaunchConfig_t q{};
+        cudaLaunchAttribute qa{};
+        q.gridDim = dim3(c);
+        q.blockDim = dim3(512);
+        q.dynamicSmemBytes = gsm;
+        qa.id = cudaLaunchAttributeClusterDimension;
+        qa.val.clusterDim.x = c;
+        qa.val.clusterDim.y = qa.val.clusterDim.z = 1;
+        q.attrs = &qa;
+        q.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, refactor_tail_gj_kernel<512>, &q) == cudaSuccess &&
+            n > 0)
+          max_cl = c;
+      }
+      cudaGetLastError();
+      if (const char* e = std::getenv("BIPM_GJ_CLUSTER")) max_cl = std::max(1, std::atoi(e));
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int cl = 1;
+    while (cl * 2 <= max_cl && M * cl * 2 <= sms) cl *= 2;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr{};
+    cfg.gridDim = dim3(M * cl);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = gsm;
+    cfg.stream = st;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = cl;
+    attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, refactor_tail_gj_kernel<512>, P, F, FT, D,
+                       static_cast<const double*>(scale), status, piv_tol, vs_src, nnz_vs, VS);
     note_launch();
     check_launch("refactor_tail_gj");
     refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
