@@ -459,7 +459,9 @@ bool Engine::factor_khat() {
   return info == 0;
 }
 
-void Engine::solve_khat(double* d_vec) { launch_cholesky_solve(khat.get(), pb.M.n_u, d_vec, st); }
+void Engine::solve_khat(double* d_vec) {
+  timed("khat_solve", [&] { launch_cholesky_solve(khat.get(), pb.M.n_u, d_vec, st); });
+}
 
 void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, double* d_pz,
                      double* d_ps, const double* d_rhat1, const double* d_rhat3,

@@ -369,61 +369,111 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
   }
 }
 
-// L L' x = b, blocked by 32 rows: the CTA stages each 32 x 32 diagonal block
-// in shared memory, one warp solves it by shuffles, the CTA updates the
-// remaining rows.
-__global__ void __launch_bounds__(1024) blocked_solve_kernel(const double* __restrict__ L, int n,
-                                                            double* b) {
-  extern __shared__ double x[];  // n
-  __shared__ double Dg[32][33];  // diagonal block, Dg[r][c] = L(c0 + r, c0 + c)
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = b[i];
+// L L' x = b, blocked by 32 rows.  Per block: one warp solves the 32 x 32
+// diagonal block by shuffles (rows / columns in registers, reciprocal pivots),
+// then the CTA updates the remaining rows.  Nothing the CTA loads from L
+// depends on x, so each thread issues its row's 32 loads of the coming update
+// and the next diagonal block's entries (double-buffered in shared memory)
+// before the warp solve: the L2 latency hides behind the solve and each block
+// costs a solve plus two barriers.  L is L2-resident after the factorisation.
+template <int B>
+__global__ void __launch_bounds__(B) blocked_solve_kernel(const double* __restrict__ L, int n,
+                                                         double* b) {
+  extern __shared__ double x[];     // n + 32 (zero padding for the last block)
+  __shared__ double Dg[2][32][33];  // diagonal blocks, Dg[.][r][c] = L(c0 + r, c0 + c)
+  constexpr int kDg = (1024 + B - 1) / B;  // block entries per thread
+  for (int i = threadIdx.x; i < n + 32; i += B) x[i] = i < n ? b[i] : 0.0;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  auto stage = [&](int c0, int w) {
-    __syncthreads();
-    const int r = threadIdx.x & 31, c = threadIdx.x >> 5;
-    if (c < 32) Dg[r][c] = (r < w && c < w) ? L[size_t(c0 + c) * n + c0 + r] : 0.0;
-    __syncthreads();
+  const int nb = (n + 31) / 32;
+  // entry e = (r, c) of block k: L(c0 + r, c0 + c), identity padding
+  auto dg_load = [&](int k, double (&v)[kDg]) {
+#pragma unroll
+    for (int q = 0; q < kDg; ++q) {
+      const int e = threadIdx.x + q * B, r = e & 31, c = e >> 5, c0 = 32 * k;
+      const int w = min(32, n - c0);
+      v[q] = (e < 1024 && k >= 0 && k < nb) ? ((r < w && c < w) ? L[size_t(c0 + c) * n + c0 + r]
+                                                                 : (r == c ? 1.0 : 0.0))
+                                            : 0.0;
+    }
   };
-  for (int c0 = 0; c0 < n; c0 += 32) {  // forward
-    const int w = min(32, n - c0);
-    stage(c0, w);
-    if (warp == 0) {
-      double xv = lane < w ? x[c0 + lane] : 0.0;
-      for (int j = 0; j < w; ++j) {
-        if (lane == j) xv /= Dg[j][j];
-        const double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane > j && lane < w) xv -= Dg[lane][j] * xj;
-      }
-      if (lane < w) x[c0 + lane] = xv;
+  auto dg_store = [&](int buf, const double (&v)[kDg]) {
+#pragma unroll
+    for (int q = 0; q < kDg; ++q) {
+      const int e = threadIdx.x + q * B;
+      if (e < 1024) Dg[buf][e & 31][e >> 5] = v[q];
     }
-    __syncthreads();
-    for (int i = c0 + w + threadIdx.x; i < n; i += blockDim.x) {
-      double acc = 0.0;
-      for (int j = 0; j < w; ++j) acc += L[size_t(c0 + j) * n + i] * x[c0 + j];
-      x[i] -= acc;
-    }
-  }
-  for (int c0 = ((n - 1) / 32) * 32; c0 >= 0; c0 -= 32) {  // backward with L'
-    const int w = min(32, n - c0);
-    stage(c0, w);
-    if (warp == 0) {
-      double xv = lane < w ? x[c0 + lane] : 0.0;
-      for (int j = w - 1; j >= 0; --j) {
-        if (lane == j) xv /= Dg[j][j];
-        const double xj = __shfl_sync(0xffffffffu, xv, j);
-        if (lane < j) xv -= Dg[j][lane] * xj;
-      }
-      if (lane < w) x[c0 + lane] = xv;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < c0; i += blockDim.x) {
-      double acc = 0.0;
-      for (int j = 0; j < w; ++j) acc += L[size_t(i) * n + c0 + j] * x[c0 + j];
-      x[i] -= acc;
-    }
-  }
+  };
+  double v[kDg];
+  dg_load(0, v);
+  dg_store(0, v);
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) b[i] = x[i];
+  for (int k = 0; k < nb; ++k) {  // forward: L y = b
+    const int c0 = 32 * k, w = min(32, n - c0), buf = k & 1;
+    const int i0 = c0 + w + threadIdx.x;  // first row of the update, prefetched
+    double l[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) l[j] = (i0 < n && j < w) ? L[size_t(c0 + j) * n + i0] : 0.0;
+    dg_load(k + 1, v);
+    if (warp == 0) {
+      const double* row = Dg[buf][lane];
+      const double rd = 1.0 / Dg[buf][lane][lane];
+      double xv = x[c0 + lane];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const double xj = __shfl_sync(0xffffffffu, xv * rd, j);
+        if (lane == j) xv = xj;
+        if (lane > j) xv -= row[j] * xj;
+      }
+      if (lane < w) x[c0 + lane] = xv;
+    }
+    dg_store(buf ^ 1, v);
+    __syncthreads();
+    for (int i = i0; i < n; i += B) {
+      if (i != i0)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) l[j] = j < w ? L[size_t(c0 + j) * n + i] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += l[j] * x[c0 + j];
+      x[i] -= acc;
+    }
+    __syncthreads();
+  }
+  dg_load(nb - 1, v);
+  dg_store(0, v);
+  __syncthreads();
+  for (int k = nb - 1, t = 0; k >= 0; --k, ++t) {  // backward: L' x = y
+    const int c0 = 32 * k, w = min(32, n - c0), buf = t & 1;
+    const int i0 = threadIdx.x;  // rows i < c0
+    double l[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) l[j] = (i0 < c0 && j < w) ? L[size_t(i0) * n + c0 + j] : 0.0;
+    dg_load(k - 1, v);
+    if (warp == 0) {
+      const double rd = 1.0 / Dg[buf][lane][lane];
+      double xv = x[c0 + lane];
+#pragma unroll
+      for (int j = 31; j >= 0; --j) {
+        const double xj = __shfl_sync(0xffffffffu, xv * rd, j);
+        if (lane == j) xv = xj;
+        if (lane < j) xv -= Dg[buf][j][lane] * xj;
+      }
+      if (lane < w) x[c0 + lane] = xv;
+    }
+    dg_store(buf ^ 1, v);
+    __syncthreads();
+    for (int i = i0; i < c0; i += B) {
+      if (i != i0)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) l[j] = j < w ? L[size_t(i) * n + c0 + j] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) acc += l[j] * x[c0 + j];
+      x[i] -= acc;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += B) b[i] = x[i];
 }
 
 }  // namespace
@@ -471,10 +521,12 @@ void launch_blocked_cholesky(double* K, int n, int* info, cudaStream_t st) {
 }
 
 void launch_blocked_solve(const double* L, int n, double* b, cudaStream_t st) {
-  const size_t smem = size_t(n) * sizeof(double);
-  cudaFuncSetAttribute(blocked_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = size_t(n + 32) * sizeof(double);
+  // 640 threads: one prefetched update row per thread up to n = 640 (more
+  // rows are loaded after the barrier), <= 102 registers so l[32] stays in them
+  cudaFuncSetAttribute(blocked_solve_kernel<640>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(smem));
-  blocked_solve_kernel<<<1, 1024, smem, st>>>(L, n, b);
+  blocked_solve_kernel<640><<<1, 640, smem, st>>>(L, n, b);
   note_launch();
   check("blocked_solve");
 }

@@ -25,7 +25,7 @@ t3 = time.time()
 r = s.solve()
 t4 = time.time()
 groups = ["ad_bundle", "ad_values", "condense", "lu_refactor", "reduce_tiles", "reduce_rhs",
-          "cholesky", "recover_state"]
+          "cholesky", "khat_solve", "recover_state"]
 kt = {g: ctx.kernel_time(g) for g in groups}
 it = r["iterations"]
 out = {"case": case, "N": N, "n_x": p.n_x, "n_u": p.n_u, "m": p.m, "status": r["status_name"],
