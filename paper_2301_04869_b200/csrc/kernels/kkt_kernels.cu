@@ -226,17 +226,38 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F
 }
 
 // Large tails (2 tl^2 doubles beyond shared memory): blocked Gauss-Jordan
+__device__ __forceinline__ void gj_dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// shared-memory strides of the Gauss-Jordan tail kernel (doubles): 16-wide
+// blocks padded to 20 and tl-wide rows to 16k + 4 so the m8n8k4 fragment
+// loads (8 rows x 4 columns / 4 rows x 8 columns) hit distinct banks
+constexpr int kGjB = 16, kGjLdb = 20;
+inline __host__ __device__ int gj_tp(int tl) { return (tl + 7) & ~7; }
+inline __host__ __device__ int gj_ldr(int tl) { return ((gj_tp(tl) + 15) & ~15) + 4; }
+inline size_t gj_smem_bytes(int tl) {
+  return (size_t(gj_tp(tl)) * kGjLdb + size_t(2) * kGjB * gj_ldr(tl) + kGjB * kGjLdb) *
+         sizeof(double);
+}
+
 // inversion of the tail block S = L_TT U_TT into D's W slot (row-major,
 // global memory, L2-resident), static pivots, 16 pivots per pass so the block
-// is streamed tl/16 times instead of tl times; W = S^{-1}.  Passes ping-pong
-// between D's two tt slots (the W' slot is scratch until the layouts kernel)
-// and end in the W slot.  A thread-block cluster of CL CTAs may share one
-// scenario (small M: the GPU would otherwise idle): every CTA forms the 16x16
-// pivot inverse redundantly and updates the rows r = rank (mod CL), one
-// cluster barrier per pass.  The pivots of the elimination are U_TT's
-// diagonal: they go to the factor's diagonal slots for the guard.  The tail
-// block's L/U values are never read by the sweeps (the tail is applied
-// through W), so F keeps S there.
+// is streamed tl/16 times instead of tl times; W = S^{-1}.  A pass is one
+// rank-16 update W <- W' - C' R2 on the FP64 tensor pipe (m8n8k4 DMMA) with
+// the Gauss-Jordan bookkeeping folded into the operands: C' = W[:, P] with
+// the pivot rows replaced by -e_p, R2 = A11^{-1} W[P, :] with the pivot
+// columns replaced by A11^{-1}, and W' = W with the pivot rows and columns
+// zeroed.  Passes ping-pong between D's two tt slots (the W' slot is scratch
+// until the layouts kernel) and end in the W slot.  A thread-block cluster of
+// CL CTAs may share one scenario (small M: the GPU would otherwise idle):
+// every CTA forms the 16x16 pivot inverse redundantly and updates its share
+// of the 8 x 64 output strips, one cluster barrier per pass.  The pivots of
+// the elimination are U_TT's diagonal: they go to the factor's diagonal slots
+// for the guard.  The tail block's L/U values are never read by the sweeps
+// (the tail is applied through W), so F keeps S there.
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double* F, double* FT,
                                                                  double* D,
@@ -244,25 +265,26 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
                                                                  int* status, double piv_tol,
                                                                  const int* vs_src, int nnz_vs,
                                                                  double* VS) {
-  constexpr int kB = 16;
+  constexpr int kB = kGjB, kLb = kGjLdb;
   extern __shared__ double gj[];
   cg::cluster_group cluster = cg::this_cluster();
   const int ncl = int(cluster.num_blocks()), crank = int(cluster.block_rank());
   const int s = blockIdx.x / ncl;
   double* Fs = F + size_t(s) * P.nnz_f;
   const int tl = P.tl, tt = tl * tl, t0 = P.t0;
-  double* Cb = gj;                      // [tl][kB]   W[:, P]
-  double* Rb = Cb + size_t(tl) * kB;    // [kB][tl]   W[P, :]
-  double* R2 = Rb + size_t(tl) * kB;    // [kB][tl]   A11^{-1} W[P, :]
-  double* Ai = R2 + size_t(tl) * kB;    // [kB][kB]   A11^{-1}
+  const int tp = gj_tp(tl), ldr = gj_ldr(tl), ntp = tp / 8;
+  double* Cb = gj;                          // [tp][kLb]  C' = W[:, P], pivot rows -e_p
+  double* Rb = Cb + size_t(tp) * kLb;       // [kB][ldr]  W[P, :]
+  double* R2 = Rb + size_t(kB) * ldr;       // [kB][ldr]  A11^{-1} W[P, :], pivot cols A11^{-1}
+  double* Ai = R2 + size_t(kB) * ldr;       // [kB][kLb]  A11^{-1}
   const int npass = (tl + kB - 1) / kB;
   double* const Wbase = D + size_t(s) * 2 * tt;  // slot b at Wbase + b tt
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gm = lane >> 2, gk = lane & 3;
   constexpr int kWarps = BLOCK / 32;
-  const int row0 = crank * kWarps + warp, rstep = kWarps * ncl;
   {
     double* W = Wbase + (npass & 1) * tt;
-    for (int i = row0; i < tl; i += rstep)
+    for (int i = crank * kWarps + warp; i < tl; i += kWarps * ncl)
       for (int j = lane; j < tl; j += 32) {
         const int src = i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
         W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
@@ -273,11 +295,18 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     const int bb = min(kB, tl - k0);
     const double* W = Wbase + ((npass - pass) & 1) * tt;
     double* Wn = Wbase + ((npass - pass - 1) & 1) * tt;
-    for (int q = threadIdx.x; q < tl * kB; q += BLOCK) {
+    for (int q = threadIdx.x; q < tp * kB; q += BLOCK) {
       const int i = q / kB, p = q % kB;
-      Cb[q] = p < bb ? W[size_t(i) * tl + k0 + p] : 0.0;
-      const int pr = q / tl, j = q % tl;
-      Rb[q] = pr < bb ? W[size_t(k0 + pr) * tl + j] : 0.0;
+      double v = 0.0;
+      if (i >= k0 && i < k0 + bb)
+        v = p == i - k0 ? -1.0 : 0.0;
+      else if (i < tl && p < bb)
+        v = W[size_t(i) * tl + k0 + p];
+      Cb[i * kLb + p] = v;
+    }
+    for (int q = threadIdx.x; q < kB * tp; q += BLOCK) {
+      const int pr = q / tp, j = q % tp;
+      Rb[pr * ldr + j] = (pr < bb && j < tl) ? W[size_t(k0 + pr) * tl + j] : 0.0;
     }
     __syncthreads();
     // A11^{-1} by Gauss-Jordan in one warp (lane = column), pivots to the factor
@@ -287,7 +316,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       double col[kB];  // lane's column of the working matrix
 #pragma unroll
       for (int r = 0; r < kB; ++r)
-        col[r] = (lane < bb && r < bb) ? Rb[r * tl + k0 + lane] : (r == lane ? 1.0 : 0.0);
+        col[r] = (lane < bb && r < bb) ? Rb[r * ldr + k0 + lane] : (r == lane ? 1.0 : 0.0);
       double inv[kB];  // lane's column of the identity being transformed
 #pragma unroll
       for (int r = 0; r < kB; ++r) inv[r] = (r == lane) ? 1.0 : 0.0;
@@ -309,57 +338,55 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       }
       if (lane < kB)
 #pragma unroll
-        for (int r = 0; r < kB; ++r) Ai[r * kB + lane] = inv[r];
+        for (int r = 0; r < kB; ++r) Ai[r * kLb + lane] = inv[r];
     }
     __syncthreads();
-    // R2 = A11^{-1} W[P, :]
-    for (int q = threadIdx.x; q < kB * tl; q += BLOCK) {
-      const int r = q / tl, j = q % tl;
-      double acc = 0.0;
+    // R2 = A11^{-1} W[P, :] (2 x ntp fragments), pivot columns A11^{-1}
+    for (int t = warp; t < 2 * ntp; t += kWarps) {
+      const int I = t & 1, J = t >> 1;
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-      for (int p = 0; p < kB; ++p) acc += Ai[r * kB + p] * Rb[p * tl + j];
-      R2[q] = acc;
+      for (int kk = 0; kk < kB; kk += 4)
+        gj_dmma(d0, d1, Ai[(I * 8 + gm) * kLb + kk + gk], Rb[(kk + gk) * ldr + J * 8 + gm]);
+      const int r = I * 8 + gm, c = J * 8 + 2 * gk;
+      R2[r * ldr + c] = (c >= k0 && c < k0 + bb) ? Ai[r * kLb + c - k0] : d0;
+      R2[r * ldr + c + 1] = (c + 1 >= k0 && c + 1 < k0 + bb) ? Ai[r * kLb + c + 1 - k0] : d1;
     }
     __syncthreads();
-    // rank-bb update of this CTA's rows; the pivot rows / columns take the
-    // Gauss-Jordan values
-    constexpr int kJ = 10;  // tl <= 320: the lane's columns of a row in registers
-    for (int i = row0; i < tl; i += rstep) {
-      const bool ip = i >= k0 && i < k0 + bb;
-      double c[kB];
+    // W_next = W' - C' R2 over this CTA's 8 x 64 strips
+    const int nch = (ntp + 7) / 8;
+    for (int it = crank * kWarps + warp; it < ntp * nch; it += kWarps * ncl) {
+      const int I = it / nch, ch = it % nch;
+      const int r = I * 8 + gm;
+      const bool rp = r >= k0 && r < k0 + bb;
+      double af[4];
 #pragma unroll
-      for (int p = 0; p < kB; ++p) c[p] = Cb[i * kB + p];
-      const double* wi = W + size_t(i) * tl;
-      double* wn = Wn + size_t(i) * tl;
-      double old[kJ];
+      for (int kk = 0; kk < 4; ++kk) af[kk] = Cb[r * kLb + 4 * kk + gk];
+      double old[8][2];
 #pragma unroll
-      for (int q = 0; q < kJ; ++q) {  // all of the row's loads in flight at once
-        const int j = lane + 32 * q;
-        old[q] = j < tl ? wi[j] : 0.0;
-      }
+      for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
-      for (int q = 0; q < kJ; ++q) {
-        const int j = lane + 32 * q;
-        if (j >= tl) break;
-        const bool jp = j >= k0 && j < k0 + bb;
-        double v;
-        if (ip) {
-          v = jp ? Ai[(i - k0) * kB + (j - k0)] : R2[(i - k0) * tl + j];
-        } else if (jp) {
-          double acc = 0.0;
-#pragma unroll
-          for (int p = 0; p < kB; ++p) acc += c[p] * Ai[p * kB + (j - k0)];
-          v = -acc;
-        } else {
-          double acc = 0.0;
-#pragma unroll
-          for (int p = 0; p < kB; ++p) acc += c[p] * R2[p * tl + j];
-          v = old[q] - acc;
+        for (int v = 0; v < 2; ++v) {
+          const int c = (ch * 8 + jj) * 8 + 2 * gk + v;
+          const bool cp = c >= k0 && c < k0 + bb;
+          old[jj][v] = (r < tl && c < tl && !rp && !cp) ? W[size_t(r) * tl + c] : 0.0;
         }
-        wn[j] = v;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        const int J = ch * 8 + jj;
+        if (J >= ntp) break;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          gj_dmma(d0, d1, af[kk], R2[(4 * kk + gk) * ldr + J * 8 + gm]);
+        const int c = J * 8 + 2 * gk;
+        if (r < tl) {
+          if (c < tl) Wn[size_t(r) * tl + c] = old[jj][0] - d0;
+          if (c + 1 < tl) Wn[size_t(r) * tl + c + 1] = old[jj][1] - d1;
+        }
       }
     }
-    cluster.sync();  // every CTA's rows of Wn written before the next pass reads them
+    cluster.sync();  // every CTA's strips of Wn written before the next pass reads them
   }
   if (crank != 0) return;
   // pivot guard (linalg.cpp:69-73) over every diagonal of U
@@ -797,7 +824,7 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status,
                                                               piv_tol, vs_src, nnz_vs, VS);
   } else {
-    const size_t gsm = (size_t(3) * P.tl * 16 + 16 * 16) * sizeof(double);
+    const size_t gsm = gj_smem_bytes(P.tl);
     cudaFuncSetAttribute(refactor_tail_gj_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(gsm));
     // small M: a cluster of CL CTAs per scenario so the grid covers the GPU
