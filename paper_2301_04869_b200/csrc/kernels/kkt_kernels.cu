@@ -269,6 +269,13 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   extern __shared__ double gj[];
   cg::cluster_group cluster = cg::this_cluster();
   const int ncl = int(cluster.num_blocks()), crank = int(cluster.block_rank());
+  // a lone CTA needs no cluster barrier (and its fence)
+  auto sync_all = [&] {
+    if (ncl > 1)
+      cluster.sync();
+    else
+      __syncthreads();
+  };
   const int s = blockIdx.x / ncl;
   double* Fs = F + size_t(s) * P.nnz_f;
   const int tl = P.tl, tt = tl * tl, t0 = P.t0;
@@ -282,31 +289,60 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gm = lane >> 2, gk = lane & 3;
   constexpr int kWarps = BLOCK / 32;
+  constexpr int kJ = 10;  // tl <= 320: a row's columns over the lanes
   {
+    // S from the factor: every load of a row in flight at once
     double* W = Wbase + (npass & 1) * tt;
-    for (int i = crank * kWarps + warp; i < tl; i += kWarps * ncl)
-      for (int j = lane; j < tl; j += 32) {
-        const int src = i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
-        W[i * tl + j] = src >= 0 ? Fs[src] : 0.0;
+    for (int i = crank * kWarps + warp; i < tl; i += kWarps * ncl) {
+      int src[kJ];
+#pragma unroll
+      for (int q = 0; q < kJ; ++q) {
+        const int j = lane + 32 * q;
+        src[q] = j >= tl ? -1 : i > j ? P.dense_src[j * tl + i] : P.dense_src[tt + j * tl + i];
       }
+      double v[kJ];
+#pragma unroll
+      for (int q = 0; q < kJ; ++q) v[q] = src[q] >= 0 ? Fs[src[q]] : 0.0;
+#pragma unroll
+      for (int q = 0; q < kJ; ++q)
+        if (lane + 32 * q < tl) W[i * tl + lane + 32 * q] = v[q];
+    }
   }
-  cluster.sync();
+  sync_all();
   for (int k0 = 0, pass = 0; k0 < tl; k0 += kB, ++pass) {
     const int bb = min(kB, tl - k0);
     const double* W = Wbase + ((npass - pass) & 1) * tt;
     double* Wn = Wbase + ((npass - pass - 1) & 1) * tt;
-    for (int q = threadIdx.x; q < tp * kB; q += BLOCK) {
-      const int i = q / kB, p = q % kB;
-      double v = 0.0;
-      if (i >= k0 && i < k0 + bb)
-        v = p == i - k0 ? -1.0 : 0.0;
-      else if (i < tl && p < bb)
-        v = W[size_t(i) * tl + k0 + p];
-      Cb[i * kLb + p] = v;
-    }
-    for (int q = threadIdx.x; q < kB * tp; q += BLOCK) {
-      const int pr = q / tp, j = q % tp;
-      Rb[pr * ldr + j] = (pr < bb && j < tl) ? W[size_t(k0 + pr) * tl + j] : 0.0;
+    {
+      // C' and W[P, :]: all of a thread's loads in flight, then the stores
+      constexpr int kQ = (320 * kB + BLOCK - 1) / BLOCK;
+      double v[kQ];
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) {
+        const int q = threadIdx.x + u * BLOCK;
+        const int i = q / kB, p = q % kB;
+        v[u] = 0.0;
+        if (i >= k0 && i < k0 + bb)
+          v[u] = p == i - k0 ? -1.0 : 0.0;
+        else if (i < tl && p < bb)
+          v[u] = W[size_t(i) * tl + k0 + p];
+      }
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) {
+        const int q = threadIdx.x + u * BLOCK;
+        if (q < tp * kB) Cb[(q / kB) * kLb + q % kB] = v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) {
+        const int q = threadIdx.x + u * BLOCK;
+        const int pr = q / tp, j = q % tp;
+        v[u] = (pr < bb && j < tl) ? W[size_t(k0 + pr) * tl + j] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kQ; ++u) {
+        const int q = threadIdx.x + u * BLOCK;
+        if (q < tp * kB) Rb[(q / tp) * ldr + q % tp] = v[u];
+      }
     }
     __syncthreads();
     // A11^{-1} by Gauss-Jordan in one warp (lane = column), pivots to the factor
@@ -353,40 +389,80 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       R2[r * ldr + c + 1] = (c + 1 >= k0 && c + 1 < k0 + bb) ? Ai[r * kLb + c + 1 - k0] : d1;
     }
     __syncthreads();
-    // W_next = W' - C' R2 over this CTA's 8 x 64 strips
-    const int nch = (ntp + 7) / 8;
-    for (int it = crank * kWarps + warp; it < ntp * nch; it += kWarps * ncl) {
+    // W_next = W' - C' R2 over this CTA's 8 x 32 strips; the next strip's
+    // loads are issued before this strip's DMMAs.  Strips clear of the pivot
+    // rows / columns and of the ragged edge (most of them) take a path
+    // without per-element predicates.
+    constexpr int kSJ = 4;  // 8-column tiles per strip
+    const int nch = (ntp + kSJ - 1) / kSJ, nit = ntp * nch;
+    auto clean = [&](int it) {
+      const int r0 = (it / nch) * 8, c0s = (it % nch) * 8 * kSJ;
+      return it < nit && r0 + 8 <= tl && c0s + 8 * kSJ <= tl &&
+             (r0 + 8 <= k0 || r0 >= k0 + bb) && (c0s + 8 * kSJ <= k0 || c0s >= k0 + bb);
+    };
+    auto load_strip = [&](int it, double (&o)[kSJ][2]) {
       const int I = it / nch, ch = it % nch;
       const int r = I * 8 + gm;
+      if (clean(it)) {
+        const double* wr = W + size_t(r) * tl + ch * 8 * kSJ + 2 * gk;
+#pragma unroll
+        for (int jj = 0; jj < kSJ; ++jj) {
+          o[jj][0] = wr[8 * jj];
+          o[jj][1] = wr[8 * jj + 1];
+        }
+        return;
+      }
       const bool rp = r >= k0 && r < k0 + bb;
+#pragma unroll
+      for (int jj = 0; jj < kSJ; ++jj)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int c = (ch * kSJ + jj) * 8 + 2 * gk + v;
+          const bool cp = c >= k0 && c < k0 + bb;
+          o[jj][v] = (it < nit && r < tl && c < tl && !rp && !cp) ? W[size_t(r) * tl + c] : 0.0;
+        }
+    };
+    const int it0 = crank * kWarps + warp, its = kWarps * ncl;
+    double old[kSJ][2];
+    load_strip(it0, old);
+    for (int it = it0; it < nit; it += its) {
+      double nxt[kSJ][2];
+      load_strip(it + its, nxt);
+      const int I = it / nch, ch = it % nch;
+      const int r = I * 8 + gm;
       double af[4];
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) af[kk] = Cb[r * kLb + 4 * kk + gk];
-      double old[8][2];
+      const double* r2 = R2 + gk * ldr + ch * 8 * kSJ + gm;
+      double d[kSJ][2];
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
+      for (int jj = 0; jj < kSJ; ++jj) {
+        d[jj][0] = d[jj][1] = 0.0;
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int c = (ch * 8 + jj) * 8 + 2 * gk + v;
-          const bool cp = c >= k0 && c < k0 + bb;
-          old[jj][v] = (r < tl && c < tl && !rp && !cp) ? W[size_t(r) * tl + c] : 0.0;
+        for (int kk = 0; kk < 4; ++kk) gj_dmma(d[jj][0], d[jj][1], af[kk], r2[4 * kk * ldr + 8 * jj]);
+      }
+      if (clean(it)) {
+        double* wn = Wn + size_t(r) * tl + ch * 8 * kSJ + 2 * gk;
+#pragma unroll
+        for (int jj = 0; jj < kSJ; ++jj) {
+          wn[8 * jj] = old[jj][0] - d[jj][0];
+          wn[8 * jj + 1] = old[jj][1] - d[jj][1];
         }
+      } else if (r < tl) {
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
-        const int J = ch * 8 + jj;
-        if (J >= ntp) break;
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          gj_dmma(d0, d1, af[kk], R2[(4 * kk + gk) * ldr + J * 8 + gm]);
-        const int c = J * 8 + 2 * gk;
-        if (r < tl) {
-          if (c < tl) Wn[size_t(r) * tl + c] = old[jj][0] - d0;
-          if (c + 1 < tl) Wn[size_t(r) * tl + c + 1] = old[jj][1] - d1;
+        for (int jj = 0; jj < kSJ; ++jj) {
+          const int c = (ch * kSJ + jj) * 8 + 2 * gk;
+          if (c < tl) Wn[size_t(r) * tl + c] = old[jj][0] - d[jj][0];
+          if (c + 1 < tl) Wn[size_t(r) * tl + c + 1] = old[jj][1] - d[jj][1];
         }
       }
+#pragma unroll
+      for (int jj = 0; jj < kSJ; ++jj) {
+        old[jj][0] = nxt[jj][0];
+        old[jj][1] = nxt[jj][1];
+      }
     }
-    cluster.sync();  // every CTA's strips of Wn written before the next pass reads them
+    sync_all();  // every CTA's strips of Wn written before the next pass reads them
   }
   if (crank != 0) return;
   // pivot guard (linalg.cpp:69-73) over every diagonal of U
