@@ -184,3 +184,32 @@ def test_split_refactor_program_factors_the_pattern(case):
             U[i, u_col[t]] = F[u_slot[t]]
     PA = A[np.ix_(perm, perm)]
     assert np.abs(L @ U - PA).max() <= 1e-10 * np.abs(PA).max()
+
+
+def _gj_folded_inverse(S, kB=16):
+    """numpy restatement of refactor_tail_gj_kernel's pass (kkt_kernels.cu):
+    each block of kB pivots is one rank-kB update W <- W' - C' R2 with
+    C' = W[:, P] (pivot rows -e_p), R2 = A11^{-1} W[P, :] (pivot columns
+    A11^{-1}) and W' = W with the pivot rows and columns zeroed."""
+    W = S.astype(np.float64).copy()
+    n = W.shape[0]
+    for k0 in range(0, n, kB):
+        P = np.arange(k0, min(n, k0 + kB))
+        Ai = np.linalg.inv(W[np.ix_(P, P)])
+        C = W[:, P].copy()
+        C[P, :] = -np.eye(len(P))
+        R2 = Ai @ W[P, :]
+        R2[:, P] = Ai
+        Wp = W.copy()
+        Wp[P, :] = 0.0
+        Wp[:, P] = 0.0
+        W = Wp - C @ R2
+    return W
+
+
+@pytest.mark.parametrize("n", [5, 16, 37, 233])
+def test_gauss_jordan_folded_update_inverts(n):
+    rng = np.random.default_rng(n)
+    S = rng.standard_normal((n, n)) + n * np.eye(n)  # static pivots stay nonzero
+    W = _gj_folded_inverse(S)
+    assert np.allclose(W @ S, np.eye(n), atol=1e-10)
