@@ -286,6 +286,7 @@ void Engine::setup_stream() {
   }
   const size_t Ms = size_t(M);
   VS.resize(Ms * size_t(sprog.nnz_vs) + 2);
+  Dp.resize(std::max<size_t>(1, Ms * size_t(sprog.stride[kArrDense])));
   kxu_t.resize(Ms * nnz(D.kxu.out) + 2);
   gu_t.resize(Ms * nnz(D.g.u) + 2);
 
@@ -329,7 +330,8 @@ void Engine::factor_gx_launch() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
-                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr, st);
+                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
+                       use_stream ? Dp.get() : nullptr, st);
   });
 }
 
@@ -337,7 +339,8 @@ idx Engine::factor_gx() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
-                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr, st);
+                       int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
+                       use_stream ? Dp.get() : nullptr, st);
   });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
@@ -375,7 +378,7 @@ void Engine::reduce_local(double dw) {
       launch_kuu_sum(kuu.get(), nnz(D.kuu.out), kuu_row.get(), kuu_col.get(),
                      int(nnz(D.kuu.out)), M, n_u, kuu_part, st);
       sl.arr[kArrSweep] = VS.get();
-      sl.arr[kArrDense] = Dt.get();
+      sl.arr[kArrDense] = Dp.get();
       sl.arr[kArrKxx] = kxx.get();
       sl.arr[kArrKxuT] = kxu_t.get();
       sl.arr[kArrGuT] = gu_t.get();

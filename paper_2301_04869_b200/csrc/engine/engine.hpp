@@ -100,7 +100,7 @@ class Engine {
   StreamProgram sprog;
   StreamLaunch sl{};
   DArr<int> sp_pat, sp_issue, sp_ring, sp_vs_src, sp_kxu_slot, sp_gu_slot, kuu_row, kuu_col;
-  DArr<double> VS, kxu_t, gu_t, sp_scratch;
+  DArr<double> VS, Dp, kxu_t, gu_t, sp_scratch;  // Dp: W, W' with padded rows
   int red_parts = 0;  // partial K_hat slabs summed by finish_reduce
   // ---- reduction workspace (tile kernel, BIPM_REDUCE=tiles)
   ReduceLaunch red{};

@@ -221,7 +221,7 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   }();
   S.max_step_bytes = std::max(4096, std::min(int(ring_bytes / step_div) & ~15, 64 * 1024));
   const idx n = L.n, t0 = L.t0, tl = L.tl;
-  S.stride[kArrDense] = 2LL * tl * tl;
+  S.stride[kArrDense] = 2LL * tl * dense_ld(tl);
   S.stride[kArrKxx] = kxx.nnz();
   S.stride[kArrKxuT] = kxu.nnz();
   S.stride[kArrGuT] = gu.nnz();

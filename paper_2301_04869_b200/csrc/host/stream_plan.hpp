@@ -53,10 +53,14 @@ inline int panel_swizzle(int r, int K) {
 }
 inline int panel_word(int r, int K) { return r * K * 8 + 16 * panel_swizzle(r, K); }
 
+// row stride of the reduction's padded copy of W, W' (kArrDense): rows start
+// on 128-byte lines so the dense step loads 32-byte vectors, 4 lanes per line
+inline int dense_ld(int tl) { return (tl + 15) & ~15; }
+
 // value arrays a step can read ([M][stride] scenario-major on the device)
 enum ValArray : int {
   kArrSweep = 0,  // sweep-ordered factor values (VS), written by the refactor
-  kArrDense = 1,  // W, W' dense tail inverses
+  kArrDense = 1,  // W, W' dense tail inverses, rows padded to dense_ld(tl)
   kArrKxx = 2,    // condensed K_xx (CSR slot order)
   kArrKxuT = 3,   // K_xu values in column (control) order
   kArrGuT = 4,    // G_u values in column (control) order

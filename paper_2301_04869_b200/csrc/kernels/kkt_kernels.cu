@@ -505,6 +505,17 @@ __global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, d
   }
 }
 
+// W, W' (row-major tl x tl, two per scenario) -> rows padded to ldw doubles
+__global__ void pad_dense_kernel(const double* __restrict__ D, double* __restrict__ Dp, int tl,
+                                 int ldw, long long n) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long row = q / ldw;  // over [M][2][tl]
+    const int j = int(q % ldw);
+    Dp[q] = j < tl ? D[row * tl + j] : 0.0;
+  }
+}
+
 // ----------------------------------------------------------- Schur reduction
 __device__ __forceinline__ FactorView factor_of(const DevLu& P, const double* F, const double* FT,
                                                 const double* D, int s) {
@@ -881,7 +892,7 @@ size_t single_rhs_smem(int n_x) {
 
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, cudaStream_t st) {
+                        int nnz_vs, double* VS, double* Dp, cudaStream_t st) {
   if (M <= 0) return;
   static double* scale = nullptr;
   static int scale_n = 0;
@@ -950,6 +961,14 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
   }
   note_launch();
   check_launch("refactor_tail");
+  if (Dp && P.tl > 0) {
+    const int ldw = (P.tl + 15) & ~15;
+    const long long n = (long long)M * 2 * P.tl * ldw;
+    pad_dense_kernel<<<int(std::min<long long>((n + 255) / 256, 8 * 148)), 256, 0, st>>>(
+        D, Dp, P.tl, ldw, n);
+    note_launch();
+    check_launch("pad_dense");
+  }
 }
 
 void plan_reduce_launch(ReduceLaunch& a, int smem_budget, int sm_count) {

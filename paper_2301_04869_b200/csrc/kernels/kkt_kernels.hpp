@@ -16,9 +16,11 @@ namespace bipm {
 // D [M][4 tl tl] used by the solve kernels.
 // VS (optional, [M][nnz_vs]): VS[s][q] = F[s][vs_src[q]] (0 where -1), the
 // sweep-ordered factor values of the streamed reduction (reduce_stream.cu).
+// Dp (optional, [M][2 tl dense_ld(tl)]): W, W' with rows padded to
+// (tl + 15) & ~15 doubles, zero-filled, for the streamed reduction's dense step.
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, cudaStream_t st);
+                        int nnz_vs, double* VS, double* Dp, cudaStream_t st);
 
 struct ReduceLaunch {
   DevLu lu;

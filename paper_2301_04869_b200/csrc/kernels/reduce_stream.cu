@@ -340,30 +340,52 @@ __device__ __forceinline__ void step_dense_global(const double* __restrict__ W, 
   constexpr int NT = K >= 8 ? K / 8 : 1;  // 8-column tiles
   const int lane = tid & 31, warp = tid >> 5;
   const int gm = lane >> 2, gk = lane & 3;
+  const int ldw = (tl + 15) & ~15;  // host/stream_plan.hpp dense_ld
   const int mtiles = (tl + 7) >> 3;
   for (int mt = warp; mt < mtiles; mt += C / 32) {
     const int i = mt * 8 + gm;
-    const double* __restrict__ wr = W + size_t(i < tl ? i : 0) * tl;
+    // lane (gm, gk) reads W(i, k0 + 4 gk .. +3) as one 32-byte vector: the 4
+    // lanes of a row cover one 128-byte line, and DMMA step j of the chunk
+    // takes k = k0 + 4 gk + j (any k order works when A and B agree)
+    const double* __restrict__ wr = W + size_t(i < tl ? i : 0) * ldw + 4 * gk;
     double acc[NT][2];
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
-    for (int k0 = 0; k0 < tl; k0 += 32) {
-      double af[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0 + 4 * u + gk;
-        af[u] = (i < tl && k < tl) ? __ldg(wr + k) : 0.0;
+    auto ld = [&](int k0, double (&r)[4]) {
+      if (k0 < tl) {
+        asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                     : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+                     : "l"(wr + k0));
+      } else {
+        r[0] = r[1] = r[2] = r[3] = 0.0;
       }
+    };
+    auto chunk = [&](int k0, const double (&r)[4]) {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0 + 4 * u + gk;
+      for (int j = 0; j < 4; ++j) {
+        const int k = k0 + 4 * gk + j;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
           const int c = n * 8 + gm;
           const double bf = (k < tl && c < K) ? lds1(xb + Pn::elem(t0 + k, c)) : 0.0;
-          dmma884(acc[n][0], acc[n][1], af[u], bf);
+          dmma884(acc[n][0], acc[n][1], r[j], bf);
         }
       }
+    };
+    // three 16-column chunks in flight (W comes from L2)
+    double r0[4], r1[4], r2[4];
+    ld(0, r0);
+    ld(16, r1);
+    ld(32, r2);
+    for (int k0 = 0; k0 < tl; k0 += 48) {
+      chunk(k0, r0);
+      ld(k0 + 48, r0);
+      if (k0 + 16 >= tl) break;
+      chunk(k0 + 16, r1);
+      ld(k0 + 64, r1);
+      if (k0 + 32 >= tl) break;
+      chunk(k0 + 32, r2);
+      ld(k0 + 80, r2);
     }
     if (i < tl) {
 #pragma unroll
@@ -600,7 +622,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
         break;
       case kDenseG: {
         const double* W = a.arr[kArrDenseDev] + size_t(s) * a.stride[kArrDenseDev] +
-                          size_t(h.aux0) * a.tl * a.tl;
+                          size_t(h.aux0) * a.tl * ((a.tl + 15) & ~15);
         step_dense_global<K, C>(W, xb, temp, a.t0, a.tl, tid);
         consumer_sync<C>();
         for (int e = tid; e < a.tl * K; e += C) sts1(xb + Pn::elem(a.t0 + e / K, e % K), temp[e]);
