@@ -69,13 +69,19 @@ __device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane, do
     const double ajj = __shfl_sync(0xffffffffu, a[j], j);
     const bool bad = !(ajj > 0.0) || isnan(ajj);
     fail = (fail == 0 && bad) ? j + 1 : fail;
-    const double d = sqrt(bad ? 1.0 : ajj);
-    const double rd = 1.0 / d;
+    // rsqrt (MUFU seed + Newton, ~1 ulp) instead of the IEEE sqrt and
+    // division subroutines: they were ~2/3 of the serial per-column chain
+    const double rd = rsqrt(bad ? 1.0 : ajj);
+    const double d = (bad ? 1.0 : ajj) * rd;
     a[j] = lane == j ? d : (lane > j ? a[j] * rd : a[j]);  // L(r, j)
     colbuf[lane] = a[j];
     __syncwarp();
+    // fixed trip count so both loops unroll completely and a[] stays in
+    // registers (a j-dependent bound was unrolled by 8 only: a[] went to
+    // local memory, ~900 cycles per column)
 #pragma unroll
-    for (int k = j + 1; k < kNb; ++k) a[k] = lane >= k ? a[k] - a[j] * colbuf[k] : a[k];
+    for (int k = 0; k < kNb; ++k)
+      if (k > j) a[k] = lane >= k ? a[k] - a[j] * colbuf[k] : a[k];
     __syncwarp();
   }
   return fail;
@@ -280,7 +286,8 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
           for (int j = 0; j < kNb; ++j) {
             x[j] *= rdiag[j];
 #pragma unroll
-            for (int k = j + 1; k < kNb; ++k) x[k] -= L[k][j] * x[j];
+            for (int k = 0; k < kNb; ++k)  // fixed trip count: full unroll, x in registers
+              if (k > j) x[k] -= L[k][j] * x[j];
           }
 #pragma unroll
           for (int j = 0; j < kNb; ++j)
