@@ -181,6 +181,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   FT.resize(Ms * size_t(L.nnz_f));
   Dt.resize(std::max<size_t>(1, Ms * 2 * size_t(L.tl) * size_t(L.tl)) + 2);
   lu_status.resize(Ms);
+  lu_scale.resize(Ms);
+  if (!single_rhs_smem(int(Mo.n_x))) rhs_scratch.resize(Ms * 2 * size_t(Mo.n_x));
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));
   rhs_part.resize(Ms * size_t(Mo.n_u));
@@ -331,7 +333,7 @@ void Engine::factor_gx_launch() {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, st);
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st);
   });
 }
 
@@ -340,7 +342,7 @@ idx Engine::factor_gx() {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, st);
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st);
   });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
@@ -435,6 +437,7 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   a.rhat3 = d_rhat3 ? d_rhat3 : rhat3.get();
   a.dw = dw;
   a.part = rhs_part.get();
+  a.scratch = rhs_scratch.size() ? rhs_scratch.get() : nullptr;
   timed("reduce_rhs", [&] { launch_reduce_rhs(a, st); });
   launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st);
   if (multi()) comm->allreduce(d_out, size_t(pb.M.n_u), RedOpKind::kSum, st);
@@ -490,6 +493,7 @@ void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, 
   a.dw = dw;
   a.px = d_px;
   a.py = d_py;
+  a.scratch = rhs_scratch.size() ? rhs_scratch.get() : nullptr;
   timed("recover_state", [&] { launch_recover_state(a, st); });
   launch_recover_slack(hx_p.v, hu_p.v, pb.M.m, pb.M.n_x, M, bd().hx.get(), bd().hu.get(), d_px, d_pu,
                        sigma_s.get(), d_r2 ? d_r2 : r2.get(), d_r4 ? d_r4 : r4.get(), d_pz, d_ps, st);

@@ -93,6 +93,7 @@ class Engine {
   DArr<double> sigma_x, sigma_s, rhat1, rhat3, r2, r4;
   DArr<double> sigma_u, rhat2;                 // n_u (replicated)
   DArr<double> F, FT, Dt;                      // LU factors [M][nnz_f], transposed, dense tails
+  DArr<double> lu_scale, rhs_scratch;         // refactor guard scale [M]; single-RHS [M][2 n_x]
   DArr<int> lu_status;
   // ---- streamed reduction (reduce_stream.cu): step program, sweep-ordered
   // factor values, column-order K_xu / G_u copies

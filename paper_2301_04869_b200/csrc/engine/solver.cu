@@ -262,7 +262,7 @@ bool Solver::attempt(double dw, const DevIter& it) {
       allred(dd_u.get(), 2 * size_t(d.n_u), RedOpKind::kSum);
       launch_aug_residual_u_finish(a, dd_u.get(), o1u.get(), scal.get() + 22, e.st);
     } else {
-      launch_aug_residual_u(a, o1u.get(), scal.get() + 22, e.st);
+      launch_aug_residual_u(a, dd_u.get(), o1u.get(), scal.get() + 22, e.st);
     }
     const auto v = fetch<2>(scal.get() + 21);
     const double rel = std::max(v[0], v[1]) / scale;

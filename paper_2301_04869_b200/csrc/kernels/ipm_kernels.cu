@@ -930,14 +930,8 @@ void launch_aug_residual_u_finish(const AugResidualArgs& a, const double* dd, do
 
 // the scenario sums spread over the GPU (warp per control), then one CTA
 // adds r1u + (sigma_u + dw) p_u and reduces the max
-void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st) {
-  static double* dd = nullptr;
-  static int dd_n = 0;
-  if (dd_n < a.d.n_u) {
-    if (dd) cudaFree(dd);
-    cudaMalloc(&dd, size_t(2) * a.d.n_u * sizeof(double));
-    dd_n = a.d.n_u;
-  }
+void launch_aug_residual_u(const AugResidualArgs& a, double* dd, double* o1u, double* out1,
+                           cudaStream_t st) {
   launch_aug_residual_u_local(a, dd, st);
   launch_aug_residual_u_finish(a, dd, o1u, out1, st);
 }

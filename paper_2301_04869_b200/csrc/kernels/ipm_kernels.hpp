@@ -99,7 +99,9 @@ struct AugResidualArgs {
 void launch_aug_residual(const AugResidualArgs& a, double* partial, double* out1,
                          cudaStream_t st);
 // o1u = r1u + (sigma_u + dw) p_u + sum_s part (double-double); out[0] = max|o1u|
-void launch_aug_residual_u(const AugResidualArgs& a, double* o1u, double* out1, cudaStream_t st);
+// dd: 2 n_u doubles of scratch (double-double sums), owned by the caller
+void launch_aug_residual_u(const AugResidualArgs& a, double* dd, double* o1u, double* out1,
+                           cudaStream_t st);
 // sharded variant: dd[2 n_u] = local sum of the per-scenario u-row partials
 // (hi, lo); after the cross-rank all-reduce, finish adds r1u + (sigma_u+dw) p_u
 void launch_aug_residual_u_local(const AugResidualArgs& a, double* dd, cudaStream_t st);

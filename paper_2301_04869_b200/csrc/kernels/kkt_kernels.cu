@@ -883,24 +883,17 @@ void check_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+}  // namespace
+
 size_t single_rhs_smem(int n_x) {
   const size_t b = size_t(2) * n_x * sizeof(double);
   return b <= 200 * 1024 ? b : 0;
 }
 
-}  // namespace
-
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, double* Dp, cudaStream_t st) {
+                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st) {
   if (M <= 0) return;
-  static double* scale = nullptr;
-  static int scale_n = 0;
-  if (scale_n < M) {
-    if (scale) cudaFree(scale);
-    cudaMalloc(&scale, size_t(M) * sizeof(double));
-    scale_n = M;
-  }
   refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
   check_launch("refactor_levels");
@@ -1042,17 +1035,9 @@ void launch_sum_parts(const double* parts, int nparts, long long len, double* ou
 
 void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
   if (a.M <= 0) return;
-  static double* scratch = nullptr;
-  static size_t scratch_n = 0;
   const size_t smem = single_rhs_smem(a.n_x);
-  if (!smem) {
-    const size_t need = size_t(a.M) * 2 * a.n_x;
-    if (need > scratch_n) {
-      if (scratch) cudaFree(scratch);
-      cudaMalloc(&scratch, need * sizeof(double));
-      scratch_n = need;
-    }
-  }
+  double* scratch = a.scratch;
+  if (!smem && !scratch) throw std::runtime_error("single-RHS kernels: scratch [M][2 n_x] required");
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(reduce_rhs_kernel<kSolveBlock>,
@@ -1074,17 +1059,9 @@ void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
 
 void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
   if (a.M <= 0) return;
-  static double* scratch = nullptr;
-  static size_t scratch_n = 0;
   const size_t smem = single_rhs_smem(a.n_x);
-  if (!smem) {
-    const size_t need = size_t(a.M) * 2 * a.n_x;
-    if (need > scratch_n) {
-      if (scratch) cudaFree(scratch);
-      cudaMalloc(&scratch, need * sizeof(double));
-      scratch_n = need;
-    }
-  }
+  double* scratch = a.scratch;
+  if (!smem && !scratch) throw std::runtime_error("single-RHS kernels: scratch [M][2 n_x] required");
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(recover_state_kernel<kSolveBlock>,

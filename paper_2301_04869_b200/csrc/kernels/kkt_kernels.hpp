@@ -20,7 +20,8 @@ namespace bipm {
 // (tl + 15) & ~15 doubles, zero-filled, for the streamed reduction's dense step.
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, double* Dp, cudaStream_t st);
+                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st);
+// scale: [M] doubles of scratch (per-scenario max |G_x| for the pivot guard)
 
 struct ReduceLaunch {
   DevLu lu;
@@ -55,7 +56,11 @@ struct RhsLaunch {
   const double *rhat1, *rhat3;  // [M][n_x]
   double dw;
   double* part;  // [M][n_u] per-scenario contributions
+  double* scratch;  // [M][2 n_x] when single_rhs_smem(n_x) == 0, else unused
 };
+// shared memory of the single-RHS kernels' two n_x vectors, 0 when they do
+// not fit (the caller then provides RhsLaunch/RecoverLaunch::scratch)
+size_t single_rhs_smem(int n_x);
 void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st);
 
 struct RecoverLaunch {
@@ -66,6 +71,7 @@ struct RecoverLaunch {
   const double *rhat1, *rhat3, *pu;
   double dw;
   double *px, *py;  // [M][n_x]
+  double* scratch;  // [M][2 n_x] when single_rhs_smem(n_x) == 0, else unused
 };
 void launch_recover_state(const RecoverLaunch& a, cudaStream_t st);
 
