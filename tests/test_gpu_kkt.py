@@ -74,7 +74,10 @@ def synthetic_condensed(p, N, seed):
     }
 
 
-@pytest.mark.parametrize("case,N", [("case118", 16), ("case1354pegase", 3), ("case2869pegase", 2)])
+# case9241pegase: one control column per tile (K = 1 streamed program) and the
+# global-memory scratch of the single-RHS kernels (2 n_x doubles > 200 KB)
+@pytest.mark.parametrize("case,N", [("case118", 16), ("case1354pegase", 3), ("case2869pegase", 2),
+                                    ("case9241pegase", 1)])
 def test_reduce_matches_oracle_on_grid_patterns(case, N):
     p = nat.Problem(case_path(case), N, 0.05, 0)
     v = synthetic_condensed(p, N, seed=7)
