@@ -262,16 +262,25 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
     {
       double(*L)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
       double* rdiag = buf + kNb * (kNb + 1);  // reciprocals of the diagonal
-      for (int q = tid; q < w * w; q += 128) {
-        const int rr = q / w, cc = q % w;
-        L[rr][cc] = cc <= rr ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
+      {
+        // the diagonal block, zero-padded beyond w: all eight loads of a
+        // thread in flight, then the stores (a serial load/store loop cost
+        // ~5k cycles per panel)
+        constexpr int kPer = kNb * kNb / 128;
+        double v[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int q = tid + u * 128, rr = q % kNb, cc = q / kNb;
+          v[u] = (rr < w && cc < w && cc <= rr) ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+          const int q = tid + u * 128;
+          L[q % kNb][q / kNb] = v[u];
+        }
       }
       __syncthreads();
       if (tid < kNb) rdiag[tid] = tid < w ? 1.0 / L[tid][tid] : 1.0;
-      for (int q = tid; q < kNb * kNb; q += 128) {  // zero the padding of L
-        const int rr = q / kNb, cc = q % kNb;
-        if (rr >= w || cc >= w) L[rr][cc] = 0.0;
-      }
       __syncthreads();
       for (int rb = blockIdx.x * 128; rb < rows; rb += gridDim.x * 128) {
         const int r = c0 + w + rb + tid;
