@@ -638,13 +638,29 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
         break;
       }
       case kCopyBack: {
+        // four loads of a thread in flight before its stores (sts* are
+        // volatile asm with a memory clobber: a plain loop waits one L2
+        // round trip per element)
         if constexpr (K == 1) {
-          for (int i = tid; i < a.n_x; i += C)
-            sts1(xb + 8 * i, reinterpret_cast<const double*>(S)[i]);
+          const double* Sd = reinterpret_cast<const double*>(S);
+          for (int i0 = tid; i0 < a.n_x; i0 += 4 * C) {
+            double t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) t[u] = i0 + u * C < a.n_x ? Sd[i0 + u * C] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i0 + u * C < a.n_x) sts1(xb + 8 * (i0 + u * C), t[u]);
+          }
         } else {
-          for (int i = tid; i < nxk2; i += C) {
-            const double2 t = reinterpret_cast<const double2*>(S)[i];
-            sts2(xb + 16 * i, t.x, t.y);
+          const double2* S2 = reinterpret_cast<const double2*>(S);
+          for (int i0 = tid; i0 < nxk2; i0 += 4 * C) {
+            double2 t[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              t[u] = i0 + u * C < nxk2 ? S2[i0 + u * C] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              if (i0 + u * C < nxk2) sts2(xb + 16 * (i0 + u * C), t[u].x, t[u].y);
           }
         }
         consumer_sync<C>();
