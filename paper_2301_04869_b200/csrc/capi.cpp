@@ -327,6 +327,7 @@ int bipm_counters(int64_t out[3]) {
 
 int bipm_ctx_profile(bipm_ctx* c, int32_t enable) {
   return guarded([&] {
+    c->eng->resolve_timers();
     if (enable && !c->eng->profiling) c->eng->ktimers.clear();  // a new profiling window
     c->eng->profiling = enable != 0;
   });
@@ -334,6 +335,7 @@ int bipm_ctx_profile(bipm_ctx* c, int32_t enable) {
 
 int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* count) {
   return guarded([&] {
+    c->eng->resolve_timers();
     auto it = c->eng->ktimers.find(name);
     *ms = it == c->eng->ktimers.end() ? 0.0 : it->second.ms;
     *count = it == c->eng->ktimers.end() ? 0 : it->second.n;

@@ -52,8 +52,10 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
   cuda_check(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
-  cuda_check(cudaEventCreate(&ev_a), "event");
-  cuda_check(cudaEventCreate(&ev_b), "event");
+  cuda_check(cudaStreamCreateWithFlags(&st_rhs, cudaStreamNonBlocking), "stream");
+  cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+  if (const char* e = std::getenv("BIPM_NO_OVERLAP")) overlap_rhs = std::atoi(e) == 0;
   const DerivPlan& D = pb.D;
   const LuPlan& L = pb.LU;
   const OpfModel& Mo = pb.M;
@@ -318,8 +320,17 @@ void Engine::setup_stream() {
 }
 
 Engine::~Engine() {
-  if (ev_a) cudaEventDestroy(ev_a);
-  if (ev_b) cudaEventDestroy(ev_b);
+  if (st_rhs) {
+    cudaStreamSynchronize(st_rhs);
+    cudaStreamDestroy(st_rhs);
+  }
+  for (auto& t : pending_timers) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (st) {
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -441,6 +452,69 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   timed("reduce_rhs", [&] { launch_reduce_rhs(a, st); });
   launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st);
   if (multi()) comm->allreduce(d_out, size_t(pb.M.n_u), RedOpKind::kSum, st);
+}
+
+void Engine::reduce_rhs_fork(double dw, double* d_out) {
+  if (!overlap_rhs) {
+    reduce_rhs_local(dw, d_out);
+    return;
+  }
+  RhsLaunch a{};
+  a.lu = lu;
+  a.gu = gu_p.v;
+  a.kxx = kxx_p.v;
+  a.kxu = kxu_p.v;
+  a.n_x = pb.M.n_x;
+  a.n_u = pb.M.n_u;
+  a.M = M;
+  a.F = F.get();
+  a.FT = FT.get();
+  a.D = Dt.get();
+  a.gu_v = bd().gu.get();
+  a.kxx_v = kxx.get();
+  a.kxu_v = kxu.get();
+  a.sigma_x = sigma_x.get();
+  a.rhat1 = rhat1.get();
+  a.rhat3 = rhat3.get();
+  a.dw = dw;
+  a.part = rhs_part.get();
+  a.scratch = rhs_scratch.size() ? rhs_scratch.get() : nullptr;
+  cuda_check(cudaEventRecord(ev_fork, st), "fork");
+  cuda_check(cudaStreamWaitEvent(st_rhs, ev_fork, 0), "fork");
+  timed("reduce_rhs", [&] { launch_reduce_rhs(a, st_rhs); }, st_rhs);
+  launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st_rhs);
+  cuda_check(cudaEventRecord(ev_join, st_rhs), "join");
+}
+
+void Engine::reduce_rhs_join(double* d_out) {
+  if (!overlap_rhs) return;
+  cuda_check(cudaStreamWaitEvent(st, ev_join, 0), "join");
+  if (multi()) comm->allreduce(d_out, size_t(pb.M.n_u), RedOpKind::kSum, st);
+}
+
+cudaEvent_t Engine::take_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cuda_check(cudaEventCreate(&e), "event");
+  return e;
+}
+
+void Engine::resolve_timers() {
+  for (auto& t : pending_timers) {
+    cudaEventSynchronize(t.b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    KTimer& k = ktimers[t.name];
+    k.ms += ms;
+    ++k.n;
+    event_pool.push_back(t.a);
+    event_pool.push_back(t.b);
+  }
+  pending_timers.clear();
 }
 
 void Engine::finish_reduce(double dw) {

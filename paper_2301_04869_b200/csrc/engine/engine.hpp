@@ -132,6 +132,12 @@ class Engine {
   // rhs of the reduced system from (rhat1, rhat3) (defaults: the engine's)
   void reduce_rhs_local(double delta_w, double* d_rhs_out, const double* d_rhat1 = nullptr,
                         const double* d_rhat3 = nullptr);
+  // the same with the engine's rhat1/rhat3, issued on st_rhs after everything
+  // already queued on st (fork) so it runs beside the next launches on st
+  // (the Schur reduction); reduce_rhs_join orders st after it and does the
+  // cross-rank sum.  Without overlap_rhs: reduce_rhs_local.
+  void reduce_rhs_fork(double delta_w, double* d_rhs_out);
+  void reduce_rhs_join(double* d_rhs_out);
   // finish_reduce (kkt.cpp:468-488): K_hat = sum of the partial tiles (all
   // ranks) + diag(sigma_u + delta_w)
   void finish_reduce(double delta_w);
@@ -147,30 +153,41 @@ class Engine {
   void upload_ad();
   void setup_stream();
 
-  // optional CUDA-event timing of named kernel groups on the engine stream
+  // optional CUDA-event timing of named kernel groups: an event pair around
+  // each launch, no host synchronisation (the GPU keeps its queue); pairs are
+  // resolved into ktimers when read (resolve_timers)
   struct KTimer {
     double ms = 0;
     long long n = 0;
   };
   bool profiling = false;
   std::map<std::string, KTimer> ktimers;
-  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  struct PendingTimer {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  std::vector<PendingTimer> pending_timers;
+  std::vector<cudaEvent_t> event_pool;
+  cudaEvent_t take_event();
+  void resolve_timers();
   template <typename F>
-  void timed(const char* name, F&& launch) {
+  void timed(const char* name, F&& launch, cudaStream_t on = nullptr) {
     if (!profiling) {
       launch();
       return;
     }
-    cudaEventRecord(ev_a, st);
+    if (!on) on = st;
+    cudaEvent_t a = take_event(), b = take_event();
+    cudaEventRecord(a, on);
     launch();
-    cudaEventRecord(ev_b, st);
-    cudaEventSynchronize(ev_b);
-    float ms = 0;
-    cudaEventElapsedTime(&ms, ev_a, ev_b);
-    KTimer& t = ktimers[name];
-    t.ms += ms;
-    ++t.n;
+    cudaEventRecord(b, on);
+    pending_timers.push_back({name, a, b});
+    if (pending_timers.size() >= 256) resolve_timers();
   }
+  // side stream for the reduced rhs, overlapped with the Schur reduction
+  cudaStream_t st_rhs = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap_rhs = true;
   idx first_bad();
   size_t nnz(const Csr& c) const { return size_t(c.nnz()); }
 };

@@ -206,9 +206,13 @@ bool Solver::attempt(double dw, const DevIter& it) {
   (void)it;
   Engine::Bundle& bd = e.bd();
   ++reductions;
+  // the rhs reduction only reads the factors and the condensed blocks: it runs
+  // on a side stream beside the Schur reduction (filling the SMs of its last
+  // wave) and joins before the rhs is used
+  e.reduce_rhs_fork(dw, rhs_sum.get());
   e.reduce_local(dw);
   e.finish_reduce(dw);
-  e.reduce_rhs_local(dw, rhs_sum.get());
+  e.reduce_rhs_join(rhs_sum.get());
   // refinement scale (independent of the factor) rides on the Cholesky sync
   launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
                    scal.get() + 20, e.st);
