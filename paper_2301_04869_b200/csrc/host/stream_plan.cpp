@@ -255,9 +255,12 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
     const Csr t = A.transpose_pattern();  // column u -> (state row, slot)
     t_slot.resize(t.val.size());
     for (size_t k = 0; k < t.val.size(); ++k) t_slot[k] = idx(t.val[k]);
-    for (int q = 0; q * R < n_u; ++q) {
-      const int ub = q * R, ue = std::min<int>(n_u, ub + R);
-      int u0 = ub;
+    // a step spans as many controls as fit (several accumulator registers
+    // q = u / R: the kernel loops over them), fewer steps than one per q
+    {
+      const int ue = int(n_u);
+      int u0 = 0;
+      const int q = 0;  // header aux0, unused by the kernel
       while (u0 < ue) {
         // grow the step while it fits
         int u1 = u0;

@@ -446,21 +446,25 @@ _Pragma("unroll")
 template <int K, int C>
 __device__ __forceinline__ void step_acc(const Hdr& h, unsigned items, unsigned col, unsigned v,
                                          unsigned xb, double (&acc)[kMaxQ], int tid) {
-  const int q = h.aux0, u0 = h.aux1;
-  const int u = q * (C / K) + tid / K, c = tid % K;
-  const int it = u - u0;
-  if (it >= 0 && it < h.n_items) {
-    const int4 m = ldsi4(items + 16 * it);
-    const int cx = K == 1 ? 0 : (((c >> 1) << 4));
-    const int co = K == 1 ? 0 : ((c & 1) << 3);
-    double a0 = 0.0, a1 = 0.0;
-    int t = m.y;
-    for (; t + 1 < m.z; t += 2) {
-      a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
-      a1 += lds1(v + 8 * (t + 1)) * lds1(xb + (ldsi(col + 4 * (t + 1)) ^ cx) + co);
+  // the step's controls [u0, u0 + n_items) may span several accumulator
+  // registers q (control u of column c lives in register q = u / (C / K))
+  const int u0 = h.aux1, n = h.n_items, c = tid % K;
+  const int cx = K == 1 ? 0 : (((c >> 1) << 4));
+  const int co = K == 1 ? 0 : ((c & 1) << 3);
+  for (int q = u0 / (C / K); q * (C / K) < u0 + n; ++q) {
+    const int u = q * (C / K) + tid / K;
+    const int it = u - u0;
+    if (it >= 0 && it < n) {
+      const int4 m = ldsi4(items + 16 * it);
+      double a0 = 0.0, a1 = 0.0;
+      int t = m.y;
+      for (; t + 1 < m.z; t += 2) {
+        a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
+        a1 += lds1(v + 8 * (t + 1)) * lds1(xb + (ldsi(col + 4 * (t + 1)) ^ cx) + co);
+      }
+      if (t < m.z) a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
+      acc_add(acc, q, -(a0 + a1));
     }
-    if (t < m.z) a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
-    acc_add(acc, q, -(a0 + a1));
   }
 }
 
