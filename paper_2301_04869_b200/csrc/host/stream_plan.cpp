@@ -1,5 +1,7 @@
 #include "stream_plan.hpp"
 
+#include <stdexcept>
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -24,8 +26,9 @@ struct Builder {
     std::vector<int> levels;  // sweep steps: 4 ints per level (unit_begin, unit_end, lg, barrier)
   };
 
+  // column entries are 16-bit panel rows, padded to 16 bytes
   static int pat_bytes(int n_items, int n_ent, int n_lev = 0) {
-    return 4 * kStepHeaderInts + 16 * n_lev + 16 * n_items + 4 * ((n_ent + 3) & ~3);
+    return 4 * kStepHeaderInts + 16 * n_lev + 16 * n_items + 2 * ((n_ent + 7) & ~7);
   }
   // lanes per work unit: all units in one pass of `lanes` threads, and at
   // least ~3 entries per lane
@@ -46,7 +49,7 @@ struct Builder {
     const int K = S.K, NG = K > kStreamUnitCols ? K / kStreamUnitCols : 1;
     const int n_items = int(p.items.size() / 4);
     const int n_lev = int(p.levels.size() / 4);
-    const int n_col = (int(p.col.size()) + 3) & ~3;
+    const int n_col = (int(p.col.size()) + 7) & ~7;  // 16-bit entries
     StepIssue is{};
     is.pat_off = int(S.pat.size());
     is.pat_bytes = pat_bytes(n_items, int(p.col.size()), n_lev);
@@ -66,8 +69,9 @@ struct Builder {
     if (p.kind == kStepSweep || p.kind == kStepSpmv)
       for (int it = 0; it < n_items; ++it)
         p.items[size_t(it) * 4] = panel_word(p.items[size_t(it) * 4], K);
-    if (p.kind == kStepSweep || p.kind == kStepSpmv || p.kind == kStepAcc)
-      for (int& c : p.col) c = panel_word(c, K);
+    // columns stay panel ROWS (16 bits; the kernel forms the panel word)
+    for (int c : p.col)
+      if (c < 0 || c > 0xffff) throw std::runtime_error("stream program: panel row exceeds 16 bits");
     const int warp0 = warp_rr;
     if (units > 0) {
       const int upw = 32 >> lg;
@@ -78,8 +82,11 @@ struct Builder {
     S.pat.insert(S.pat.end(), hdr, hdr + kStepHeaderInts);
     S.pat.insert(S.pat.end(), p.levels.begin(), p.levels.end());
     S.pat.insert(S.pat.end(), p.items.begin(), p.items.end());
-    S.pat.insert(S.pat.end(), p.col.begin(), p.col.end());
-    S.pat.resize(S.pat.size() + size_t(n_col - int(p.col.size())), 0);
+    for (int i = 0; i < n_col; i += 2) {
+      const int c0 = i < int(p.col.size()) ? p.col[size_t(i)] : 0;
+      const int c1 = i + 1 < int(p.col.size()) ? p.col[size_t(i) + 1] : 0;
+      S.pat.push_back(int(unsigned(c0) | (unsigned(c1) << 16)));
+    }
     is.val_arr = p.val_count > 0 ? p.val_arr : 0;
     is.val_off = p.val_off;
     is.val_count = p.val_count;

@@ -34,7 +34,7 @@ enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre
 // Step pattern block: a 64-byte header (16 ints)
 //   {kind, flags, n_items, n_col, aux0, aux1, vcount, par, lg, n_units, warp0, n_lev, 0...}
 // then n_lev int4 level records (sweep steps), n_items int4 items and n_col
-// column words.  All-warp steps (dense, spmv): a unit is (item, group of up to
+// 16-bit column entries (panel rows; the kernel forms the panel word).  All-warp steps (dense, spmv): a unit is (item, group of up to
 // 8 panel columns) served by 2^lg lanes, chunks of 32 >> lg units dealt to
 // the 16 consumer warps round robin from warp0.  Sweep steps: aux0 = T, the
 // team of the lowest T warps running them; level record = (unit begin, unit

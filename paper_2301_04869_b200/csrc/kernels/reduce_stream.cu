@@ -176,6 +176,14 @@ __device__ __forceinline__ void acc_add(double (&acc)[kMaxQ], int q, double v) {
     if (r == q) acc[r] += v;
 }
 
+// column entry t of a step: a 16-bit panel row -> its panel word
+template <int K>
+__device__ __forceinline__ int colw(unsigned col, int t) {
+  unsigned short r;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(col + 2 * t));
+  return Panel<K>::word(int(r));
+}
+
 // Step header (host/stream_plan.hpp): 16 ints
 struct Hdr {
   int kind, flags, n_items, n_col, aux0, aux1, vcount, par, lg, n_units, warp0, n_lev;
@@ -265,12 +273,12 @@ __device__ __forceinline__ void step_sweep(const Hdr& h, unsigned lev, unsigned 
         m = ldsi4(items + 16 * item);
         int t = m.y + dg + sub;
         for (; t + g < m.z; t += 2 * g) {
-          const int w0 = ldsi(col + 4 * t), w1 = ldsi(col + 4 * (t + g));
+          const int w0 = colw<K>(col, t), w1 = colw<K>(col, t + g);
           const double v0 = lds1(v + 8 * t), v1 = lds1(v + 8 * (t + g));
           Pn::fma(a, v0, xb, w0, cg);
           Pn::fma(a, v1, xb, w1, cg);
         }
-        if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, ldsi(col + 4 * t), cg);
+        if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, colw<K>(col, t), cg);
       }
       reduce_lanes<Pn::CW>(a, g);
       if (active && sub == 0) {
@@ -417,12 +425,12 @@ _Pragma("unroll")
       m = ldsi4(items + 16 * item);
       int t = m.y + sub;
       for (; t + g < m.z; t += 2 * g) {
-        const int w0 = ldsi(col + 4 * t), w1 = ldsi(col + 4 * (t + g));
+        const int w0 = colw<K>(col, t), w1 = colw<K>(col, t + g);
         const double v0 = lds1(v + 8 * t), v1 = lds1(v + 8 * (t + g));
         Pn::fma(a, v0, xb, w0, cg);
         Pn::fma(a, v1, xb, w1, cg);
       }
-      if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, ldsi(col + 4 * t), cg);
+      if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, colw<K>(col, t), cg);
     }
     reduce_lanes<Pn::CW>(a, g);
     if (active && sub == 0) {
@@ -459,10 +467,10 @@ __device__ __forceinline__ void step_acc(const Hdr& h, unsigned items, unsigned 
       double a0 = 0.0, a1 = 0.0;
       int t = m.y;
       for (; t + 1 < m.z; t += 2) {
-        a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
-        a1 += lds1(v + 8 * (t + 1)) * lds1(xb + (ldsi(col + 4 * (t + 1)) ^ cx) + co);
+        a0 += lds1(v + 8 * t) * lds1(xb + (colw<K>(col, t) ^ cx) + co);
+        a1 += lds1(v + 8 * (t + 1)) * lds1(xb + (colw<K>(col, t + 1) ^ cx) + co);
       }
-      if (t < m.z) a0 += lds1(v + 8 * t) * lds1(xb + (ldsi(col + 4 * t) ^ cx) + co);
+      if (t < m.z) a0 += lds1(v + 8 * t) * lds1(xb + (colw<K>(col, t) ^ cx) + co);
       acc_add(acc, q, -(a0 + a1));
     }
   }
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
     const unsigned lev = base + 4 * kStepHeaderIntsDev;
     const unsigned items = lev + 16 * h.n_lev;
     const unsigned col = items + 16 * h.n_items;
-    const unsigned vals = col + 4 * h.n_col;
+    const unsigned vals = col + 2 * h.n_col;
     const int vshift = (h.par & 1) ^ ((h.par >> 1) & s & 1);
     const unsigned v = vals + 8 * vshift;
     tr(3);

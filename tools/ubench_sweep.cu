@@ -40,7 +40,7 @@ __device__ void sweep_timed(int e_x, int e_y, int lg, int T, unsigned items, uns
           int w[4];
           double vv[4];
 #pragma unroll
-          for (int u = 0; u < 4; ++u) w[u] = ldsi(col + 4 * (t + u * g));
+          for (int u = 0; u < 4; ++u) w[u] = colw<K>(col, t + u * g);
 #pragma unroll
           for (int u = 0; u < 4; ++u) vv[u] = lds1(v + 8 * (t + u * g));
 #pragma unroll
@@ -48,12 +48,12 @@ __device__ void sweep_timed(int e_x, int e_y, int lg, int T, unsigned items, uns
         }
       }
       for (; t + g < m.z; t += 2 * g) {
-        const int w0 = ldsi(col + 4 * t), w1 = ldsi(col + 4 * (t + g));
+        const int w0 = colw<K>(col, t), w1 = colw<K>(col, t + g);
         const double v0 = lds1(v + 8 * t), v1 = lds1(v + 8 * (t + g));
         Pn::fma(a, v0, xb, w0, 0);
         Pn::fma(a, v1, xb, w1, 0);
       }
-      if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, ldsi(col + 4 * t), 0);
+      if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, colw<K>(col, t), 0);
     }
     // consume a[] so the timing includes the FMAs
     double sum = 0;
@@ -90,14 +90,14 @@ __global__ void __launch_bounds__(C) level_bench(int n_x, int units, int ent, in
   // step layout: level record | items | col | values
   int4* levr = reinterpret_cast<int4*>(ring);
   int4* items = levr + 1;
-  int* col = reinterpret_cast<int*>(items + units);
-  double* v = reinterpret_cast<double*>(col + ((units * ent + 3) & ~3));
+  unsigned short* col = reinterpret_cast<unsigned short*>(items + units);  // 16-bit panel rows
+  double* v = reinterpret_cast<double*>(col + ((units * ent + 7) & ~7));
   const int tid = threadIdx.x;
   for (int i = tid; i < n_x * K; i += C) X[i] = 1e-3 * (i % 97);
   for (int u = tid; u < units; u += C)
     items[u] = make_int4(Panel<K>::word((u * 37) % n_x), u * ent, (u + 1) * ent, 0);
   for (int t = tid; t < units * ent; t += C) {
-    col[t] = Panel<K>::word((t * 7919 + 13) % n_x);
+    col[t] = (unsigned short)((t * 7919 + 13) % n_x);
     v[t] = 1e-6 * (t % 31);
   }
   if (tid == 0) levr[0] = make_int4(0, units, lg, 1);
