@@ -481,13 +481,14 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
   constexpr int kThreads = C + 32;
   using Pn = Panel<K>;
   extern __shared__ __align__(1024) unsigned char smem[];
-  // layout: X panel (offset 0, 256-byte aligned rows) | temp | barriers |
-  // ring offsets | tile lists | ring
+  // layout: X panel (offset 0, 256-byte aligned rows) | barriers | ring
+  // offsets | tile lists | ring.  The dense-tail product's output stages in
+  // the CTA's global scratch S (free while the dense steps run: S carries
+  // K~_xx T only from the product steps to the copy-back), which leaves its
+  // tl x K doubles of shared memory to the ring.
   const int P = a.steps;
   double* X = reinterpret_cast<double*>(smem);
-  double* temp = X + size_t(a.n_x) * K;
-  unsigned long long* full =
-      reinterpret_cast<unsigned long long*>(temp + ((size_t(a.tl) * K + 1) & ~size_t(1)));
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(X + size_t(a.n_x) * K);
   unsigned long long* empty = full + kNB;
   int* ring_off = reinterpret_cast<int*>(empty + kNB);
   const int tile = blockIdx.x, chunk = blockIdx.y;
@@ -580,6 +581,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = 0.0;
   char* S = reinterpret_cast<char*>(a.scratch + size_t(chunk * gridDim.x + tile) * a.n_x * K);
+  double* temp = reinterpret_cast<double*>(S);
   const int nxk2 = a.n_x * K / 2;  // 16-byte chunks of the panel (K >= 2)
   const bool stamp = a.phase && tile == 0 && chunk == 0 && tid == 0;
   Tracer tr;
@@ -637,7 +639,16 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
                           size_t(h.aux0) * a.tl * ((a.tl + 15) & ~15);
         step_dense_global<K, C>(W, xb, temp, a.t0, a.tl, tid);
         consumer_sync<C>();
-        for (int e = tid; e < a.tl * K; e += C) sts1(xb + Pn::elem(a.t0 + e / K, e % K), temp[e]);
+        for (int e0 = tid; e0 < a.tl * K; e0 += 4 * C) {  // four L2 loads in flight
+          double t[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t[u] = e0 + u * C < a.tl * K ? temp[e0 + u * C] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * C;
+            if (e < a.tl * K) sts1(xb + Pn::elem(a.t0 + e / K, e % K), t[u]);
+          }
+        }
         break;
       }
       case kAcc:
@@ -741,9 +752,11 @@ __global__ void gather_values_kernel(const double* __restrict__ in, long long in
 }  // namespace
 
 size_t stream_smem_bytes(int n_x, int K, int tl, int steps, int list_cap, int ring_bytes) {
-  // panel + dense-tail temp + barriers + ring offsets + tile lists + ring
-  return size_t(n_x) * K * 8 + ((size_t(tl) * K + 1) & ~size_t(1)) * 8 + 2 * kNB * 8 +
-         size_t((steps + 3) & ~3) * 4 + size_t(list_cap) * 8 + 16 + ring_bytes;
+  // panel + barriers + ring offsets + tile lists + ring (the dense-tail output
+  // stages in global scratch: tl is not needed here)
+  (void)tl;
+  return size_t(n_x) * K * 8 + 2 * kNB * 8 + size_t((steps + 3) & ~3) * 4 +
+         size_t(list_cap) * 8 + 16 + ring_bytes;
 }
 
 int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap, int ctas_per_sm) {
