@@ -316,7 +316,7 @@ void Engine::setup_stream() {
   sl.kuu = kuu_p.v;
   sl.iperm = lu.iperm;
   const int tiles = (n_u + K - 1) / K;
-  sp_scratch.resize(size_t(tiles) * sl.nchunks * n_x * K);
+  sp_scratch.resize(size_t(tiles) * sl.nchunks * (size_t(n_x) * K + size_t(list_cap)));
 }
 
 Engine::~Engine() {

@@ -495,11 +495,15 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
   const int j0 = tile * K;
   const int k = min(K, a.n_u - j0);
   // tile lists: (panel byte offset, slot) of the tile's G_u and K_xu columns
-  int2* gu_list = reinterpret_cast<int2*>(ring_off + ((P + 3) & ~3));
+  // tile lists in the CTA's global scratch, after S (n_x K doubles): read
+  // once per scenario, so shared memory goes to the ring instead
+  double* cta_scratch =
+      a.scratch + size_t(chunk * gridDim.x + tile) * (size_t(a.n_x) * K + a.list_cap);
+  int2* gu_list = reinterpret_cast<int2*>(cta_scratch + size_t(a.n_x) * K);
   const int n_gu = a.gu.t_ptr[j0 + k] - a.gu.t_ptr[j0];
   const int n_kxu = a.kxu.t_ptr[j0 + k] - a.kxu.t_ptr[j0];
   int2* kxu_list = gu_list + ((n_gu + 1) & ~1);
-  unsigned char* ring = reinterpret_cast<unsigned char*>(kxu_list + ((n_kxu + 1) & ~1));
+  unsigned char* ring = reinterpret_cast<unsigned char*>(ring_off + ((P + 3) & ~3));
   ring = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(ring) + 15) & ~size_t(15));
   const unsigned xb = smem_u32(X), rb = smem_u32(ring);
 
@@ -580,7 +584,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
   double acc[kMaxQ];
 #pragma unroll
   for (int q = 0; q < kMaxQ; ++q) acc[q] = 0.0;
-  char* S = reinterpret_cast<char*>(a.scratch + size_t(chunk * gridDim.x + tile) * a.n_x * K);
+  char* S = reinterpret_cast<char*>(cta_scratch);
   double* temp = reinterpret_cast<double*>(S);
   const int nxk2 = a.n_x * K / 2;  // 16-byte chunks of the panel (K >= 2)
   const bool stamp = a.phase && tile == 0 && chunk == 0 && tid == 0;
@@ -620,7 +624,17 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
         }
         consumer_sync<C>();
         const double* gu = a.gu_v + size_t(s) * a.gu.nnz;
-        for (int e = tid; e < n_gu; e += C) sts1(xb + gu_list[e].x, gu[gu_list[e].y]);
+        for (int e0 = tid; e0 < n_gu; e0 += 4 * C) {  // list and value loads in flight
+          int2 l[4];
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) l[u] = e0 + u * C < n_gu ? gu_list[e0 + u * C] : make_int2(0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) g[u] = e0 + u * C < n_gu ? gu[l[u].y] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (e0 + u * C < n_gu) sts1(xb + l[u].x, g[u]);
+        }
         break;
       }
       case kSweep:
@@ -688,8 +702,18 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
         }
         consumer_sync<C>();
         const double* kxu = a.kxu_v + size_t(s) * a.kxu.nnz;
-        for (int e = tid; e < n_kxu; e += C)
-          sts1(xb + kxu_list[e].x, lds1(xb + kxu_list[e].x) + kxu[kxu_list[e].y]);
+        for (int e0 = tid; e0 < n_kxu; e0 += 4 * C) {
+          int2 l[4];
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            l[u] = e0 + u * C < n_kxu ? kxu_list[e0 + u * C] : make_int2(0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) g[u] = e0 + u * C < n_kxu ? kxu[l[u].y] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (e0 + u * C < n_kxu) sts1(xb + l[u].x, lds1(xb + l[u].x) + g[u]);
+        }
         break;
       }
       default:
@@ -752,11 +776,11 @@ __global__ void gather_values_kernel(const double* __restrict__ in, long long in
 }  // namespace
 
 size_t stream_smem_bytes(int n_x, int K, int tl, int steps, int list_cap, int ring_bytes) {
-  // panel + barriers + ring offsets + tile lists + ring (the dense-tail output
-  // stages in global scratch: tl is not needed here)
+  // panel + barriers + ring offsets + ring (the dense-tail output and the
+  // tile lists live in global scratch: tl and list_cap are not needed here)
   (void)tl;
-  return size_t(n_x) * K * 8 + 2 * kNB * 8 + size_t((steps + 3) & ~3) * 4 +
-         size_t(list_cap) * 8 + 16 + ring_bytes;
+  (void)list_cap;
+  return size_t(n_x) * K * 8 + 2 * kNB * 8 + size_t((steps + 3) & ~3) * 4 + 16 + ring_bytes;
 }
 
 int stream_ring_capacity(int n_x, int K, int tl, int steps, int list_cap, int ctas_per_sm) {
