@@ -117,8 +117,12 @@ struct LuPlan {
 };
 
 // dense tail selection (make_lu_plan): top etree levels of at most
-// kTailWidth rows, at most kMaxTail rows (env BIPM_TAIL_WIDTH / BIPM_TAIL_MAX)
-constexpr idx kTailWidth = 6;
+// kTailWidth rows, at most kMaxTail rows (env BIPM_TAIL_WIDTH / BIPM_TAIL_MAX,
+// the latter clamped to kMaxTail, the Gauss-Jordan kernel's limit).  Measured
+// at 1354 (tl 233 -> 320): the reduction loses more sweep levels than it gains
+// DMMA work, -10 % per reduction, +1.2 ms per refactor, -6 % per iteration
+// (widths >= 12 all reach the 320-row cap there; 8: -3 %, 6: the old default)
+constexpr idx kTailWidth = 16;
 constexpr idx kMaxTail = 320;
 
 std::vector<idx> min_degree_order(const Csr& sym_pattern);
