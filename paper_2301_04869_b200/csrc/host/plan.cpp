@@ -436,7 +436,7 @@ LuPlan make_lu_plan(const Csr& A) {
     idx width = kTailWidth, max_rows = kMaxTail;
     if (const char* e = std::getenv("BIPM_TAIL_WIDTH")) width = std::atoi(e);
     if (const char* e = std::getenv("BIPM_TAIL_MAX"))
-      max_rows = std::max<idx>(0, std::min<idx>(kMaxTail, std::atoi(e)));
+      max_rows = std::max<idx>(0, std::min<idx>(kMaxTailLimit, std::atoi(e)));
     const std::vector<char> tail = choose_tail_rows(lrow, width, max_rows);
     std::vector<idx> perm2;
     perm2.reserve(size_t(n));

@@ -118,12 +118,14 @@ struct LuPlan {
 
 // dense tail selection (make_lu_plan): top etree levels of at most
 // kTailWidth rows, at most kMaxTail rows (env BIPM_TAIL_WIDTH / BIPM_TAIL_MAX,
-// the latter clamped to kMaxTail, the Gauss-Jordan kernel's limit).  Measured
-// at 1354 (tl 233 -> 320): the reduction loses more sweep levels than it gains
-// DMMA work, -10 % per reduction, +1.2 ms per refactor, -6 % per iteration
-// (widths >= 12 all reach the 320-row cap there; 8: -3 %, 6: the old default)
+// the latter clamped to kMaxTailLimit).  Measured at 1354: width 6 (tl 233)
+// -> 16 (tl 307): the reduction loses more sweep levels than it gains DMMA
+// work, -10 % per reduction, +1.2 ms per refactor, -6 % per iteration; wider
+// tails (width 32: tl 452, 64: tl 489) shave another 5 % off the reduction
+// but the Gauss-Jordan inverse grows as tl^3 (7-12 ms per refactor): net loss
 constexpr idx kTailWidth = 16;
 constexpr idx kMaxTail = 320;
+constexpr idx kMaxTailLimit = 512;  // the Gauss-Jordan kernel's limit (env BIPM_TAIL_MAX up to it)
 
 std::vector<idx> min_degree_order(const Csr& sym_pattern);
 LuPlan make_lu_plan(const Csr& gx_pattern);

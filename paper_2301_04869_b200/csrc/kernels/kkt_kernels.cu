@@ -236,6 +236,7 @@ __device__ __forceinline__ void gj_dmma(double& d0, double& d1, double a, double
 // blocks padded to 20 and tl-wide rows to 16k + 4 so the m8n8k4 fragment
 // loads (8 rows x 4 columns / 4 rows x 8 columns) hit distinct banks
 constexpr int kGjB = 16, kGjLdb = 20;
+constexpr int kGjMaxTail = 512;  // host/plan.hpp kMaxTail must not exceed it
 inline __host__ __device__ int gj_tp(int tl) { return (tl + 7) & ~7; }
 inline __host__ __device__ int gj_ldr(int tl) { return ((gj_tp(tl) + 15) & ~15) + 4; }
 inline size_t gj_smem_bytes(int tl) {
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gm = lane >> 2, gk = lane & 3;
   constexpr int kWarps = BLOCK / 32;
-  constexpr int kJ = 10;  // tl <= 320: a row's columns over the lanes
+  constexpr int kJ = kGjMaxTail / 32;  // a row's columns over the lanes
   {
     // S from the factor: every load of a row in flight at once
     double* W = Wbase + (npass & 1) * tt;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     double* Wn = Wbase + ((npass - pass - 1) & 1) * tt;
     {
       // C' and W[P, :]: all of a thread's loads in flight, then the stores
-      constexpr int kQ = (320 * kB + BLOCK - 1) / BLOCK;
+      constexpr int kQ = (kGjMaxTail * kB + BLOCK - 1) / BLOCK;
       double v[kQ];
 #pragma unroll
       for (int u = 0; u < kQ; ++u) {
