@@ -11,22 +11,29 @@
  * them.
  *
  * Reference interfaces replaced (file:line under proj/core):
- *   bipm_problem_create      opf::parse_matpower_file + generate_scenarios +
+ *   bipm_problem_create[_ex] opf::parse_matpower_file + generate_scenarios +
  *                            build_block_opf + make_ad_plan
  *                            (opf_parse.cpp:216, scenarios.cpp:44,
  *                             opf_model.cpp:624, autodiff.cpp:180)
+ *   bipm_problem_create_tables  the same from the reference's in-memory
+ *                            tables: opf::CaseData + opf::ScenarioSet
+ *                            (opf.hpp:54-82; build_block_opf, opf_model.cpp:624)
+ *   bipm_problem_create_patterns  make_ad_plan's split patterns +
+ *                            make_condense_work (autodiff.hpp:40-60,
+ *                            kkt.cpp:111-117): the KKT operators only
  *   bipm_eval_bundle         eval_bundle_range            (autodiff.hpp:131-133)
  *   bipm_eval_values         batch_eval                   (autodiff.hpp:96-97)
- *   bipm_condense            condense                     (kkt.hpp:110)
+ *   bipm_condense            condense                     (kkt.hpp:110, kkt.cpp:123-170)
  *   bipm_factor_gx           factor_gx_range / BlockDiagFactor::factor
- *                                                         (kkt.hpp:162, linalg.hpp:213)
+ *                                                         (kkt.hpp:162, linalg.cpp:51-89)
  *   bipm_reduce              reduce + finish_reduce       (kkt.hpp:139-142)
- *   bipm_reduce_rhs          reduce_rhs_group             (kkt.cpp:209)
+ *   bipm_reduce_rhs          reduce_rhs_group + all_reduce_sum (kkt.cpp:209-239)
  *   bipm_dense_factor_solve  factor_dense_sym + solve     (linalg.hpp:116, kkt.cpp:965-976)
  *   bipm_recover             recover_state_adjoint + recover_slack_dual
  *                                                         (kkt.hpp:114,147-148)
- *   bipm_solve_reduced       solve_reduced                (kkt.hpp:170-172)
+ *   bipm_solve_reduced       solve_reduced                (kkt.hpp:170-172, kkt.cpp:945-1006)
  *   bipm_solve               solve (the IPM driver)       (ipm.hpp:361)
+ *   bipm_solver_iterate      SolveResult::iterate         (ipm.hpp:41-52, model.hpp:41-55)
  */
 #ifndef BIPM_GPU_H
 #define BIPM_GPU_H
@@ -53,11 +60,71 @@ typedef struct bipm_problem bipm_problem; /* host model + symbolic plans */
 typedef struct bipm_ctx bipm_ctx;         /* one GPU owning scenarios [lo, hi) */
 
 const char* bipm_last_error(void);
+/* global scenario index the last failure names (SingularBlockError::block,
+ * NonFiniteError::block; types.hpp:99-109), -1 when none */
+int32_t bipm_last_error_block(void);
 int bipm_version(void);
 
 /* ---- problem (host, no GPU needed) ---------------------------------- */
+/* MATPOWER file + generate_scenarios(cs, N, sigma, {}, seed) */
 int bipm_problem_create(const char* case_path, int32_t N, double sigma, uint64_t seed,
                         bipm_problem** out);
+/* the same with contingencies: branch indices (into mpc.branch, in service),
+ * the k-th outaged in scenario k mod N (scenarios.cpp:44-80) */
+int bipm_problem_create_ex(const char* case_path, int32_t N, double sigma, uint64_t seed,
+                           const int32_t* contingencies, int32_t n_contingencies,
+                           bipm_problem** out);
+
+/* opf::CaseData (opf.hpp:19-62) as row-major tables, file units (MW, MVAr,
+ * degrees).  Columns follow the reference's row structs:
+ *   bus     [nbus][10]   id type Pd Qd Gs Bs Vm Va Vmax Vmin       (BusRow)
+ *   gen     [ngen][9]    bus Pg Qg Qmax Qmin Vg status Pmax Pmin   (GenRow)
+ *   branch  [nbranch][9] from to r x b rateA tap shift status      (BranchRow)
+ *   gencost [ngencost][4] model startup shutdown ncost, with the ncost
+ *           coefficients of row i (highest order first) consecutive in
+ *           gencost_coef                                          (GenCostRow) */
+#define BIPM_BUS_COLS 10
+#define BIPM_GEN_COLS 9
+#define BIPM_BRANCH_COLS 9
+#define BIPM_GENCOST_COLS 4
+typedef struct {
+  const char* name;
+  double base_mva;
+  int32_t nbus, ngen, nbranch, ngencost;
+  const double* bus;
+  const double* gen;
+  const double* branch;
+  const double* gencost;
+  const double* gencost_coef;
+} bipm_case_tables;
+/* opf::ScenarioSet (opf.hpp:64-74): multipliers [N][nbus] (the reference's
+ * Matrix(nbus, N)); outages of scenario s are outage_branch[outage_ptr[s] ..
+ * outage_ptr[s+1]) (branch indices); outage_ptr may be NULL (no outages) */
+typedef struct {
+  int32_t N;
+  double sigma;
+  uint64_t seed;
+  const double* multipliers;
+  const int32_t* outage_ptr;
+  const int32_t* outage_branch;
+} bipm_scenario_tables;
+int bipm_problem_create_tables(const bipm_case_tables* cs, const bipm_scenario_tables* sc,
+                               bipm_problem** out);
+
+/* a shared int32 CSR pattern (SparsityPattern, sparse.hpp:13-30) */
+typedef struct {
+  int32_t rows, cols;
+  const int32_t* row_ptr; /* rows + 1 */
+  const int32_t* col_ind; /* row_ptr[rows], strictly increasing per row */
+} bipm_csr;
+/* KKT-operator problem from the derivative patterns of a reference AdPlan:
+ * G_x | G_u = g_split.x_pat | u_pat, H_x | H_u = h_split.x_pat | u_pat,
+ * W_xx, W_xu, W_uu = w_split.xx, xu, uu.  Contexts of such a problem serve
+ * the KKT operators (condense ... solve_reduced); the AD and the IPM driver
+ * need an OPF problem. */
+int bipm_problem_create_patterns(int32_t N, const bipm_csr* gx, const bipm_csr* gu,
+                                 const bipm_csr* hx, const bipm_csr* hu, const bipm_csr* wxx,
+                                 const bipm_csr* wxu, const bipm_csr* wuu, bipm_problem** out);
 void bipm_problem_destroy(bipm_problem* p);
 /* dims[0..9] = N, n_x, n_u, m, n_b, nbus, nbranch, ngen, nnz(L+U) factor, levels(fwd) */
 int bipm_problem_dims(const bipm_problem* p, int32_t dims[10]);
@@ -95,6 +162,61 @@ int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block);
  * diag(sigma_u + delta_w), rhs includes -rhat2.  Requires bipm_factor_gx. */
 int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* khat,
                 double* rhs);
+
+/* ---- reduced-strategy operators (kkt.hpp:53-172) --------------------------
+ * The augmented system of one ctx (AugmentedSystem, kkt.hpp:53-80) with the
+ * bundle blocks it references, scenario-major over the ctx's M scenarios.
+ * sigma_u and r1u are the full coupling rows (summed over ALL N scenarios,
+ * as assemble_augmented builds them), identical on every rank. */
+typedef struct {
+  const double *gx, *gu, *hx, *hu, *wxx, *wxu, *wuu; /* [M][nnz] */
+  const double *sigma_x, *r1x, *r3;                  /* [M][n_x]; r3 = g */
+  const double *sigma_s, *r2, *r4;                   /* [M][m] */
+  const double *sigma_u, *r1u;                       /* [n_u] */
+} bipm_augmented;
+/* CondensedSystem outputs (kkt.hpp:86-103); NULL members are skipped.
+ * rhat2 is the full coupling row (all ranks). */
+typedef struct {
+  double *kxx, *kxu, *kuu; /* [M][nnz K_..] on the condensed patterns (kxx_p, ...) */
+  double *rhat1, *rhat3;   /* [M][n_x] */
+  double *rhat2;           /* [n_u] */
+} bipm_condensed_out;
+/* condense(sys, work): BIPM_NON_INTERIOR when a Sigma_s entry is not positive */
+int bipm_condense(bipm_ctx* c, const bipm_augmented* a, const bipm_condensed_out* out);
+/* reduce_rhs_group over the ctx's scenarios, all-reduced over the ranks:
+ * rhs = sum_b [G_u' G_x^{-T} (rhat1 - K~_xx a) + K_xu' a], a = G_x^{-1} rhat3
+ * (no -rhat2 term).  Requires bipm_factor_gx. */
+int bipm_reduce_rhs(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* rhs);
+/* slack-side rows recover_slack_dual needs (kkt.cpp:172-188) */
+typedef struct {
+  const double *hx, *hu;            /* [M][nnz H_x], [M][nnz H_u] */
+  const double *sigma_s, *r2, *r4;  /* [M][m] */
+} bipm_slack_rows;
+/* recover_state_adjoint + recover_slack_dual at p_u (n_u): p_x, p_y [M][n_x],
+ * p_z, p_s [M][m].  Requires bipm_factor_gx. */
+int bipm_recover(bipm_ctx* c, const bipm_condensed* in, const bipm_slack_rows* s,
+                 double delta_w, const double* pu, double* px, double* py, double* pz,
+                 double* ps);
+/* RegSchedule (kkt.hpp:20-29); zero fields take the reference default */
+typedef struct {
+  double delta_w0, delta_w_min, delta_w_max, kappa_minus, kappa_plus, kappa_plus_emergency;
+} bipm_reg_schedule;
+typedef struct { /* Step (kkt.hpp:38-44); NULL members are skipped */
+  double *px, *pu, *ps, *pz, *py;
+} bipm_step;
+typedef struct { /* StepInfo (kkt.hpp:46-51) + the refinement rounds taken */
+  double delta_w;
+  int32_t corrections, refinements;
+  int64_t reductions;
+} bipm_step_info;
+/* solve_reduced: condense, batched G_x refactor, inertia loop of reduce +
+ * shift + dense Cholesky, recovery and up to 3 refinement rounds, all on the
+ * device.  delta_w_last is the warm start carried across calls (in/out).
+ * BIPM_SINGULAR_BLOCK (+ the reference's augmented fallback on the caller's
+ * side), BIPM_NON_INTERIOR, BIPM_LINEAR_SOLVE map onto the reference's
+ * exceptions. */
+int bipm_solve_reduced(bipm_ctx* c, const bipm_augmented* a, const bipm_reg_schedule* reg,
+                       double* delta_w_last, const bipm_step* out, bipm_step_info* info);
 
 /* Derivative bundle outputs (host, scenario-major over M; any may be NULL):
  * DerivativeBundle (autodiff.hpp:117-127). */
@@ -145,6 +267,7 @@ typedef struct { /* IpmOptions (ipm.hpp:7-25); zero fields take the default */
   int32_t max_iter; /* 300 */
 } bipm_solve_options;
 
+#define BIPM_STATUS_NOT_STARTED -2 /* bipm_solver_step before bipm_solver_start: BIPM_INVALID_ARGUMENT */
 #define BIPM_STATUS_RUNNING -1
 #define BIPM_STATUS_OPTIMAL 0
 #define BIPM_STATUS_MAX_ITER 1
@@ -166,6 +289,13 @@ int bipm_solver_start(bipm_solver* s);
 int bipm_solver_step(bipm_solver* s, int32_t* status);
 /* result so far; u (n_u, may be NULL) receives the current controls */
 int bipm_solver_result(bipm_solver* s, bipm_solve_result* r, double* u);
+/* the solver's current primal-dual point (Iterate, model.hpp:41-55), host
+ * arrays: x, y, kappa_lo, kappa_up [M][n_x]; s, z, nu_lo, nu_up [M][m];
+ * u, lambda_lo, lambda_up [n_u]; NULL members are skipped */
+typedef struct {
+  double *x, *u, *s, *y, *z, *kappa_lo, *kappa_up, *nu_lo, *nu_up, *lambda_lo, *lambda_up;
+} bipm_iterate;
+int bipm_solver_iterate(bipm_solver* s, const bipm_iterate* out);
 /* IterationLog k: rec[15] = iter, objective, inf_pr, inf_du, complementarity,
  * mu, alpha_primal, alpha_dual, t_ad, t_kkt, t_total, corrections,
  * refinements, delta_w, full_step */

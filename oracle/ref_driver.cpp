@@ -7,6 +7,7 @@
 //
 //   bipm_ref solve --case F --N n --sigma s --seed k [--groups G --workers W
 //                  --max-iter I --batch B --tol t] [--iterate-out DIR]
+//                  [--contingencies l1,l2,...]
 //       full reference solve (proj/core/src/ipm.cpp:435-664); prints one JSON
 //       object: status, iterations, objective, per-iteration logs, timers.
 //   bipm_ref dump --case F --N n --sigma s --seed k --iter K --out DIR
@@ -31,6 +32,12 @@
 #include "blockipm/ipm.hpp"
 #include "blockipm/kkt.hpp"
 #include "blockipm/opf.hpp"
+#ifdef BIPM_WITH_GPU_SHIM
+// bipm_ref_gpu: the same driver linked with integration/bipm_reference_shim.cpp
+// (--gpu kkt | ad | kkt,ad routes the reference's solve_reduced and/or its
+// AD calls to the B200 engine through the C-ABI)
+#include "bipm_reference_shim.hpp"
+#endif
 
 using namespace blockipm;
 
@@ -108,13 +115,20 @@ IpmOptions options_from(const Args& a) {
   return o;
 }
 
-BlockNlp load(const Args& a, opf::CaseData* cs_out = nullptr) {
+BlockNlp load(const Args& a, opf::CaseData* cs_out = nullptr, opf::ScenarioSet* sc_out = nullptr) {
   opf::CaseData cs = opf::parse_matpower_file(a.get("case"));
   const index_t N = std::stoi(a.get("N", "1"));
   const double sigma = std::stod(a.get("sigma", "0"));
   const std::uint64_t seed = std::stoull(a.get("seed", "0"));
-  opf::ScenarioSet sc = opf::generate_scenarios(cs, N, sigma, {}, seed);
+  std::vector<index_t> cont;  // --contingencies 4,7,...: branch indices, round-robin
+  {
+    std::stringstream ss(a.get("contingencies"));
+    for (std::string tok; std::getline(ss, tok, ',');)
+      if (!tok.empty()) cont.push_back(index_t(std::stoi(tok)));
+  }
+  opf::ScenarioSet sc = opf::generate_scenarios(cs, N, sigma, cont, seed);
   if (cs_out) *cs_out = cs;
+  if (sc_out) *sc_out = sc;
   return opf::build_block_opf(cs, sc);
 }
 
@@ -133,7 +147,14 @@ void dump_iterate(Dumper& d, const std::string& pre, const Iterate& it) {
 }
 
 int cmd_solve(const Args& a) {
-  const BlockNlp nlp = load(a);
+  opf::CaseData cs;
+  opf::ScenarioSet sc;
+  const BlockNlp nlp = load(a, &cs, &sc);
+#ifdef BIPM_WITH_GPU_SHIM
+  const std::string gpu = a.get("gpu");
+  if (gpu.find("kkt") != std::string::npos) bipm_shim::enable_kkt(true);
+  if (gpu.find("ad") != std::string::npos) bipm_shim::enable_ad(cs, sc);
+#endif
   IpmOptions o = options_from(a);
   Executor exec(o.exec);
   const auto t0 = std::chrono::steady_clock::now();
@@ -161,6 +182,10 @@ int cmd_solve(const Args& a) {
                     {"t_total", l.t_total},   {"corr", l.corrections},    {"fallback", l.fallback}});
   j["logs"] = logs;
   j["u"] = r.iterate.u;
+#ifdef BIPM_WITH_GPU_SHIM
+  j["gpu_kkt_calls"] = bipm_shim::kkt_calls();
+  j["gpu_ad_calls"] = bipm_shim::ad_calls();
+#endif
   std::printf("%s\n", j.dump().c_str());
   if (!a.get("iterate-out").empty()) {
     Dumper d{a.get("iterate-out")};

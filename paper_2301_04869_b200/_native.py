@@ -29,9 +29,10 @@ STATUS = {
 
 
 class BipmError(RuntimeError):
-    def __init__(self, code: int, msg: str):
+    def __init__(self, code: int, msg: str, block: int = -1):
         super().__init__(f"{STATUS.get(code, code)}: {msg}")
         self.code = code
+        self.block = block
 
 
 class SingularBlockError(BipmError):
@@ -42,7 +43,15 @@ class NonFiniteError(BipmError):
     """Mirror of blockipm::NonFiniteError (types.hpp:105-109)."""
 
 
-_EXC = {1: SingularBlockError, 2: NonFiniteError}
+class NonInteriorError(BipmError):
+    """Mirror of blockipm::NonInteriorError (kkt.hpp:31-33)."""
+
+
+class LinearSolveError(BipmError):
+    """Mirror of blockipm::LinearSolveError (kkt.hpp:34-36)."""
+
+
+_EXC = {1: SingularBlockError, 2: NonFiniteError, 6: NonInteriorError, 7: LinearSolveError}
 
 _lib = None
 _P = ctypes.c_void_p
@@ -52,6 +61,7 @@ _I = ctypes.POINTER(ctypes.c_int32)
 # exported symbol -> (restype, argtypes); also the list the CPU tests check
 SIGNATURES = {
     "bipm_last_error": (ctypes.c_char_p, []),
+    "bipm_last_error_block": (ctypes.c_int32, []),
     "bipm_version": (ctypes.c_int, []),
     "bipm_problem_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_double,
                                            ctypes.c_uint64, ctypes.POINTER(_P)]),
@@ -92,6 +102,17 @@ SIGNATURES = {
                                              ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_step_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
                                             ctypes.c_int32, _I]),
+    "bipm_problem_create_ex": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int32, ctypes.c_double,
+                                              ctypes.c_uint64, _I, ctypes.c_int32,
+                                              ctypes.POINTER(_P)]),
+    "bipm_problem_create_tables": (ctypes.c_int, [_P, _P, ctypes.POINTER(_P)]),
+    "bipm_problem_create_patterns": (ctypes.c_int, [ctypes.c_int32, _P, _P, _P, _P, _P, _P, _P,
+                                                    ctypes.POINTER(_P)]),
+    "bipm_condense": (ctypes.c_int, [_P, _P, _P]),
+    "bipm_reduce_rhs": (ctypes.c_int, [_P, _P, ctypes.c_double, _D]),
+    "bipm_recover": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, _D, _D, _D, _D, _D]),
+    "bipm_solve_reduced": (ctypes.c_int, [_P, _P, _P, _D, _P, _P]),
+    "bipm_solver_iterate": (ctypes.c_int, [_P, _P]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -127,7 +148,7 @@ def _destroy(obj, fn_name: str) -> None:
 def check(code: int) -> None:
     if code != 0:
         msg = lib().bipm_last_error().decode()
-        raise _EXC.get(code, BipmError)(code, msg)
+        raise _EXC.get(code, BipmError)(code, msg, lib().bipm_last_error_block())
 
 
 def dptr(a: np.ndarray):
@@ -142,6 +163,71 @@ class _Condensed(ctypes.Structure):
 
 class _Bundle(ctypes.Structure):
     _fields_ = [(n, _D) for n in BUNDLE_FIELDS]
+
+
+AUGMENTED_FIELDS = ("gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "sigma_x", "r1x", "r3",
+                    "sigma_s", "r2", "r4", "sigma_u", "r1u")
+CONDENSED_OUT_FIELDS = ("kxx", "kxu", "kuu", "rhat1", "rhat3", "rhat2")
+STEP_FIELDS = ("px", "pu", "ps", "pz", "py")
+ITERATE_FIELDS = ("x", "u", "s", "y", "z", "kappa_lo", "kappa_up", "nu_lo", "nu_up",
+                  "lambda_lo", "lambda_up")
+
+
+class _Augmented(ctypes.Structure):
+    _fields_ = [(n, _D) for n in AUGMENTED_FIELDS]
+
+
+class _CondensedOut(ctypes.Structure):
+    _fields_ = [(n, _D) for n in CONDENSED_OUT_FIELDS]
+
+
+class _SlackRows(ctypes.Structure):
+    _fields_ = [(n, _D) for n in ("hx", "hu", "sigma_s", "r2", "r4")]
+
+
+class _RegSchedule(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("delta_w0", "delta_w_min", "delta_w_max",
+                                               "kappa_minus", "kappa_plus",
+                                               "kappa_plus_emergency")]
+
+
+class _Step(ctypes.Structure):
+    _fields_ = [(n, _D) for n in STEP_FIELDS]
+
+
+class _StepInfo(ctypes.Structure):
+    _fields_ = [("delta_w", ctypes.c_double), ("corrections", ctypes.c_int32),
+                ("refinements", ctypes.c_int32), ("reductions", ctypes.c_int64)]
+
+
+class _Iterate(ctypes.Structure):
+    _fields_ = [(n, _D) for n in ITERATE_FIELDS]
+
+
+class _Csr(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int32), ("cols", ctypes.c_int32), ("row_ptr", _I),
+                ("col_ind", _I)]
+
+
+class _CaseTables(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char_p), ("base_mva", ctypes.c_double),
+                ("nbus", ctypes.c_int32), ("ngen", ctypes.c_int32), ("nbranch", ctypes.c_int32),
+                ("ngencost", ctypes.c_int32), ("bus", _D), ("gen", _D), ("branch", _D),
+                ("gencost", _D), ("gencost_coef", _D)]
+
+
+class _ScenarioTables(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("sigma", ctypes.c_double), ("seed", ctypes.c_uint64),
+                ("multipliers", _D), ("outage_ptr", _I), ("outage_branch", _I)]
+
+
+def iptr(a: np.ndarray):
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_I)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, _D, ctypes.c_int64, ctypes.c_int32)
@@ -171,18 +257,73 @@ class _SolveResult(ctypes.Structure):
                 ("reductions", ctypes.c_int64)]
 
 
-SOLVE_STATUS = {-1: "Running", 0: "Optimal", 1: "MaxIter", 2: "Infeasible"}
+SOLVE_STATUS = {-2: "NotStarted", -1: "Running", 0: "Optimal", 1: "MaxIter", 2: "Infeasible"}
 LOG_FIELDS = ("iter", "objective", "inf_pr", "inf_du", "complementarity", "mu", "alpha_p",
               "alpha_d", "t_ad", "t_kkt", "t_total", "corr", "refinements", "delta_w",
               "full_step")
 
 
 class Problem:
-    """Host model + symbolic plans (no GPU): bipm_problem_create."""
+    """Host model + symbolic plans (no GPU): bipm_problem_create[_ex].
 
-    def __init__(self, case_path: str, N: int, sigma: float = 0.0, seed: int = 0):
+    ``contingencies``: branch indices outaged round-robin over the scenarios
+    (generate_scenarios, scenarios.cpp:44-80)."""
+
+    def __init__(self, case_path: str | None, N: int, sigma: float = 0.0, seed: int = 0,
+                 contingencies=(), _handle=None):
         h = _P()
-        check(lib().bipm_problem_create(case_path.encode(), N, sigma, seed, ctypes.byref(h)))
+        if _handle is not None:
+            h = _handle
+        elif contingencies:
+            c = np.ascontiguousarray(contingencies, dtype=np.int32)
+            check(lib().bipm_problem_create_ex(case_path.encode(), N, sigma, seed, iptr(c),
+                                               len(c), ctypes.byref(h)))
+        else:
+            check(lib().bipm_problem_create(case_path.encode(), N, sigma, seed, ctypes.byref(h)))
+        self._init(h)
+
+    @classmethod
+    def from_tables(cls, base_mva: float, bus, gen, branch, gencost_rows, gencost_coef,
+                    multipliers, outages=None, sigma: float = 0.0, seed: int = 0,
+                    name: str = "tables"):
+        """bipm_problem_create_tables: the reference's CaseData / ScenarioSet as
+        tables (columns in include/bipm_gpu.h)."""
+        keep = [_f64(bus), _f64(gen), _f64(branch), _f64(gencost_rows), _f64(gencost_coef),
+                _f64(multipliers)]
+        t = _CaseTables(name.encode(), base_mva, keep[0].shape[0], keep[1].shape[0],
+                        keep[2].shape[0], keep[3].shape[0], *[dptr(a) for a in keep[:5]])
+        N = keep[5].shape[0]
+        sc = _ScenarioTables(N, sigma, seed, dptr(keep[5]), None, None)
+        if outages is not None:
+            ptr = np.zeros(N + 1, dtype=np.int32)
+            ptr[1:] = np.cumsum([len(o) for o in outages])
+            idx = np.ascontiguousarray(np.concatenate([np.asarray(o, dtype=np.int32)
+                                                       for o in outages] + [np.zeros(0, np.int32)]),
+                                       dtype=np.int32)
+            keep += [ptr, idx]
+            sc.outage_ptr, sc.outage_branch = iptr(ptr), iptr(idx)
+        h = _P()
+        check(lib().bipm_problem_create_tables(ctypes.byref(t), ctypes.byref(sc),
+                                               ctypes.byref(h)))
+        return cls(None, N, _handle=h)
+
+    @classmethod
+    def from_patterns(cls, N: int, pats: dict):
+        """bipm_problem_create_patterns: pats[name] = (row_ptr, col_ind, (rows, cols))
+        for gx, gu, hx, hu, wxx, wxu, wuu (KKT operators only)."""
+        keep, cs = [], []
+        for k in ("gx", "gu", "hx", "hu", "wxx", "wxu", "wuu"):
+            rp, ci, shape = pats[k]
+            rp = np.ascontiguousarray(rp, dtype=np.int32)
+            ci = np.ascontiguousarray(ci, dtype=np.int32)
+            keep += [rp, ci]
+            cs.append(_Csr(shape[0], shape[1], iptr(rp), iptr(ci)))
+        h = _P()
+        check(lib().bipm_problem_create_patterns(N, *[ctypes.byref(c) for c in cs],
+                                                 ctypes.byref(h)))
+        return cls(None, N, _handle=h)
+
+    def _init(self, h):
         self._h = h
         d = (ctypes.c_int32 * 10)()
         check(lib().bipm_problem_dims(h, d))
@@ -237,6 +378,60 @@ class Context:
         rhs = np.zeros(n_u)
         check(lib().bipm_reduce(self._h, ctypes.byref(c), delta_w, dptr(khat), dptr(rhs)))
         return khat.reshape(n_u, n_u).T.copy(), rhs  # column-major -> numpy
+
+    def _augmented(self, a: dict):
+        keep = {k: _f64(a[k]) for k in AUGMENTED_FIELDS}
+        return keep, _Augmented(**{k: dptr(v) for k, v in keep.items()})
+
+    def condense(self, **aug):
+        """condense (kkt.cpp:123-170) through bipm_condense."""
+        keep, a = self._augmented(aug)
+        p, M = self.problem, self.hi - self.lo
+        nnz = {k: len(p.array(k + "_p_colind")) for k in ("kxx", "kxu", "kuu")}
+        out = {k: np.zeros((M, v)) for k, v in nnz.items()}
+        out.update(rhat1=np.zeros((M, p.n_x)), rhat3=np.zeros((M, p.n_x)), rhat2=np.zeros(p.n_u))
+        o = _CondensedOut(**{k: dptr(v) for k, v in out.items()})
+        check(lib().bipm_condense(self._h, ctypes.byref(a), ctypes.byref(o)))
+        return out
+
+    def _condensed(self, arrays: dict):
+        keep = {k: _f64(arrays[k]) for k, _ in _Condensed._fields_}
+        return keep, _Condensed(**{k: dptr(v) for k, v in keep.items()})
+
+    def reduce_rhs(self, delta_w: float, **arrays):
+        """reduce_rhs_group (kkt.cpp:209-239), summed over the ctx's scenarios."""
+        keep, c = self._condensed(arrays)
+        rhs = np.zeros(self.problem.n_u)
+        check(lib().bipm_reduce_rhs(self._h, ctypes.byref(c), delta_w, dptr(rhs)))
+        return rhs
+
+    def recover(self, delta_w: float, pu, hx, hu, sigma_s, r2, r4, **arrays):
+        """recover_state_adjoint + recover_slack_dual (kkt.cpp:507-532, 172-188)."""
+        keep, c = self._condensed(arrays)
+        srk = [_f64(v) for v in (hx, hu, sigma_s, r2, r4)]
+        sr = _SlackRows(*[dptr(v) for v in srk])
+        p, M = self.problem, self.hi - self.lo
+        pu = _f64(pu)
+        px, py = np.zeros((M, p.n_x)), np.zeros((M, p.n_x))
+        pz, ps = np.zeros((M, p.m)), np.zeros((M, p.m))
+        check(lib().bipm_recover(self._h, ctypes.byref(c), ctypes.byref(sr), delta_w, dptr(pu),
+                                 dptr(px), dptr(py), dptr(pz), dptr(ps)))
+        return {"px": px, "py": py, "pz": pz, "ps": ps}
+
+    def solve_reduced(self, delta_w_last: float = 0.0, reg: dict | None = None, **aug):
+        """solve_reduced (kkt.cpp:945-1006) through bipm_solve_reduced.
+        Returns (step dict, info dict, delta_w_last)."""
+        keep, a = self._augmented(aug)
+        p, M = self.problem, self.hi - self.lo
+        out = {"px": np.zeros((M, p.n_x)), "pu": np.zeros(p.n_u), "ps": np.zeros((M, p.m)),
+               "pz": np.zeros((M, p.m)), "py": np.zeros((M, p.n_x))}
+        st = _Step(**{k: dptr(v) for k, v in out.items()})
+        r = _RegSchedule(**(reg or {}))
+        dwl = ctypes.c_double(delta_w_last)
+        info = _StepInfo()
+        check(lib().bipm_solve_reduced(self._h, ctypes.byref(a), ctypes.byref(r),
+                                       ctypes.byref(dwl), ctypes.byref(st), ctypes.byref(info)))
+        return out, {k: getattr(info, k) for k, _ in _StepInfo._fields_}, dwl.value
 
     def bundle_shapes(self):
         p, M = self.problem, self.hi - self.lo
@@ -344,6 +539,18 @@ class Solver:
         out["status_name"] = SOLVE_STATUS.get(r.status, str(r.status))
         out["u"] = u
         out["logs"] = [self.log(k) for k in range(r.iterations)]
+        return out
+
+    def iterate(self) -> dict:
+        """The current primal-dual point (Iterate, model.hpp:41-55)."""
+        p, M = self.ctx.problem, self.ctx.hi - self.ctx.lo
+        shapes = {"x": (M, p.n_x), "y": (M, p.n_x), "kappa_lo": (M, p.n_x),
+                  "kappa_up": (M, p.n_x), "s": (M, p.m), "z": (M, p.m), "nu_lo": (M, p.m),
+                  "nu_up": (M, p.m), "u": (p.n_u,), "lambda_lo": (p.n_u,),
+                  "lambda_up": (p.n_u,)}
+        out = {k: np.zeros(shapes[k]) for k in ITERATE_FIELDS}
+        it = _Iterate(**{k: dptr(v) for k, v in out.items()})
+        check(lib().bipm_solver_iterate(self._h, ctypes.byref(it)))
         return out
 
     def log(self, k: int) -> dict:

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "engine/engine.hpp"
+#include "engine/kkt_step.hpp"
 #include "engine/solver.hpp"
 
 using namespace bipm;
@@ -20,6 +21,11 @@ struct bipm_problem {
 struct bipm_ctx {
   const bipm_problem* prob = nullptr;
   std::unique_ptr<Engine> eng;
+  std::unique_ptr<KktStep> kkt;  // operator-level solve_reduced state (created on first use)
+  KktStep& step_op() {
+    if (!kkt) kkt = std::make_unique<KktStep>(*eng);
+    return *kkt;
+  }
 };
 
 struct bipm_solver {
@@ -30,14 +36,17 @@ struct bipm_solver {
 namespace {
 
 thread_local std::string g_err;
+thread_local int32_t g_err_block = -1;
 
 template <typename F>
 int guarded(F&& f) {
   try {
+    g_err_block = -1;
     f();
     return BIPM_OK;
   } catch (const Error& e) {
     g_err = e.what();
+    g_err_block = e.block;
     return e.code;
   } catch (const std::exception& e) {
     g_err = e.what();
@@ -108,9 +117,14 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
 
 }  // namespace
 
+namespace {
+void upload_condensed(Engine& e, const bipm_condensed* in);
+}
+
 extern "C" {
 
 const char* bipm_last_error(void) { return g_err.c_str(); }
+int32_t bipm_last_error_block(void) { return g_err_block; }
 int bipm_version(void) { return 1; }
 
 int bipm_problem_create(const char* case_path, int32_t N, double sigma, uint64_t seed,
@@ -119,6 +133,119 @@ int bipm_problem_create(const char* case_path, int32_t N, double sigma, uint64_t
     if (!case_path || !out) throw Error(kInvalidArgument, "null argument");
     auto bp = std::make_unique<bipm_problem>();
     bp->p = Problem::from_case_file(case_path, N, sigma, seed);
+    *out = bp.release();
+  });
+}
+
+int bipm_problem_create_ex(const char* case_path, int32_t N, double sigma, uint64_t seed,
+                           const int32_t* contingencies, int32_t n_contingencies,
+                           bipm_problem** out) {
+  return guarded([&] {
+    if (!case_path || !out || n_contingencies < 0 || (n_contingencies > 0 && !contingencies))
+      throw Error(kInvalidArgument, "null argument");
+    auto bp = std::make_unique<bipm_problem>();
+    bp->p = Problem::from_case_file(
+        case_path, N, sigma, seed,
+        std::vector<idx>(contingencies, contingencies + n_contingencies));
+    *out = bp.release();
+  });
+}
+
+int bipm_problem_create_tables(const bipm_case_tables* t, const bipm_scenario_tables* sc,
+                               bipm_problem** out) {
+  return guarded([&] {
+    if (!t || !sc || !out) throw Error(kInvalidArgument, "null argument");
+    if (t->nbus < 1 || t->ngen < 1 || t->nbranch < 1 || !t->bus || !t->gen || !t->branch)
+      throw Error(kInvalidArgument, "case tables: need buses, generators and branches");
+    GridCase cs;
+    cs.name = t->name ? t->name : "tables";
+    cs.baseMVA = t->base_mva;
+    for (int32_t i = 0; i < t->nbus; ++i) {
+      const double* r = t->bus + size_t(i) * BIPM_BUS_COLS;
+      CaseBus b;
+      b.id = int(r[0]);
+      b.type = int(r[1]);
+      b.Pd = r[2], b.Qd = r[3], b.Gs = r[4], b.Bs = r[5], b.Vm = r[6], b.Va = r[7];
+      b.Vmax = r[8], b.Vmin = r[9];
+      cs.bus.push_back(b);
+    }
+    for (int32_t i = 0; i < t->ngen; ++i) {
+      const double* r = t->gen + size_t(i) * BIPM_GEN_COLS;
+      CaseGen g;
+      g.bus = int(r[0]);
+      g.Pg = r[1], g.Qg = r[2], g.Qmax = r[3], g.Qmin = r[4], g.Vg = r[5];
+      g.status = int(r[6]);
+      g.Pmax = r[7], g.Pmin = r[8];
+      cs.gen.push_back(g);
+    }
+    for (int32_t i = 0; i < t->nbranch; ++i) {
+      const double* r = t->branch + size_t(i) * BIPM_BRANCH_COLS;
+      CaseBranch l;
+      l.from = int(r[0]);
+      l.to = int(r[1]);
+      l.r = r[2], l.x = r[3], l.b = r[4], l.rateA = r[5], l.tap = r[6], l.shift = r[7];
+      l.status = int(r[8]);
+      cs.branch.push_back(l);
+    }
+    if (t->ngencost > 0) {
+      if (!t->gencost || !t->gencost_coef || t->ngencost != t->ngen)
+        throw Error(kInvalidArgument, "case tables: one gencost row per generator");
+      size_t off = 0;
+      for (int32_t i = 0; i < t->ngencost; ++i) {
+        const double* r = t->gencost + size_t(i) * BIPM_GENCOST_COLS;
+        CaseCost c;
+        c.model = int(r[0]);
+        c.ncost = int(r[3]);
+        if (c.model != 2 || c.ncost < 0 || c.ncost > 3)
+          throw Error(kInvalidArgument, "case tables: polynomial costs of degree <= 2 only");
+        c.coef.assign(t->gencost_coef + off, t->gencost_coef + off + c.ncost);
+        off += size_t(c.ncost);
+        cs.cost.push_back(c);
+      }
+    }
+    (void)cs.ref_bus();  // exactly one reference bus (throws otherwise)
+    if (sc->N < 1 || !sc->multipliers) throw Error(kInvalidArgument, "scenarios: need N >= 1");
+    ScenarioDraw d;
+    d.N = sc->N;
+    d.sigma = sc->sigma;
+    d.seed = sc->seed;
+    d.mult.assign(sc->multipliers, sc->multipliers + size_t(sc->N) * size_t(t->nbus));
+    d.outages.assign(size_t(sc->N), {});
+    if (sc->outage_ptr) {
+      for (int32_t s = 0; s < sc->N; ++s)
+        for (int32_t k = sc->outage_ptr[s]; k < sc->outage_ptr[s + 1]; ++k) {
+          const int32_t l = sc->outage_branch[k];
+          if (l < 0 || l >= t->nbranch || !cs.branch[size_t(l)].status)
+            throw Error(kInvalidArgument, "scenario outage names an unknown or out-of-service branch");
+          d.outages[size_t(s)].push_back(l);
+        }
+    }
+    auto bp = std::make_unique<bipm_problem>();
+    bp->p = Problem::from_parts(std::move(cs), std::move(d));
+    *out = bp.release();
+  });
+}
+
+int bipm_problem_create_patterns(int32_t N, const bipm_csr* gx, const bipm_csr* gu,
+                                 const bipm_csr* hx, const bipm_csr* hu, const bipm_csr* wxx,
+                                 const bipm_csr* wxu, const bipm_csr* wuu, bipm_problem** out) {
+  return guarded([&] {
+    if (!gx || !gu || !hx || !hu || !wxx || !wxu || !wuu || !out)
+      throw Error(kInvalidArgument, "null argument");
+    auto csr = [](const bipm_csr* c) {
+      if (c->rows < 0 || c->cols < 0 || !c->row_ptr)
+        throw Error(kInvalidArgument, "pattern: bad shape");
+      Csr r;
+      r.rows = c->rows;
+      r.cols = c->cols;
+      r.ptr.assign(c->row_ptr, c->row_ptr + c->rows + 1);
+      if (r.ptr.back() > 0 && !c->col_ind) throw Error(kInvalidArgument, "pattern: null col_ind");
+      r.ind.assign(c->col_ind, c->col_ind + r.ptr.back());
+      return r;
+    };
+    auto bp = std::make_unique<bipm_problem>();
+    bp->p = Problem::from_patterns(N, csr(gx), csr(gu), csr(hx), csr(hu), csr(wxx), csr(wxu),
+                                   csr(wuu));
     *out = bp.release();
   });
 }
@@ -157,7 +284,7 @@ void bipm_ctx_destroy(bipm_ctx* c) { delete c; }
 int bipm_factor_gx(bipm_ctx* c, const double* gx, int32_t* singular_block) {
   return guarded([&] {
     Engine& e = *c->eng;
-    e.bd().gx.upload(gx, e.bd().gx.size(), e.st);
+    e.bd().gx.copy_from(gx, e.bd().gx.size(), e.st);
     const idx bad = e.factor_gx();
     if (singular_block) *singular_block = bad;
     if (bad >= 0) throw Error(kSingularBlock, "singular block " + std::to_string(bad), bad);
@@ -168,15 +295,7 @@ int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* k
                 double* rhs) {
   return guarded([&] {
     Engine& e = *c->eng;
-    e.bd().gu.upload(in->gu, e.bd().gu.size(), e.st);
-    e.kxx.upload(in->kxx, e.kxx.size(), e.st);
-    e.kxu.upload(in->kxu, e.kxu.size(), e.st);
-    e.kuu.upload(in->kuu, e.kuu.size(), e.st);
-    e.sigma_x.upload(in->sigma_x, e.sigma_x.size(), e.st);
-    e.rhat1.upload(in->rhat1, e.rhat1.size(), e.st);
-    e.rhat3.upload(in->rhat3, e.rhat3.size(), e.st);
-    e.sigma_u.upload(in->sigma_u, e.sigma_u.size(), e.st);
-    e.rhat2.upload(in->rhat2, e.rhat2.size(), e.st);
+    upload_condensed(e, in);
     e.reduce_local(delta_w);
     e.finish_reduce(delta_w);
     e.reduce_rhs_local(delta_w, e.rhs.get());
@@ -186,6 +305,155 @@ int bipm_reduce(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* k
     e.khat.download(khat, e.khat.size(), e.st);
     e.sync();
     for (size_t i = 0; i < r.size(); ++i) rhs[i] = r[i] - in->rhat2[i];
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+void upload_condensed(Engine& e, const bipm_condensed* in) {
+  if (!in || !in->gu || !in->kxx || !in->kxu || !in->kuu || !in->sigma_x || !in->rhat1 ||
+      !in->rhat3 || !in->sigma_u || !in->rhat2)
+    throw Error(kInvalidArgument, "condensed system: null array");
+  const size_t Ms = size_t(e.M), nx = Ms * size_t(e.pb.M.n_x);
+  const DerivPlan& D = e.pb.D;
+  e.bd().gu.copy_from(in->gu, Ms * size_t(D.g.u.nnz()), e.st);
+  e.kxx.copy_from(in->kxx, Ms * size_t(D.kxx.out.nnz()), e.st);
+  e.kxu.copy_from(in->kxu, Ms * size_t(D.kxu.out.nnz()), e.st);
+  e.kuu.copy_from(in->kuu, Ms * size_t(D.kuu.out.nnz()), e.st);
+  e.sigma_x.copy_from(in->sigma_x, nx, e.st);
+  e.rhat1.copy_from(in->rhat1, nx, e.st);
+  e.rhat3.copy_from(in->rhat3, nx, e.st);
+  e.sigma_u.copy_from(in->sigma_u, size_t(e.pb.M.n_u), e.st);
+  e.rhat2.copy_from(in->rhat2, size_t(e.pb.M.n_u), e.st);
+}
+
+// the augmented system (and the bundle blocks it references) into the engine
+// and the KKT step; NonInterior when a Sigma_s entry is not positive, as
+// condense does (kkt.cpp:138-141)
+void upload_augmented(Engine& e, KktStep& k, const bipm_augmented* a) {
+  if (!a || !a->gx || !a->gu || !a->hx || !a->hu || !a->wxx || !a->wxu || !a->wuu ||
+      !a->sigma_x || !a->r1x || !a->r3 || !a->sigma_s || !a->r2 || !a->r4 || !a->sigma_u ||
+      !a->r1u)
+    throw Error(kInvalidArgument, "augmented system: null array");
+  const size_t nm = size_t(e.M) * size_t(e.pb.M.m);
+  for (size_t i = 0; i < nm; ++i)
+    if (!(a->sigma_s[i] > 0))
+      throw Error(kNonInterior, "condense: Sigma_s not positive (zero slack gap)",
+                  e.lo + idx(i / size_t(std::max(1, e.pb.M.m))));
+  Engine::Bundle& b = e.bd();
+  const size_t nx = size_t(e.M) * size_t(e.pb.M.n_x);
+  b.gx.copy_from(a->gx, b.gx.size(), e.st);
+  b.gu.copy_from(a->gu, b.gu.size(), e.st);
+  b.hx.copy_from(a->hx, b.hx.size(), e.st);
+  b.hu.copy_from(a->hu, b.hu.size(), e.st);
+  b.wxx.copy_from(a->wxx, b.wxx.size(), e.st);
+  b.wxu.copy_from(a->wxu, b.wxu.size(), e.st);
+  b.wuu.copy_from(a->wuu, b.wuu.size(), e.st);
+  b.g.copy_from(a->r3, b.g.size(), e.st);
+  e.sigma_x.copy_from(a->sigma_x, nx, e.st);
+  e.sigma_s.copy_from(a->sigma_s, nm, e.st);
+  e.r2.copy_from(a->r2, nm, e.st);
+  e.r4.copy_from(a->r4, nm, e.st);
+  e.sigma_u.copy_from(a->sigma_u, size_t(e.pb.M.n_u), e.st);
+  k.r1x.copy_from(a->r1x, nx, e.st);
+  k.r1u.copy_from(a->r1u, size_t(e.pb.M.n_u), e.st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bipm_condense(bipm_ctx* c, const bipm_augmented* a, const bipm_condensed_out* out) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    KktStep& k = c->step_op();
+    upload_augmented(e, k, a);
+    k.condense();
+    if (out) {
+      auto dl = [&](const DArr<double>& v, double* dst, size_t n) {
+        if (dst) v.download(dst, n, e.st);
+      };
+      dl(e.kxx, out->kxx, size_t(e.M) * size_t(e.pb.D.kxx.out.nnz()));
+      dl(e.kxu, out->kxu, e.kxu.size());
+      dl(e.kuu, out->kuu, e.kuu.size());
+      dl(e.rhat1, out->rhat1, e.rhat1.size());
+      dl(e.rhat2, out->rhat2, e.rhat2.size());
+      dl(e.rhat3, out->rhat3, e.rhat3.size());
+    }
+    e.sync();
+  });
+}
+
+int bipm_reduce_rhs(bipm_ctx* c, const bipm_condensed* in, double delta_w, double* rhs) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    if (!rhs) throw Error(kInvalidArgument, "null argument");
+    upload_condensed(e, in);
+    e.reduce_rhs_local(delta_w, e.rhs.get());
+    e.rhs.download(rhs, e.rhs.size(), e.st);
+    e.sync();
+  });
+}
+
+int bipm_recover(bipm_ctx* c, const bipm_condensed* in, const bipm_slack_rows* sr,
+                 double delta_w, const double* pu, double* px, double* py, double* pz,
+                 double* ps) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    if (!sr || !sr->hx || !sr->hu || !sr->sigma_s || !sr->r2 || !sr->r4 || !pu || !px || !py ||
+        !pz || !ps)
+      throw Error(kInvalidArgument, "null argument");
+    upload_condensed(e, in);
+    e.bd().hx.copy_from(sr->hx, e.bd().hx.size(), e.st);
+    e.bd().hu.copy_from(sr->hu, e.bd().hu.size(), e.st);
+    e.sigma_s.copy_from(sr->sigma_s, e.sigma_s.size(), e.st);
+    e.r2.copy_from(sr->r2, e.r2.size(), e.st);
+    e.r4.copy_from(sr->r4, e.r4.size(), e.st);
+    const OpfModel& M = e.pb.M;
+    const size_t nx = size_t(e.M) * M.n_x, nm = size_t(e.M) * M.m;
+    DArr<double> dpu, dpx(nx), dpy(nx), dpz(nm), dps(nm);
+    dpu.upload(pu, size_t(M.n_u), e.st);
+    e.recover(delta_w, dpu.get(), dpx.get(), dpy.get(), dpz.get(), dps.get());
+    dpx.download(px, nx, e.st);
+    dpy.download(py, nx, e.st);
+    dpz.download(pz, nm, e.st);
+    dps.download(ps, nm, e.st);
+    e.sync();
+  });
+}
+
+int bipm_solve_reduced(bipm_ctx* c, const bipm_augmented* a, const bipm_reg_schedule* reg,
+                       double* delta_w_last, const bipm_step* out, bipm_step_info* info) {
+  return guarded([&] {
+    Engine& e = *c->eng;
+    if (!delta_w_last || !out) throw Error(kInvalidArgument, "null argument");
+    KktStep& k = c->step_op();
+    RegOptions r;
+    if (reg) {
+      if (reg->delta_w0 > 0) r.delta_w0 = reg->delta_w0;
+      if (reg->delta_w_min > 0) r.delta_w_min = reg->delta_w_min;
+      if (reg->delta_w_max > 0) r.delta_w_max = reg->delta_w_max;
+      if (reg->kappa_minus > 0) r.kappa_minus = reg->kappa_minus;
+      if (reg->kappa_plus > 0) r.kappa_plus = reg->kappa_plus;
+      if (reg->kappa_plus_emergency > 0) r.kappa_plus_emergency = reg->kappa_plus_emergency;
+    }
+    upload_augmented(e, k, a);
+    k.condense();
+    k.factor_launch();
+    k.check_factor(nullptr);
+    k.solve(*delta_w_last, r);
+    double* dst[5] = {out->px, out->pu, out->ps, out->pz, out->py};
+    for (int j = 0; j < 5; ++j)
+      if (dst[j]) k.p[j].download(dst[j], k.p[j].size(), e.st);
+    e.sync();
+    if (info) {
+      info->delta_w = k.last_dw;
+      info->corrections = k.corrections;
+      info->refinements = k.refinements;
+      info->reductions = k.reductions;
+    }
   });
 }
 
@@ -293,6 +561,16 @@ int bipm_solver_step(bipm_solver* s, int32_t* status) {
 
 int bipm_solver_result(bipm_solver* s, bipm_solve_result* r, double* u) {
   return guarded([&] { fill_result(*s->s, r, u); });
+}
+
+int bipm_solver_iterate(bipm_solver* s, const bipm_iterate* out) {
+  return guarded([&] {
+    if (!out) throw Error(kInvalidArgument, "null argument");
+    double* const dst[11] = {out->x,        out->u,        out->s,     out->y,
+                             out->z,        out->kappa_lo, out->kappa_up, out->nu_lo,
+                             out->nu_up,    out->lambda_lo, out->lambda_up};
+    s->s->host_iterate(dst);
+  });
 }
 
 int bipm_solver_log(bipm_solver* s, int32_t k, double rec[15]) {

@@ -51,6 +51,13 @@ class DArr {
     if (n_) cuda_check(cudaMemcpyAsync(p_, src, n_ * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
     stats().h2d_bytes += (long long)(n_ * sizeof(T));
   }
+  // copy n <= size() elements into the front of the array (keeps its size:
+  // some arrays carry alignment padding past their logical length)
+  void copy_from(const T* src, size_t n, cudaStream_t st) {
+    if (n > n_) throw std::runtime_error("copy_from: source longer than the array");
+    if (n) cuda_check(cudaMemcpyAsync(p_, src, n * sizeof(T), cudaMemcpyHostToDevice, st), "upload");
+    stats().h2d_bytes += (long long)(n * sizeof(T));
+  }
   void download(T* dst, size_t n, cudaStream_t st) const {
     if (n) cuda_check(cudaMemcpyAsync(dst, p_, n * sizeof(T), cudaMemcpyDeviceToHost, st), "download");
     stats().d2h_bytes += (long long)(n * sizeof(T));

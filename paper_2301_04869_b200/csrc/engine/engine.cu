@@ -19,10 +19,56 @@ std::unique_ptr<Problem> Problem::from_parts(GridCase cs, ScenarioDraw sc) {
 }
 
 std::unique_ptr<Problem> Problem::from_case_file(const std::string& path, idx N, double sigma,
-                                                 std::uint64_t seed) {
+                                                 std::uint64_t seed,
+                                                 const std::vector<idx>& contingencies) {
   GridCase cs = read_matpower_file(path);
-  ScenarioDraw sc = draw_scenarios(cs, N, sigma, {}, seed);
+  ScenarioDraw sc = draw_scenarios(cs, N, sigma, contingencies, seed);
   return from_parts(std::move(cs), std::move(sc));
+}
+
+std::unique_ptr<Problem> Problem::from_patterns(idx N, Csr gx, Csr gu, Csr hx, Csr hu, Csr wxx,
+                                                Csr wxu, Csr wuu) {
+  const idx n_x = gx.rows, n_u = gu.cols, m = hx.rows;
+  auto need = [](bool ok, const char* what) {
+    if (!ok) throw Error(kInvalidArgument, std::string("patterns: ") + what);
+  };
+  need(N >= 1 && n_x >= 1 && n_u >= 1, "need N, n_x, n_u >= 1");
+  need(gx.cols == n_x && gu.rows == n_x, "G_x must be n_x x n_x and G_u n_x x n_u");
+  need(hu.rows == m && hx.cols == n_x && hu.cols == n_u, "H_x / H_u shapes");
+  need(wxx.rows == n_x && wxx.cols == n_x && wxu.rows == n_x && wxu.cols == n_u &&
+           wuu.rows == n_u && wuu.cols == n_u,
+       "W_xx / W_xu / W_uu shapes");
+  for (const Csr* c : {&gx, &gu, &hx, &hu, &wxx, &wxu, &wuu}) {
+    need(c->ptr.size() == size_t(c->rows) + 1 && c->ptr.front() == 0 &&
+             c->ptr.back() == c->nnz(),
+         "row pointers");
+    for (idx i = 0; i < c->rows; ++i)
+      for (idx k = c->ptr[size_t(i)]; k < c->ptr[size_t(i) + 1]; ++k)
+        need(c->ind[size_t(k)] >= 0 && c->ind[size_t(k)] < c->cols &&
+                 (k == c->ptr[size_t(i)] || c->ind[size_t(k)] > c->ind[size_t(k) - 1]),
+             "column indices must be in range and strictly increasing per row");
+  }
+  auto p = std::make_unique<Problem>();
+  p->model = false;
+  p->M.N = N;
+  p->M.n_x = n_x;
+  p->M.n_u = n_u;
+  p->M.m = m;
+  p->M.name = "patterns";
+  DerivPlan& D = p->D;
+  D.g.x = std::move(gx);
+  D.g.u = std::move(gu);
+  D.h.x = std::move(hx);
+  D.h.u = std::move(hu);
+  D.wxx = std::move(wxx);
+  D.wxu = std::move(wxu);
+  D.wuu = std::move(wuu);
+  // the reference's make_condense_work (kkt.cpp:111-117)
+  D.kxx = plan_condense_program(D.wxx, D.h.x, D.h.x);
+  D.kxu = plan_condense_program(D.wxu, D.h.x, D.h.u);
+  D.kuu = plan_condense_program(D.wuu, D.h.u, D.h.u);
+  p->LU = make_lu_plan(D.g.x);
+  return p;
 }
 
 void DevPattern::upload(const Csr& p) {
@@ -166,7 +212,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
     b.wuu.resize(Ms * nnz(D.wuu));
     b.grad.resize(Ms * size_t(Mo.n_d()));
   }
-  upload_ad();
+  if (pb.has_model()) upload_ad();
   // +2: the streamed reduction's bulk copies start on a 16-byte boundary
   kxx.resize(Ms * nnz(D.kxx.out) + 2);
   kxu.resize(Ms * nnz(D.kxu.out));
@@ -685,6 +731,8 @@ void Engine::upload_ad() {
 
 idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const double* dY,
                         const double* dZ, double obj_w, bool check) {
+  if (!pb.has_model())
+    throw Error(kInvalidArgument, "eval_bundle: the problem was built from patterns only");
   AdBuffers b{};
   b.X = dX;
   b.u = du;
@@ -714,6 +762,8 @@ idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const d
 
 idx Engine::eval_values(const double* dX, const double* du, double* df, double* dg,
                         double* dh) {
+  if (!pb.has_model())
+    throw Error(kInvalidArgument, "eval_values: the problem was built from patterns only");
   AdBuffers b{};
   b.X = dX;
   b.u = du;

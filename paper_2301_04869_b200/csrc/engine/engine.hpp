@@ -24,17 +24,31 @@
 
 namespace bipm {
 
+// Host model + symbolic plans.  Two ways in:
+//  * from an OPF case (file or the reference's CaseData / ScenarioSet tables):
+//    everything, including the basis kernel's data the AD needs;
+//  * from the derivative patterns alone (from_patterns): the KKT operators
+//    only (condense, refactor, reduce, recover, solve_reduced) -- what a
+//    reference solve needs when its own AD and IPM call the GPU for
+//    solve_reduced.
 struct Problem {
   GridCase cs;
   ScenarioDraw sc;
-  OpfModel M;
+  OpfModel M;  // dims only when built from patterns
   LaneDeps deps;
   DerivPlan D;
   LuPlan LU;
   AdProgram AD;
+  bool model = true;
+  bool has_model() const { return model; }
   static std::unique_ptr<Problem> from_case_file(const std::string& path, idx N, double sigma,
-                                                 std::uint64_t seed);
+                                                 std::uint64_t seed,
+                                                 const std::vector<idx>& contingencies = {});
   static std::unique_ptr<Problem> from_parts(GridCase cs, ScenarioDraw sc);
+  // N scenarios sharing G_x | G_u (n_x x n_x | n_x x n_u), H_x | H_u (m x .)
+  // and the Lagrangian Hessian blocks W_xx, W_xu, W_uu
+  static std::unique_ptr<Problem> from_patterns(idx N, Csr gx, Csr gu, Csr hx, Csr hu, Csr wxx,
+                                                Csr wxu, Csr wuu);
 };
 
 struct DevPattern {

@@ -28,8 +28,13 @@ DevIter Solver::IterStore::view() {
                  kup.get(), nlo.get(), nup.get(), llo.get(), lup.get()};
 }
 
-Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
+Solver::Solver(Engine& eng, const SolverOptions& opt)
+    : e(eng), o(opt), io(eng), kkt(eng, opt.refine_rounds) {
   const OpfModel& M = e.pb.M;
+  if (!e.pb.has_model())
+    throw Error(kInvalidArgument,
+                "the interior-point driver needs the OPF model (a problem built from patterns "
+                "only serves the KKT operators)");
   d = IpmDims{e.M, M.n_x, M.n_u, M.m, M.n_d()};
   xlo.upload(M.x_lo);
   xup.upload(M.x_up);
@@ -44,35 +49,13 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
     for (DArr<double>* a : {&s.s, &s.z, &s.nlo, &s.nup}) a->resize(nm);
     for (DArr<double>* a : {&s.u, &s.llo, &s.lup}) a->resize(nu);
   }
-  for (DArr<double>* s : {p, q}) {
-    s[0].resize(nx);
-    s[1].resize(nu);
-    s[2].resize(nm);
-    s[3].resize(nm);
-    s[4].resize(nx);
-  }
   bsv[0].resize(nx);
   bsv[1].resize(nx);
   bsv[2].resize(nm);
   bsv[3].resize(nm);
   bsv[4].resize(nu);
   bsv[5].resize(nu);
-  r1x.resize(nx);
-  r1u.resize(nu);
   gsum_u.resize(nu);
-  rhat2_part.resize(size_t(d.M) * nu);
-  o1x.resize(nx);
-  o1u.resize(nu);
-  o2.resize(nm);
-  o3.resize(nx);
-  o4.resize(nm);
-  o1u_part.resize(size_t(d.M) * nu * 2);
-  c_rhat1.resize(nx);
-  c_rhat2.resize(nu);
-  rhs_sum.resize(nu);
-  pu_rhs.resize(nu);
-  red_u.resize(nu);
-  dd_u.resize(2 * nu);
   ft.resize(size_t(d.M));
   gt.resize(nx);
   ht.resize(nm);
@@ -81,7 +64,6 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
   flag.resize(1);
   eval_counter.resize(1);
   eval_counter.zero(e.st);
-  cuda_check(cudaMallocHost(&pinned, 64 * sizeof(double)), "cudaMallocHost");
   // multiplier count of the scaled error (ipm.cpp:345-379): structural
   double fin_x = 0, fin_s = 0, fin_u = 0;
   for (idx i = 0; i < M.n_x; ++i) fin_x += std::isfinite(M.x_lo[size_t(i)]) + std::isfinite(M.x_up[size_t(i)]);
@@ -93,41 +75,6 @@ Solver::Solver(Engine& eng, const SolverOptions& opt) : e(eng), o(opt) {
 
 double Solver::now() const {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
-
-template <int K>
-std::array<double, K> Solver::fetch(const double* dptr) {
-  cuda_check(cudaMemcpyAsync(pinned, dptr, K * sizeof(double), cudaMemcpyDeviceToHost, e.st),
-             "fetch");
-  stats().d2h_bytes += K * (long long)sizeof(double);
-  e.sync();
-  std::array<double, K> r;
-  std::copy(pinned, pinned + K, r.begin());
-  return r;
-}
-
-double Solver::fetch1(const double* dptr) { return fetch<1>(dptr)[0]; }
-
-void Solver::allred(double* dptr, size_t n, RedOpKind op) {
-  if (e.multi()) e.comm->allreduce(dptr, n, op, e.st);
-}
-
-double Solver::host_all(double v, RedOpKind op) {
-  if (!e.multi()) return v;
-  double* slot = scal.get() + 30;
-  cuda_check(cudaMemcpyAsync(slot, &v, sizeof(double), cudaMemcpyHostToDevice, e.st), "h2d");
-  e.comm->allreduce(slot, 1, op, e.st);
-  return fetch1(slot);
-}
-
-idx Solver::global_first_bad(idx local_bad) {
-  if (!e.multi()) return local_bad;
-  const double v = host_all(local_bad >= 0 ? double(local_bad) : 1e300, RedOpKind::kMin);
-  return v < 1e299 ? idx(v) : -1;
-}
-
-DevStep Solver::step_view(DArr<double>* s) {
-  return DevStep{s[0].get(), s[1].get(), s[2].get(), s[3].get(), s[4].get()};
 }
 
 Solver::ErrEval Solver::kkt_eval(const DevIter& it, Engine::Bundle& bd, const double mus[4],
@@ -181,10 +128,11 @@ void Solver::start() {
   icur = 0;
   IterStore& s = its[0];
   DArr<double> dx0;
-  dx0.upload(x0);
-  s.u.upload(u0);
-  s.llo.upload(llo);
-  s.lup.upload(lup);
+  // stream-ordered: kernels of an earlier solve may still use these buffers
+  dx0.upload(x0.data(), x0.size(), e.st);
+  s.u.upload(u0.data(), u0.size(), e.st);
+  s.llo.upload(llo.data(), llo.size(), e.st);
+  s.lup.upload(lup.data(), lup.size(), e.st);
   launch_init_x(d, cur(), b, dx0.get(), o.mu0, e.st);
   if (d.m > 0) {
     const idx bad = global_first_bad(e.eval_values(s.x.get(), s.u.get(), ft.get(), gt.get(), ht.get()));
@@ -202,147 +150,24 @@ void Solver::start() {
   t0_ = std::chrono::steady_clock::now();
 }
 
-bool Solver::attempt(double dw, const DevIter& it) {
-  (void)it;
-  Engine::Bundle& bd = e.bd();
-  ++reductions;
-  // the rhs reduction only reads the factors and the condensed blocks: it runs
-  // on a side stream beside the Schur reduction (filling the SMs of its last
-  // wave) and joins before the rhs is used
-  e.reduce_rhs_fork(dw, rhs_sum.get());
-  e.reduce_local(dw);
-  e.finish_reduce(dw);
-  e.reduce_rhs_join(rhs_sum.get());
-  // refinement scale (independent of the factor) rides on the Cholesky sync
-  launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
-                   scal.get() + 20, e.st);
-  allred(scal.get() + 20, 1, RedOpKind::kMax);
-  cudaMemcpyAsync(pinned + 40, scal.get() + 20, sizeof(double), cudaMemcpyDeviceToHost, e.st);
-  if (!e.factor_khat()) return false;
-  const double scale = pinned[40];
-  // solve_with(c, first_sum): p_u, then state/adjoint and slack/dual recovery
-  launch_pu_rhs(d.n_u, rhs_sum.get(), e.rhat2.get(), p[1].get(), true, e.st);
-  e.solve_khat(p[1].get());
-  e.recover(dw, p[1].get(), p[0].get(), p[4].get(), p[3].get(), p[2].get());
-  // refinement against the unreduced augmented system (kkt.cpp:988-999)
-  const DerivPlan& D = e.pb.D;
-  (void)D;
-  for (int round = 0; round < o.refine_rounds; ++round) {
-    AugResidualArgs a{};
-    a.d = d;
-    a.gx = e.gx_p.v;
-    a.gu = e.gu_p.v;
-    a.hx = e.hx_p.v;
-    a.hu = e.hu_p.v;
-    a.wxx = e.wxx_p.v;
-    a.wxu = e.wxu_p.v;
-    a.wuu = e.wuu_p.v;
-    a.gx_v = bd.gx.get();
-    a.gu_v = bd.gu.get();
-    a.hx_v = bd.hx.get();
-    a.hu_v = bd.hu.get();
-    a.wxx_v = bd.wxx.get();
-    a.wxu_v = bd.wxu.get();
-    a.wuu_v = bd.wuu.get();
-    a.sigma_x = e.sigma_x.get();
-    a.sigma_s = e.sigma_s.get();
-    a.sigma_u = e.sigma_u.get();
-    a.r1x = r1x.get();
-    a.r1u = r1u.get();
-    a.r2 = e.r2.get();
-    a.r3 = bd.g.get();
-    a.r4 = e.r4.get();
-    a.p = step_view(p);
-    a.dw = dw;
-    a.o1x = o1x.get();
-    a.o2 = o2.get();
-    a.o3 = o3.get();
-    a.o4 = o4.get();
-    a.o1u_part = o1u_part.get();
-    launch_aug_residual(a, partial.get(), scal.get() + 21, e.st);
-    if (e.multi()) {
-      allred(scal.get() + 21, 1, RedOpKind::kMax);
-      launch_aug_residual_u_local(a, dd_u.get(), e.st);
-      allred(dd_u.get(), 2 * size_t(d.n_u), RedOpKind::kSum);
-      launch_aug_residual_u_finish(a, dd_u.get(), o1u.get(), scal.get() + 22, e.st);
-    } else {
-      launch_aug_residual_u(a, dd_u.get(), o1u.get(), scal.get() + 22, e.st);
-    }
-    const auto v = fetch<2>(scal.get() + 21);
-    const double rel = std::max(v[0], v[1]) / scale;
-    if (rel <= 1e-12) break;
-    ++refinements;
-    // substitute_rhs (kkt.cpp:342-358): re-condense only the rhs from rho
-    launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
-                         o4.get(), o2.get(), o1x.get(), c_rhat1.get(), rhat2_part.get(), e.st);
-    condensed_u_sum(rhat2_part.get(), o1u.get(), c_rhat2.get());
-    e.reduce_rhs_local(dw, rhs_sum.get(), c_rhat1.get(), o3.get());
-    launch_pu_rhs(d.n_u, rhs_sum.get(), c_rhat2.get(), q[1].get(), false, e.st);
-    e.solve_khat(q[1].get());
-    e.recover(dw, q[1].get(), q[0].get(), q[4].get(), q[3].get(), q[2].get(), c_rhat1.get(),
-              o3.get(), o2.get(), o4.get());
-    launch_axpy_step(d, step_view(p), step_view(q), e.st);
-  }
-  return true;
-}
-
 void Solver::compute_step(const DevIter& it) {
   Engine::Bundle& bd = e.bd();
   flag.zero(e.st);
   launch_grad_u_sum(d, bd.grad.get(), gsum_u.get(), e.st);
   allred(gsum_u.get(), size_t(d.n_u), RedOpKind::kSum);
-  launch_assemble_xs(d, it, b, bd.grad.get(), bd.h.get(), mu, e.sigma_x.get(), r1x.get(),
+  launch_assemble_xs(d, it, b, bd.grad.get(), bd.h.get(), mu, e.sigma_x.get(), kkt.r1x.get(),
                      e.sigma_s.get(), e.r2.get(), e.r4.get(), flag.get(), e.st);
-  launch_assemble_u(d, it, b, gsum_u.get(), mu, e.sigma_u.get(), r1u.get(), flag.get(), e.st);
-  cuda_check(cudaMemcpyAsync(e.rhat3.get(), bd.g.get(), e.rhat3.size() * sizeof(double),
-                             cudaMemcpyDeviceToDevice, e.st),
-             "rhat3");
-  e.condense_blocks();
-  launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
-                       e.r4.get(), e.r2.get(), r1x.get(), e.rhat1.get(), rhat2_part.get(), e.st);
-  condensed_u_sum(rhat2_part.get(), r1u.get(), e.rhat2.get());
-  e.factor_gx_launch();
-  // one round trip for the interiority flag and the refactor statuses
-  std::vector<int> st_host(static_cast<size_t>(d.M) + 1);
-  flag.download(st_host.data(), 1, e.st);
-  e.lu_status.download(st_host.data() + 1, size_t(d.M), e.st);
-  e.sync();
-  if (host_all(double(st_host[0]), RedOpKind::kMax) > 0)
-    throw Error(kNonInterior, "iterate not strictly interior");
-  idx local_sing = -1;
-  for (idx k = 0; k < d.M; ++k)
-    if (st_host[size_t(k) + 1]) {
-      local_sing = e.lo + k;
-      break;
-    }
-  const idx sing = global_first_bad(local_sing);
-  if (sing >= 0)
-    throw Error(kSingularBlock,
-                "singular block " + std::to_string(sing) +
-                    " (the reference falls back to the augmented strategy, which is not on the "
-                    "GPU path)",
-                sing);
-  corrections = 0;
-  refinements = 0;
-  double dw = 0.0;
-  if (!attempt(0.0, it)) {
-    dw = delta_w_last == 0 ? o.reg.delta_w0
-                           : std::max(o.reg.delta_w_min, delta_w_last * o.reg.kappa_minus);
-    for (;;) {
-      ++corrections;
-      if (attempt(dw, it)) {
-        delta_w_last = dw;
-        break;
-      }
-      dw *= delta_w_last == 0 ? o.reg.kappa_plus_emergency : o.reg.kappa_plus;
-      if (dw > o.reg.delta_w_max)
-        throw Error(kLinearSolve, "inertia correction: regularization budget exhausted");
-    }
-  }
-  last_dw = dw;
+  launch_assemble_u(d, it, b, gsum_u.get(), mu, e.sigma_u.get(), kkt.r1u.get(), flag.get(), e.st);
+  kkt.condense();
+  kkt.factor_launch();
+  kkt.check_factor(&flag);  // one round trip: interiority flag + refactor statuses
+  kkt.solve(delta_w_last, o.reg);
+  reductions = kkt.reductions;
 }
 
 int Solver::step() {
+  if (status == kNotStarted)
+    throw Error(kInvalidArgument, "solver: step() before start()");
   if (status != kRunning) return status;
   IterRecord log;
   log.iter = iter;
@@ -401,12 +226,12 @@ int Solver::step() {
   const double tk = now();
   compute_step(it);
   log.t_kkt = now() - tk;
-  log.corrections = corrections;
-  log.refinements = refinements;
-  log.delta_w = last_dw;
+  log.corrections = kkt.corrections;
+  log.refinements = kkt.refinements;
+  log.delta_w = kkt.last_dw;
 
   DevBoundStep bs{bsv[0].get(), bsv[1].get(), bsv[2].get(), bsv[3].get(), bsv[4].get(), bsv[5].get()};
-  const DevStep ps = step_view(p);
+  const DevStep ps = kkt.step_view();
   launch_bound_steps(d, it, b, ps, mu, o.tau, bs, partial.get(), scal.get(), e.st);
   allred(scal.get(), 2, RedOpKind::kMin);
   const auto caps = fetch<2>(scal.get());
@@ -442,7 +267,7 @@ int Solver::step() {
   allred(scal.get(), 1, RedOpKind::kSum);
   allred(scal.get() + 1, 2, RedOpKind::kMax);
   allred(scal.get() + 3, 5, RedOpKind::kSum);
-  launch_merit_u(d, it, b, p[1].get(), mu, scal.get() + 8, e.st);
+  launch_merit_u(d, it, b, ps.pu, mu, scal.get() + 8, e.st);
   const auto mv = fetch<10>(scal.get());
   const double viol0 = mv[0];
   const double penalty = 1.2 * std::max(mv[1], mv[2]) + 0.1;
@@ -505,29 +330,32 @@ double Solver::step_timed(int* st_out) {
   return ms;
 }
 
-// base + sum over scenarios of part (and over ranks when sharded)
-void Solver::condensed_u_sum(const double* part, const double* base, double* out) {
-  if (!e.multi()) {
-    launch_scenario_sum(d.M, d.n_u, part, base, out, e.st);
-    return;
-  }
-  launch_scenario_sum(d.M, d.n_u, part, nullptr, red_u.get(), e.st);
-  allred(red_u.get(), size_t(d.n_u), RedOpKind::kSum);
-  launch_scenario_sum(1, d.n_u, red_u.get(), base, out, e.st);
-}
-
 int Solver::solve() {
   start();
   while (status == kRunning) step();
   return status;
 }
 
-std::vector<double> Solver::host_u() const {
-  return const_cast<Solver*>(this)->its[icur].u.to_host();
+std::vector<double> Solver::host_u() {
+  std::vector<double> h(its[icur].u.size());
+  its[icur].u.download(h.data(), h.size(), e.st);
+  e.sync();
+  return h;
 }
 
-std::vector<double> Solver::host_x() const {
-  return const_cast<Solver*>(this)->its[icur].x.to_host();
+std::vector<double> Solver::host_x() {
+  std::vector<double> h(its[icur].x.size());
+  its[icur].x.download(h.data(), h.size(), e.st);
+  e.sync();
+  return h;
+}
+
+void Solver::host_iterate(double* const out[11]) {
+  IterStore& s = its[icur];
+  DArr<double>* a[11] = {&s.x, &s.u, &s.s, &s.y, &s.z, &s.klo, &s.kup, &s.nlo, &s.nup, &s.llo, &s.lup};
+  for (int k = 0; k < 11; ++k)
+    if (out[k]) a[k]->download(out[k], a[k]->size(), e.st);
+  e.sync();
 }
 
 }  // namespace bipm

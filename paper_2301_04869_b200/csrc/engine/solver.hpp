@@ -14,13 +14,10 @@
 
 #include "../kernels/ipm_kernels.hpp"
 #include "engine.hpp"
+#include "host_link.hpp"
+#include "kkt_step.hpp"
 
 namespace bipm {
-
-struct RegOptions {  // RegSchedule (kkt.hpp:20-29)
-  double delta_w0 = 1e-4, delta_w_min = 1e-20, delta_w_max = 1e40;
-  double kappa_minus = 1.0 / 3.0, kappa_plus = 8.0, kappa_plus_emergency = 100.0;
-};
 
 struct SolverOptions {  // IpmOptions (ipm.hpp:7-25)
   double tol = 1e-6, mu0 = 1e-1, kappa_mu = 0.2, theta_mu = 1.5, tau = 0.995, kappa_eps = 10.0;
@@ -39,7 +36,14 @@ struct IterRecord {  // IterationLog (ipm.hpp:27-36)
   bool full_step = false;
 };
 
-enum SolveStatusCode : int { kRunning = -1, kOptimal = 0, kMaxIter = 1, kInfeasible = 2, kLinFail = 3 };
+enum SolveStatusCode : int {
+  kNotStarted = -2,
+  kRunning = -1,
+  kOptimal = 0,
+  kMaxIter = 1,
+  kInfeasible = 2,
+  kLinFail = 3
+};
 
 class Solver {
  public:
@@ -52,7 +56,7 @@ class Solver {
   // solve first when it already terminated); returns the device ms
   double step_timed(int* st_out);
 
-  int status = kRunning;
+  int status = kNotStarted;  // step() before start() is an error
   int iter = 0;
   double mu = 0, delta_w_last = 0, objective = 0;
   std::vector<IterRecord> logs;
@@ -60,9 +64,12 @@ class Solver {
   long long reductions = 0;  // K_hat assemblies (every inertia attempt)
   std::string message;
 
-  // host copies of the final iterate
-  std::vector<double> host_u() const;
-  std::vector<double> host_x() const;
+  // host copies of the current iterate (stream-ordered after the queued work)
+  std::vector<double> host_u();
+  std::vector<double> host_x();
+  // every array of the current primal-dual point (Iterate, model.hpp:41-55):
+  // x, u, s, y, z, kappa_lo, kappa_up, nu_lo, nu_up, lambda_lo, lambda_up
+  void host_iterate(double* const out[11]);
 
  private:
   struct Scaled {
@@ -80,21 +87,21 @@ class Solver {
   };
   ErrEval kkt_eval(const DevIter& it, Engine::Bundle& bd, const double mus[4], bool check_bad);
   Scaled scaled_of(const ErrEval& E, int k) const;
-  bool attempt(double dw, const DevIter& it);  // one inertia-loop attempt (kkt.cpp:954-1001)
-  void compute_step(const DevIter& it);         // solve_reduced (kkt.cpp:945-1006)
-  double fetch1(const double* d);
-  // cross-rank exchange (no-ops on a single GPU)
-  void allred(double* d, size_t n, RedOpKind op);
-  double host_all(double v, RedOpKind op);
-  idx global_first_bad(idx local_bad);
-  void condensed_u_sum(const double* part, const double* base, double* out);
+  // assemble_augmented on the device, then solve_reduced (kkt.cpp:945-1006)
+  void compute_step(const DevIter& it);
+  double fetch1(const double* d) { return io.fetch1(d); }
   template <int K>
-  std::array<double, K> fetch(const double* d);
-  DevStep step_view(DArr<double>* s);
+  std::array<double, K> fetch(const double* d) {
+    return io.fetch<K>(d);
+  }
+  void allred(double* d, size_t n, RedOpKind op) { io.allred(d, n, op); }
+  idx global_first_bad(idx local_bad) { return io.global_first_bad(local_bad); }
   double now() const;
 
   Engine& e;
   SolverOptions o;
+  HostLink io;
+  KktStep kkt;
   IpmDims d{};
   DevBounds b{};
   DArr<double> xlo, xup, ulo, uup, slo, sup;
@@ -104,19 +111,12 @@ class Solver {
   DevIter alt() { return its[1 - icur].view(); }
   bool bundle_fresh = false;
   double mult_count = 0;
-  // augmented / refinement storage
-  DArr<double> r1x, r1u, gsum_u, rhat2_part;
-  DArr<double> p[5], q[5];  // px, pu, ps, pz, py
+  DArr<double> gsum_u;
   DArr<double> bsv[6];
-  DArr<double> o1x, o1u, o2, o3, o4, o1u_part;
-  DArr<double> c_rhat1, c_rhat2, rhs_sum, pu_rhs, red_u, dd_u;
   DArr<double> ft, gt, ht;  // line-search trial values
   DArr<double> partial, scal;
   DArr<int> flag;
   DArr<unsigned int> eval_counter;
-  double* pinned = nullptr;
-  int corrections = 0, refinements = 0;
-  double last_dw = 0;
   std::chrono::steady_clock::time_point t0_;
 };
 

@@ -22,7 +22,9 @@ def case_path(name: str) -> str:
 
 
 def golden_files():
-    return sorted(glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """reduced-KKT dump fixtures (not the iterates_*.npz solve summaries)"""
+    return sorted(p for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("iterates_"))
 
 
 @pytest.fixture(scope="session")

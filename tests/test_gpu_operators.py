@@ -1,0 +1,146 @@
+"""Operator-level parity: each reduced-strategy operator of the C-ABI against
+the reference's own outputs at the same inputs (fixtures dumped by
+oracle/_ref/bipm_ref from the reference's public API, tests/golden/).
+
+  condense        kkt.cpp:123-170      <= 1e-12 relative
+  reduce_rhs      kkt.cpp:209-239      <= 1e-9  (as K_hat / rhs)
+  recover         kkt.cpp:507-532, 172-188   <= 1e-7
+  solve_reduced   kkt.cpp:945-1006     <= 1e-7, same delta_w / corrections
+                  (the whole operator: condense, refactor, inertia loop,
+                  Cholesky, recovery and refinement rounds)
+
+Every fixture runs twice: on an OPF problem built from the case file and on a
+KKT-only problem built from the fixture's own patterns
+(bipm_problem_create_patterns -- what a reference solve uses when it calls
+the GPU for solve_reduced).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, case_path
+from paper_2301_04869_b200 import _native as nat
+
+pytestmark = pytest.mark.gpu
+
+FIXTURES = ["case9_N8_s005_it3", "case118_N4_s005_it5", "case118_N4_s005_it20",
+            "case1354pegase_N4_s005_it40", "case9241pegase_N2_s005_it2"]
+PATTERNS = ("gx", "gu", "hx", "hu", "wxx", "wxu", "wuu")
+
+
+def available(names):
+    return [n for n in names if os.path.exists(os.path.join(GOLDEN, n + ".npz"))]
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.abs(a - b).max(initial=0.0)) / max(1e-300, float(np.abs(b).max(initial=0.0)))
+
+
+def augmented(fx):
+    a = {k: fx[k] for k in PATTERNS}
+    a.update(sigma_x=fx["sigma_x"], r1x=fx["r1x"], r3=fx["r3"], sigma_s=fx["sigma_s"],
+             r2=fx["r2"], r4=fx["r4"], sigma_u=fx["sigma_u"], r1u=fx["r1u"])
+    return a
+
+
+def condensed(fx):
+    return {k: fx[k] for k in ("gu", "kxx", "kxu", "kuu", "sigma_x", "rhat1", "rhat3",
+                               "sigma_u", "rhat2")}
+
+
+def make_ctx(fx, kind):
+    N = fx.dims[0]
+    if kind == "case":
+        p = nat.Problem(case_path(fx.meta["case"]), N, fx.meta["sigma"], fx.meta["seed"])
+    else:
+        pats = {k: (fx[k + "_p_rowptr"], fx[k + "_p_colind"], tuple(fx.meta[k + "_p_shape"]))
+                for k in PATTERNS}
+        p = nat.Problem.from_patterns(N, pats)
+    return nat.Context(p)
+
+
+@pytest.fixture(scope="module", params=available(FIXTURES))
+def fx(request, goldens):
+    return goldens[request.param]
+
+
+@pytest.mark.parametrize("kind", ["case", "patterns"])
+def test_condense_matches_reference(fx, kind):
+    ctx = make_ctx(fx, kind)
+    for k in ("kxx", "kxu", "kuu"):  # the condensed patterns are the reference's
+        assert np.array_equal(ctx.problem.array(k + "_p_rowptr"), fx[k + "_p_rowptr"])
+        assert np.array_equal(ctx.problem.array(k + "_p_colind"), fx[k + "_p_colind"])
+    out = ctx.condense(**augmented(fx))
+    for k in ("kxx", "kxu", "kuu", "rhat1", "rhat2", "rhat3"):
+        assert rel(out[k], fx[k]) <= 1e-12, (k, rel(out[k], fx[k]))
+
+
+@pytest.mark.parametrize("kind", ["case", "patterns"])
+def test_reduce_rhs_matches_reference(fx, kind):
+    ctx = make_ctx(fx, kind)
+    ctx.factor_gx(fx["gx"])
+    for dw, sfx in ((0.0, "0"), (fx.meta["dw_probe"], "dw")):
+        rhs = ctx.reduce_rhs(dw, **condensed(fx)) - fx["rhat2"]
+        assert rel(rhs, fx["rhs_" + sfx]) <= 1e-9, (sfx, rel(rhs, fx["rhs_" + sfx]))
+
+
+@pytest.mark.parametrize("kind", ["case", "patterns"])
+def test_recover_matches_reference(fx, kind):
+    """p_x, p_y, p_z, p_s at the reference's p_u.  The reference step carries
+    its refinement corrections, which differ from recover(p_u) by the
+    refinement residual only (relative 1e-12 .. 1e-9)."""
+    ctx = make_ctx(fx, kind)
+    ctx.factor_gx(fx["gx"])
+    dw = fx.meta["step_delta_w"]
+    out = ctx.recover(dw, fx["pu"], fx["hx"], fx["hu"], fx["sigma_s"], fx["r2"], fx["r4"],
+                      **condensed(fx))
+    for k in ("px", "py", "pz", "ps"):
+        assert rel(out[k], fx[k]) <= 1e-7, (k, rel(out[k], fx[k]))
+
+
+@pytest.mark.parametrize("kind", ["case", "patterns"])
+def test_solve_reduced_matches_reference(fx, kind):
+    """The whole solve_reduced operator from the augmented system: the step
+    and the inertia decisions (delta_w, corrections) of the reference's
+    compute_step at the fixture iterate (fresh warm start)."""
+    ctx = make_ctx(fx, kind)
+    step, info, dwl = ctx.solve_reduced(0.0, **augmented(fx))
+    assert info["corrections"] == fx.meta["step_corrections"]
+    assert info["delta_w"] == pytest.approx(fx.meta["step_delta_w"], rel=1e-12, abs=0.0)
+    for k in ("px", "pu", "ps", "pz", "py"):
+        assert rel(step[k], fx[k]) <= 1e-7, (k, rel(step[k], fx[k]))
+    # a second call with the returned warm start is the reference's next-step
+    # behaviour: same system, delta_w_last carried
+    step2, info2, _ = ctx.solve_reduced(dwl, **augmented(fx))
+    if info["corrections"] == 0:
+        assert info2["corrections"] == 0
+        assert rel(step2["pu"], step["pu"]) <= 1e-12
+
+
+def test_solve_reduced_reports_non_interior(goldens):
+    fx = goldens["case9_N8_s005_it3"]
+    ctx = make_ctx(fx, "patterns")
+    a = augmented(fx)
+    a["sigma_s"] = a["sigma_s"].copy()
+    a["sigma_s"][3, 2] = 0.0
+    with pytest.raises(nat.NonInteriorError):
+        ctx.solve_reduced(0.0, **a)
+
+
+def test_solve_reduced_reports_singular_block(goldens):
+    """A G_x block with a zero column is singular: SingularBlockError with the
+    lowest such scenario, which the reference answers with its augmented
+    fallback (ipm.cpp:502-507)."""
+    fx = goldens["case118_N4_s005_it5"]
+    ctx = make_ctx(fx, "patterns")
+    a = augmented(fx)
+    gx = a["gx"].copy()
+    ci = fx["gx_p_colind"]
+    gx[2, ci == 7] = 0.0
+    gx[3, ci == 11] = 0.0
+    a["gx"] = gx
+    with pytest.raises(nat.SingularBlockError) as e:
+        ctx.solve_reduced(0.0, **a)
+    assert "singular block 2" in str(e.value)

@@ -12,6 +12,8 @@ import numpy as np
 import pytest
 
 from conftest import GOLDEN, case_path
+from iterate_check import compare
+from matpower_tables import read_case
 from paper_2301_04869_b200 import _native as nat
 
 pytestmark = pytest.mark.gpu
@@ -39,6 +41,80 @@ def test_solve_matches_reference(case, N, sigma):
         assert a["objective"] == pytest.approx(b["objective"], rel=1e-6)
 
 
+def iterate_golden(key):
+    path = os.path.join(GOLDEN, f"iterates_{key}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated (tests/golden/make_golden.py)")
+    return np.load(path)
+
+
+@pytest.mark.parametrize("case,N,sigma", [("case9", 8, 0.0), ("case9", 8, 0.05),
+                                          ("case118", 4, 0.05), ("case118", 64, 0.05)])
+def test_final_iterate_matches_reference(case, N, sigma):
+    """Primal AND dual iterates (x, u, s, y, z and every bound multiplier) of
+    the converged GPU solve against the reference's final Iterate."""
+    ref = iterate_golden(f"{case}_N{N}_s{str(sigma).replace('.', '')}")
+    s = nat.Solver(nat.Context(nat.Problem(case_path(case), N, sigma, 0)))
+    r = s.solve()
+    assert r["iterations"] == int(ref["iterations"][0])
+    assert r["objective"] == pytest.approx(float(ref["objective"][0]), rel=1e-6)
+    compare(s.iterate(), ref)
+
+
+CONT = json.load(open(os.path.join(GOLDEN, "solves_contingency.json")))
+
+
+@pytest.mark.parametrize("key", sorted(CONT))
+def test_contingency_solve_matches_reference(key):
+    """Outage scenarios (generate_scenarios contingencies, round-robin;
+    outaged branches contribute exactly zero, opf_model.cpp:383-384): same
+    iterations, objective, trajectory and final iterate as the reference."""
+    ref = CONT[key]
+    case, rest = key.split("_N")
+    N = int(rest.split("_")[0])
+    p = nat.Problem(case_path(case), N, 0.05, 0, contingencies=ref["contingencies"])
+    s = nat.Solver(nat.Context(p))
+    r = s.solve()
+    assert r["status_name"] == ref["status"] == "Optimal"
+    assert r["iterations"] == ref["iterations"]
+    assert abs(r["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
+    for a, b in zip(r["logs"], ref["logs"]):
+        assert int(a["corr"]) == b["corr"]
+        assert a["objective"] == pytest.approx(b["objective"], rel=1e-6)
+    compare(s.iterate(), iterate_golden(key))
+
+
+def test_outaged_branch_rows_vanish():
+    """test_opf.cpp:348-366: branch 4 out in scenario 0 of case9 (N=2,
+    sigma 0): its squared-flow rows h[4], h[L+4] are exactly zero there and
+    nonzero in the intact scenario."""
+    p = nat.Problem(case_path("case9"), 2, 0.0, 3, contingencies=[4])
+    ctx = nat.Context(p)
+    X = np.tile(p.array("x_start"), (2, 1))
+    u = np.maximum(p.array("u_start"), 0.3)
+    _, _, h = ctx.eval_values(X, u)
+    L = p.nbranch
+    assert h[0, 4] == 0.0 and h[0, L + 4] == 0.0
+    assert h[1, 4] != 0.0
+
+
+def test_problem_from_tables_matches_case_file():
+    """bipm_problem_create_tables (the reference's CaseData + ScenarioSet in
+    memory) builds the same problem as the case-file path and solves it the
+    same way."""
+    path = case_path("case118")
+    p_file = nat.Problem(path, 4, 0.05, 0)
+    t = read_case(path)
+    mult = p_file.array("mult").reshape(4, -1)
+    p_tab = nat.Problem.from_tables(multipliers=mult, sigma=0.05, seed=0, **t)
+    for k in ("L_g_val", "L_h_val", "L_f_val", "L_g_colind", "x_lo", "s_up", "u_start", "pd"):
+        assert np.array_equal(p_tab.array(k), p_file.array(k)), k
+    r_file = nat.Solver(nat.Context(p_file)).solve()
+    r_tab = nat.Solver(nat.Context(p_tab)).solve()
+    assert r_tab["iterations"] == r_file["iterations"]
+    assert r_tab["objective"] == r_file["objective"]
+
+
 def test_step_api_matches_whole_solve():
     p = nat.Problem(case_path("case9"), 8, 0.05, 0)
     ctx = nat.Context(p)
@@ -63,11 +139,13 @@ def test_case1354_N256_matches_reference_at_scale():
     ref = json.load(open(os.path.join(GOLDEN, "solves_large.json")))[
         "case1354pegase_N256_s0.05_seed0"]
     p = nat.Problem(case_path("case1354pegase"), 256, 0.05, 0)
-    r = nat.Solver(nat.Context(p)).solve()
+    s = nat.Solver(nat.Context(p))
+    r = s.solve()
     assert r["status_name"] == "Optimal" and r["iterations"] == ref["iterations"]
     assert abs(r["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
     u_ref = np.array(ref["u"])
     assert np.abs(r["u"] - u_ref).max() <= 1e-6 * max(1.0, np.abs(u_ref).max())
+    compare(s.iterate(), iterate_golden("case1354pegase_N256_s005"))
 
 
 def test_case2869_N512_first_iterations_match_reference():

@@ -13,8 +13,15 @@ from paper_2301_04869_b200 import _native as nat
 
 
 def header_symbols():
+    """Every bipm_* name the header mentions -- declarations AND the names in
+    its comments (the reference-interface table) -- minus the type names."""
     text = open(os.path.join(ROOT, "include", "bipm_gpu.h")).read()
-    return sorted(set(re.findall(r"\b(bipm_[a-z_0-9]+)\s*\(", text)))
+    names = set(re.findall(r"\b(bipm_[a-z_0-9]+)\b(?!\.h)", text))
+    types = set(re.findall(r"}\s*(bipm_[a-z_0-9]+)\s*;", text))
+    types |= set(re.findall(r"typedef\s+struct\s+bipm_[a-z_0-9]+\s+(bipm_[a-z_0-9]+)\s*;", text))
+    types |= set(re.findall(r"typedef\s+struct\s+(bipm_[a-z_0-9]+)", text))
+    types |= set(re.findall(r"\(\s*\*\s*(bipm_[a-z_0-9]+)\s*\)", text))
+    return sorted(names - types)
 
 
 def test_library_exports_every_header_symbol():
