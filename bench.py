@@ -11,7 +11,13 @@ configs[2]); it fits one B200 (~0.6 GB resident), so N=1 runs it whole and
 --gpus N shards its scenarios (override with --case/--scenarios, e.g. configs[1]
 = case118 / 64).
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--comm nccl|gloo]
+
+--gpus N without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (127.0.0.1).  Rank r drives GPU
+r mod device_count; --comm gloo exchanges through host-staged gloo all-reduces
+instead of NCCL, so N ranks can share one GPU (the two-rank strong-scaling
+path on a one-GPU box).
 
 Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
 """
@@ -120,7 +126,7 @@ def algorithmic_bytes(p, info, group, M):
     if group == "reduce_tiles":
         per = 7 * n_x * n_u * 8 + 2 * nnz_f * 12 + (nnz["gu"] + nnz["kxx"] + nnz["kxu"] +
                                                      nnz["kuu"]) * 12
-        return M * per + info["nchunks"] * n_u * n_u * 8
+        return M * per + n_u * n_u * 8  # one K_hat per GPU (G n_u^2 8)
     if group == "lu_refactor":
         return M * (nnz["gx"] + nnz_f) * 8
     if group in ("reduce_rhs", "recover_state"):
@@ -150,18 +156,33 @@ def bench_ours(a, rank, world):
     import torch
     from paper_2301_04869_b200 import _native as nat
 
-    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = max(1, torch.cuda.device_count())
+    dev = int(os.environ.get("LOCAL_RANK", "0")) % ndev
     torch.cuda.set_device(dev)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if a.comm == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group("gloo")
     from paper_2301_04869_b200.distributed import sharded_context
+
+    def max_over_ranks(v: float) -> float:
+        if not dist:
+            return v
+        t = torch.tensor([v], dtype=torch.float64,
+                         device="cuda" if a.comm == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     case_file = os.path.join(DATA_DIR, a.case + ".m")
     workload = f"{a.case}_N{a.scenarios}"
     p = nat.Problem(case_file, a.scenarios, a.sigma, a.seed)
-    # one scenario group per GPU; K_hat / rhs / norms all-reduced over NCCL
-    ctx = sharded_context(p, world, rank, device=dev, backend="nccl")
+    # one scenario group per rank; K_hat / rhs / norms all-reduced (NCCL over
+    # NVLink, or host-staged gloo)
+    ctx = sharded_context(p, world, rank, device=dev, backend=a.comm)
+    comm = ctx.comm_info()
     info = ctx.info()
     solver = nat.Solver(ctx)
     solver.start()
@@ -189,11 +210,7 @@ def bench_ours(a, rank, world):
               "cholesky", "recover_state"]
     kt = {g: ctx.kernel_time(g) for g in groups}
     ctx.profile(False)
-    total_ms = sum(times)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(times))
     ms_per_step = total_ms / a.steps
 
     # end to end through the public C-ABI with host buffers: context upload
@@ -214,7 +231,7 @@ def bench_ours(a, rank, world):
         torch.cuda.synchronize()
         h0_r = nat.counters()
         t0 = time.perf_counter()
-        ctx2 = sharded_context(p, world, rank, device=dev, backend="nccl")
+        ctx2 = sharded_context(p, world, rank, device=dev, backend=a.comm)
         torch.cuda.synchronize()
         t_ctx_r = time.perf_counter() - t0
         t_s = time.perf_counter()
@@ -225,14 +242,12 @@ def bench_ours(a, rank, world):
         e2e_r = time.perf_counter() - t0
         del sol2
         h1_r = nat.counters()
-        if dist:
-            t = torch.tensor([e2e_r], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_r = float(t.item())
-        runs.append((e2e_r, t_ctx_r, h0_r, h1_r, t_setup_r))
+        e2e_r = max_over_ranks(e2e_r)
+        # each run keeps its own iteration count and result
+        runs.append((e2e_r, t_ctx_r, h0_r, h1_r, t_setup_r, res))
         del ctx2
         gc.collect()
-    e2e_s, t_ctx, h0, h1, t_setup = sorted(runs, key=lambda x: x[0])[len(runs) // 2]
+    e2e_s, t_ctx, h0, h1, t_setup, res = sorted(runs, key=lambda x: x[0])[len(runs) // 2]
     iters = max(1, res["iterations"])
 
     dom = max(kt, key=lambda g: kt[g][0])
@@ -242,7 +257,7 @@ def bench_ours(a, rank, world):
     achieved = (algo / (dom_ms / dom_n * 1e-3)) / 1e9 if dom_n else 0.0
     line = {
         "metric": METRIC, "value": round(ms_per_step, 4), "unit": "ms/iteration",
-        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "n_gpus": world, "devices_used": min(world, ndev), "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": round(ms_per_step, 4), "higher_is_better": False,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic MATPOWER replica {a.case} (reference proj/data, gen_cases.py), "
@@ -250,7 +265,8 @@ def bench_ours(a, rank, world):
         "config": {"workload": workload, "case": a.case, "scenarios": a.scenarios,
                    "sigma": a.sigma, "seed": a.seed,
                    "parallelism": "1 GPU" if world == 1 else
-                   f"dp{world}: scenario groups per GPU, NCCL all-reduce of K_hat/rhs/norms",
+                   f"dp{world}: scenario groups per rank, {a.comm} all-reduce of K_hat/rhs/norms"
+                   + ("" if world <= ndev else f", {world} ranks on {ndev} GPU(s)"),
                    "step": "one IPM iteration (iterations warmup.. of a fresh solve)",
                    "l2": "flushed (256 MiB write) before every timed iteration"},
         "total_solve_s": round(res["t_total"], 5), "iterations": res["iterations"],
@@ -263,6 +279,7 @@ def bench_ours(a, rank, world):
                 "h2d_bytes_per_step": int((h1["h2d_bytes"] - h0["h2d_bytes"]) / iters),
                 "d2h_bytes_per_step": int((h1["d2h_bytes"] - h0["d2h_bytes"]) / iters)},
         "gpu_launches": int(c1["launches"] - c0["launches"]),
+        "comm": comm,
         "roofline": {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 2),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 5),
                      "peak_kind": peak_kind, "traffic": ncu_traffic(workload, dom),
@@ -271,20 +288,35 @@ def bench_ours(a, rank, world):
         "kernel_ms_per_step": {g: round(v[0] / a.steps, 4) for g, v in kt.items()},
     }
     if rank == 0 and world == 1 and not a.no_cpu_baseline and os.path.exists(REF_BIN):
+        # the same iteration window as the GPU value (iterations warmup..),
+        # bounded to cpu_iters timed iterations (~10-30 s of host work)
         cores = cpu_cores()
-        j = run_reference_solve(a.case, a.scenarios, a.sigma, a.seed, a.cpu_iters, cores)
-        it = max(1, j["iterations"])
+        n_cpu = max(1, min(a.cpu_iters, a.steps))
+        j = run_reference_solve(a.case, a.scenarios, a.sigma, a.seed, a.warmup + n_cpu, cores)
+        logs = j["logs"][a.warmup:a.warmup + n_cpu] or j["logs"][-1:]
+        ms = 1e3 * sum(l["t_total"] for l in logs) / len(logs)
         line["cpu_baseline"] = {
-            "value": round(1e3 * j["t_total"] / it, 3), "unit": "ms/iteration", "cores": cores,
-            "kind": "reference",
-            "sample": f"reference solve of {workload} capped at {a.cpu_iters} iterations "
-                      f"({j['iterations']} run, {j['status']}), --groups/--workers {cores}; "
-                      "Eigen SparseLU restated in oracle/stubs",
-            "total_s": round(j["t_total"], 3), "iterations": j["iterations"]}
+            "value": round(ms, 3), "unit": "ms/iteration", "cores": cores, "kind": "reference",
+            "cpu_model": cpu_model(),
+            "sample": f"iterations {a.warmup}..{a.warmup + len(logs) - 1} of the reference "
+                      f"solve of {workload} (IterationLog.t_total; {j['iterations']} run), "
+                      f"--groups/--workers {cores}; Eigen SparseLU restated in oracle/stubs",
+            "iterations_timed": len(logs)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def bench_reference(a, rank, world):
@@ -305,7 +337,7 @@ def bench_reference(a, rank, world):
                    "sigma": a.sigma, "seed": a.seed, "parallelism": f"{cores} host threads",
                    "step": "one IPM iteration (reference IterationLog.t_total)"},
         "cpu_baseline": {"value": round(ms, 4), "unit": "ms/iteration", "cores": cores,
-                         "kind": "reference",
+                         "kind": "reference", "cpu_model": cpu_model(),
                          "sample": f"iterations {a.warmup}..{a.warmup + len(logs) - 1} of the "
                                    f"reference solve (--groups/--workers {cores}); Eigen "
                                    "SparseLU restated in oracle/stubs"},
@@ -326,18 +358,29 @@ def main():
     ap.add_argument("--scenarios", type=int, default=256)
     ap.add_argument("--sigma", type=float, default=0.05)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--cpu-iters", type=int, default=4,
-                    help="iteration cap of the CPU baseline sample (bounded: ~10-30 s of "
-                         "host work at the default workload)")
+    ap.add_argument("--cpu-iters", type=int, default=3,
+                    help="timed iterations of the CPU baseline sample, after the same warm-up "
+                         "iterations as the GPU value (bounded: ~10-30 s of host work)")
+    ap.add_argument("--comm", choices=["nccl", "gloo"], default="nccl",
+                    help="cross-rank exchange: NCCL (one GPU per rank) or host-staged gloo "
+                         "(ranks may share a GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-runs", type=int, default=3,
                     help="end-to-end solves (fresh context each); the median is reported")
     a = ap.parse_args()
     a.warmup = max(3, a.warmup)
+    if "WORLD_SIZE" not in os.environ and a.gpus > 1:
+        # --gpus N outside torchrun: re-launch under torch.distributed.run
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.run(cmd).returncode)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(a.gpus)))
-    if "WORLD_SIZE" not in os.environ:
-        world = 1
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if a.impl == "reference":
         bench_reference(a, rank, world)
     else:

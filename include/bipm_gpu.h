@@ -253,6 +253,8 @@ int bipm_partition(int32_t N, int32_t G, int32_t* ranges);
 /* NCCL (loaded with dlopen): rank 0 creates the id, every rank joins */
 int bipm_nccl_unique_id(uint8_t out[128]);
 int bipm_ctx_set_nccl(bipm_ctx* c, const uint8_t id[128], int32_t nranks, int32_t rank);
+/* out = {kind (0 none, 1 NCCL, 2 host callback), communicator ranks, rank} */
+int bipm_ctx_comm(const bipm_ctx* c, int32_t out[3]);
 /* host-staged exchange through a callback (op: 0 sum, 1 max, 2 min, in place) */
 typedef void (*bipm_allreduce_fn)(void* user, double* buf, int64_t n, int32_t op);
 int bipm_ctx_set_host_comm(bipm_ctx* c, bipm_allreduce_fn fn, void* user, int32_t nranks,

@@ -113,6 +113,7 @@ SIGNATURES = {
     "bipm_recover": (ctypes.c_int, [_P, _P, _P, ctypes.c_double, _D, _D, _D, _D, _D]),
     "bipm_solve_reduced": (ctypes.c_int, [_P, _P, _P, _D, _P, _P]),
     "bipm_solver_iterate": (ctypes.c_int, [_P, _P]),
+    "bipm_ctx_comm": (ctypes.c_int, [_P, _I]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -501,6 +502,13 @@ class Context:
         n = ctypes.c_int64(0)
         check(lib().bipm_ctx_debug_buffer(self._h, out, cap, ctypes.byref(n)))
         return list(out[:n.value])
+
+    def comm_info(self) -> dict:
+        """The context's exchange: kind (none / nccl / host), ranks, rank."""
+        out = (ctypes.c_int32 * 3)()
+        check(lib().bipm_ctx_comm(self._h, out))
+        return {"kind": {0: "none", 1: "nccl", 2: "host"}.get(out[0], str(out[0])),
+                "nranks": out[1], "rank": out[2]}
 
     def info(self) -> dict:
         out = (ctypes.c_int64 * 12)()

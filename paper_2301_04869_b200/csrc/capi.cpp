@@ -786,6 +786,15 @@ int bipm_ctx_set_host_comm(bipm_ctx* c, bipm_allreduce_fn fn, void* user, int32_
   });
 }
 
+int bipm_ctx_comm(const bipm_ctx* c, int32_t out[3]) {
+  return guarded([&] {
+    const Engine& e = *c->eng;
+    out[0] = e.comm ? e.comm->kind() : 0;
+    out[1] = e.comm ? e.comm->size() : 1;
+    out[2] = e.comm ? e.comm->rank() : 0;
+  });
+}
+
 int bipm_partition(int32_t N, int32_t G, int32_t* ranges) {
   return guarded([&] {
     if (G < 1 || G > N) throw Error(kInvalidArgument, "partition: need 1 <= G <= N");

@@ -30,6 +30,8 @@ struct NcclApi {
   int (*CommInitRank)(ncclComm_t*, int, NcclId, int) = nullptr;
   int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*CommDestroy)(ncclComm_t) = nullptr;
+  int (*CommCount)(const ncclComm_t, int*) = nullptr;
+  int (*CommUserRank)(const ncclComm_t, int*) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
 
   static NcclApi& get() {
@@ -51,6 +53,9 @@ struct NcclApi {
       api.AllReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, ncclComm_t,
                                                cudaStream_t)>(sym("ncclAllReduce"));
       api.CommDestroy = reinterpret_cast<int (*)(ncclComm_t)>(sym("ncclCommDestroy"));
+      api.CommCount = reinterpret_cast<int (*)(const ncclComm_t, int*)>(sym("ncclCommCount"));
+      api.CommUserRank =
+          reinterpret_cast<int (*)(const ncclComm_t, int*)>(sym("ncclCommUserRank"));
       api.GetErrorString = reinterpret_cast<const char* (*)(int)>(sym("ncclGetErrorString"));
     }
     return api;
@@ -68,12 +73,18 @@ class NcclCommImpl final : public Comm {
     std::memcpy(nid.internal, id, 128);
     ck(cudaSetDevice(device), "cudaSetDevice");
     api.check(api.CommInitRank(&comm_, nranks, nid, rank), "ncclCommInitRank");
+    // what the communicator itself reports (evidence the ranks joined)
+    api.check(api.CommCount(comm_, &n_), "ncclCommCount");
+    api.check(api.CommUserRank(comm_, &r_), "ncclCommUserRank");
+    if (n_ != nranks || r_ != rank)
+      throw std::runtime_error("ncclCommInitRank: communicator reports a different rank layout");
   }
   ~NcclCommImpl() override {
     if (comm_) NcclApi::get().CommDestroy(comm_);
   }
   int rank() const override { return r_; }
   int size() const override { return n_; }
+  int kind() const override { return 1; }
   void allreduce(double* d, size_t n, RedOpKind op, cudaStream_t st) override {
     if (!n) return;
     const int o = op == RedOpKind::kSum ? kNcclSum : (op == RedOpKind::kMax ? kNcclMax : kNcclMin);
@@ -95,6 +106,7 @@ class HostCommImpl final : public Comm {
   }
   int rank() const override { return r_; }
   int size() const override { return n_; }
+  int kind() const override { return 2; }
   void allreduce(double* d, size_t n, RedOpKind op, cudaStream_t st) override {
     if (!n) return;
     if (n > cap_) {

@@ -26,6 +26,7 @@ class Comm {
   virtual ~Comm() = default;
   virtual int rank() const = 0;
   virtual int size() const = 0;
+  virtual int kind() const = 0;  // 1 NCCL, 2 host callback
   // in-place all-reduce of n doubles of device memory, ordered on stream st
   virtual void allreduce(double* d, size_t n, RedOpKind op, cudaStream_t st) = 0;
 };
