@@ -333,6 +333,17 @@ int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap,
  * column-major) shifted by 1e-13 max(1,|K|_inf), Cholesky; *pd = 1 when
  * positive definite, then rhs is overwritten by K^{-1} rhs */
 int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, int32_t* pd);
+/* The Bunch-Kaufman branch of DenseSymFactor::factor (dsytrf 'L' on the
+ * shifted K, linalg.cpp:136-145, lapack.cpp:40-97): inertia = {pos, neg,
+ * zero} of D; rhs (may be NULL) is overwritten by K^{-1} rhs when zero = 0.
+ * bipm_dense_factor_solve and the engine's inertia loop use it when the
+ * Cholesky rejects a pivot within rounding of zero: *pd then reports the BK
+ * verdict neg = 0 and zero = 0, as the reference's attempt does
+ * (kkt.cpp:969-971). */
+int bipm_dense_inertia(int32_t n, const double* k_colmajor, double* rhs, int32_t inertia[3]);
+/* out = {attempts decided by the Bunch-Kaufman inertia so far, the accepted
+ * K_hat factor is Bunch-Kaufman (1) or Cholesky (0)} */
+int bipm_ctx_factor_stats(bipm_ctx* c, int64_t out[2]);
 /* whole solve: start + steps until a terminal status */
 int bipm_solve(bipm_ctx* c, const bipm_solve_options* opts, bipm_solve_result* r, double* u);
 

@@ -114,6 +114,8 @@ SIGNATURES = {
     "bipm_solve_reduced": (ctypes.c_int, [_P, _P, _P, _D, _P, _P]),
     "bipm_solver_iterate": (ctypes.c_int, [_P, _P]),
     "bipm_ctx_comm": (ctypes.c_int, [_P, _I]),
+    "bipm_dense_inertia": (ctypes.c_int, [ctypes.c_int32, _D, _D, _I]),
+    "bipm_ctx_factor_stats": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64)]),
 }
 
 BUNDLE_FIELDS = ("f", "g", "h", "gx", "gu", "hx", "hu", "wxx", "wxu", "wuu", "grad_lag")
@@ -503,6 +505,11 @@ class Context:
         check(lib().bipm_ctx_debug_buffer(self._h, out, cap, ctypes.byref(n)))
         return list(out[:n.value])
 
+    def factor_stats(self) -> dict:
+        out = (ctypes.c_int64 * 2)()
+        check(lib().bipm_ctx_factor_stats(self._h, out))
+        return {"bk_fallbacks": out[0], "khat_bk": bool(out[1])}
+
     def comm_info(self) -> dict:
         """The context's exchange: kind (none / nccl / host), ranks, rank."""
         out = (ctypes.c_int32 * 3)()
@@ -586,6 +593,15 @@ def counters() -> dict:
     out = (ctypes.c_int64 * 3)()
     check(lib().bipm_counters(out))
     return {"launches": out[0], "h2d_bytes": out[1], "d2h_bytes": out[2]}
+
+
+def dense_inertia(K: np.ndarray, b: np.ndarray | None = None):
+    """Bunch-Kaufman LDL' of the shifted K on the GPU: ((pos, neg, zero), K^{-1} b)."""
+    K = np.ascontiguousarray(np.asarray(K, dtype=np.float64).T)  # column-major
+    x = None if b is None else np.array(b, dtype=np.float64)
+    out = (ctypes.c_int32 * 3)()
+    check(lib().bipm_dense_inertia(len(K), dptr(K), None if x is None else dptr(x), out))
+    return (out[0], out[1], out[2]), x
 
 
 def dense_factor_solve(K: np.ndarray, b: np.ndarray):

@@ -748,25 +748,82 @@ int bipm_ctx_info(bipm_ctx* c, int64_t out[12]) {
   });
 }
 
+namespace {
+// BK factor (+ inertia) of the shifted K; solves rhs when the factor is
+// nonsingular.  inertia = {pos, neg, zero}
+void bk_factor_solve(int32_t n, const double* k_colmajor, double* rhs, int32_t inertia[3],
+                     cudaStream_t st) {
+  DArr<double> K, b;
+  DArr<int> ipiv{size_t(n)}, in{size_t(4)};
+  DArr<unsigned char> state{bk_work_bytes(n)};
+  K.upload(k_colmajor, size_t(n) * n, st);
+  launch_bk_factor(K.get(), n, ipiv.get(), state.get(), in.get(), st);
+  in.download(inertia, 3, st);
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  if (rhs && inertia[2] == 0) {
+    b.upload(rhs, size_t(n), st);
+    launch_bk_solve(K.get(), n, ipiv.get(), b.get(), st);
+    b.download(rhs, size_t(n), st);
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  }
+}
+}  // namespace
+
 int bipm_dense_factor_solve(int32_t n, const double* k_colmajor, double* rhs, int32_t* pd) {
   return guarded([&] {
+    if (n < 1 || !k_colmajor || !pd) throw Error(kInvalidArgument, "null argument");
     cudaStream_t st;
     cuda_check(cudaStreamCreate(&st), "stream");
     DArr<double> K, b;
-    DArr<int> info(4);
+    DArr<int> info(8);
     K.upload(k_colmajor, size_t(n) * n, st);
-    b.upload(rhs, size_t(n), st);
     launch_shift_cholesky(K.get(), n, info.get(), nullptr, st);
-    int inf = 0;
-    info.download(&inf, 1, st);
+    int inf[8] = {0};
+    info.download(inf, 6, st);
     cuda_check(cudaStreamSynchronize(st), "sync");
-    *pd = inf == 0 ? 1 : 0;
-    if (inf == 0) {
-      launch_cholesky_solve(K.get(), n, b.get(), st);
-      b.download(rhs, size_t(n), st);
-      cuda_check(cudaStreamSynchronize(st), "sync");
+    if (inf[0] == 0) {
+      *pd = 1;
+      if (rhs) {
+        b.upload(rhs, size_t(n), st);
+        launch_cholesky_solve(K.get(), n, b.get(), st);
+        b.download(rhs, size_t(n), st);
+        cuda_check(cudaStreamSynchronize(st), "sync");
+      }
+    } else {
+      // the same borderline rule as the engine (Engine::factor_khat)
+      double kinf = 0.0, piv = 0.0;
+      std::memcpy(&kinf, inf + 2, sizeof(double));
+      std::memcpy(&piv, inf + 4, sizeof(double));
+      const double tol = 4.0 * n * 2.220446049250313e-16 * std::max(1.0, kinf);
+      *pd = 0;
+      if (piv > -tol) {
+        int32_t in3[3];
+        std::vector<double> x(rhs ? rhs : k_colmajor, rhs ? rhs + n : k_colmajor);
+        bk_factor_solve(n, k_colmajor, rhs ? x.data() : nullptr, in3, st);
+        if (in3[1] == 0 && in3[2] == 0) {
+          *pd = 1;
+          if (rhs) std::copy(x.begin(), x.end(), rhs);
+        }
+      }
     }
     cudaStreamDestroy(st);
+  });
+}
+
+int bipm_dense_inertia(int32_t n, const double* k_colmajor, double* rhs, int32_t inertia[3]) {
+  return guarded([&] {
+    if (n < 1 || !k_colmajor || !inertia) throw Error(kInvalidArgument, "null argument");
+    cudaStream_t st;
+    cuda_check(cudaStreamCreate(&st), "stream");
+    bk_factor_solve(n, k_colmajor, rhs, inertia, st);
+    cudaStreamDestroy(st);
+  });
+}
+
+int bipm_ctx_factor_stats(bipm_ctx* c, int64_t out[2]) {
+  return guarded([&] {
+    out[0] = c->eng->bk_fallbacks;
+    out[1] = c->eng->khat_bk ? 1 : 0;
   });
 }
 

@@ -127,6 +127,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   };
   lu_arrays.reserve(120);
   lu.n = L.n;
+  lu.growth = 1e10;  // ~10 of 16 digits lost to growth: the refinement cannot recover them
+  if (const char* e = std::getenv("BIPM_GROWTH_LIMIT")) lu.growth = std::atof(e);
   lu.nnz_l = L.nnz_l;
   lu.nnz_f = L.nnz_f;
   lu.n_fwd = idx(L.fwd_ptr.size()) - 1;
@@ -234,7 +236,11 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   khat.resize(size_t(Mo.n_u) * Mo.n_u);
   rhs.resize(size_t(Mo.n_u));
   rhs_part.resize(Ms * size_t(Mo.n_u));
-  chol_info.resize(4);  // status + an 8-byte |K|_inf slot (dense_chol.cu)
+  chol_info.resize(8);  // status, |K|_inf, rejected pivot (kkt_kernels.hpp)
+  bk_ipiv.resize(size_t(Mo.n_u));
+  bk_inertia.resize(4);
+  bk_state.resize(bk_work_bytes(Mo.n_u));
+  if (const char* e = std::getenv("BIPM_FORCE_BK")) force_bk = std::atoi(e) != 0;
 
   red.lu = lu;
   red.gu = gu_p.v;
@@ -577,16 +583,45 @@ void Engine::finish_reduce(double dw) {
   launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st);
 }
 
-bool Engine::factor_khat() {
-  timed("cholesky", [&] { launch_shift_cholesky(khat.get(), pb.M.n_u, chol_info.get(), nullptr, st); });
-  int info = 0;
-  chol_info.download(&info, 1, st);
+bool Engine::factor_khat(double dw) {
+  const int n = pb.M.n_u;
+  timed("cholesky", [&] { launch_shift_cholesky(khat.get(), n, chol_info.get(), nullptr, st); });
+  int info[8] = {0};
+  chol_info.download(info, 6, st);
   sync();
-  return info == 0;
+  khat_bk = false;
+  if (info[0] == 0) return true;
+  double kinf = 0.0, piv = 0.0;
+  std::memcpy(&kinf, info + 2, sizeof(double));
+  std::memcpy(&piv, info + 4, sizeof(double));
+  // dpotrf rejects a pivot that is not > 0; a clearly negative (or NaN) one
+  // means K_hat is indefinite, which the reference's Bunch-Kaufman inertia
+  // reports too (neg > 0): reject without factoring again
+  const double tol = 4.0 * n * 2.220446049250313e-16 * std::max(1.0, kinf);
+  if (!(piv > -tol) && !force_bk) return false;
+  finish_reduce(dw);  // K_hat again: the Cholesky overwrote it
+  timed("cholesky", [&] {
+    launch_bk_factor(khat.get(), n, bk_ipiv.get(), bk_state.get(), bk_inertia.get(), st);
+  });
+  int in[3] = {0, 0, 0};
+  bk_inertia.download(in, 3, st);
+  sync();
+  ++bk_fallbacks;
+  if (in[1] == 0 && in[2] == 0) {
+    khat_bk = true;
+    return true;
+  }
+  return false;
 }
 
 void Engine::solve_khat(double* d_vec) {
-  timed("khat_solve", [&] { launch_cholesky_solve(khat.get(), pb.M.n_u, d_vec, st); });
+  const int n = pb.M.n_u;
+  timed("khat_solve", [&] {
+    if (khat_bk)
+      launch_bk_solve(khat.get(), n, bk_ipiv.get(), d_vec, st);
+    else
+      launch_cholesky_solve(khat.get(), n, d_vec, st);
+  });
 }
 
 void Engine::recover(double dw, const double* d_pu, double* d_px, double* d_py, double* d_pz,

@@ -155,9 +155,20 @@ class Engine {
   // finish_reduce (kkt.cpp:468-488): K_hat = sum of the partial tiles (all
   // ranks) + diag(sigma_u + delta_w)
   void finish_reduce(double delta_w);
-  // shift + Cholesky (kkt.cpp:965-971); true when positive definite
-  bool factor_khat();
+  // shift + Cholesky (kkt.cpp:965-971); true when the reference would accept
+  // the attempt.  A Cholesky failure at a pivot within rounding of zero is
+  // decided by the Bunch-Kaufman inertia of K_hat instead (linalg.cpp:136-145,
+  // dense_bk.cu): K_hat is re-summed from the partial slabs (finish_reduce at
+  // dw) and the attempt is accepted, and later solved with the LDL' factors,
+  // iff BK reports neg = 0 and zero = 0.  BIPM_FORCE_BK=1 takes that path on
+  // every Cholesky failure (tests).
+  bool factor_khat(double dw);
   void solve_khat(double* d_vec);
+  bool khat_bk = false;       // the accepted factor is Bunch-Kaufman (else Cholesky)
+  bool force_bk = false;
+  long long bk_fallbacks = 0;  // borderline attempts decided by the BK inertia
+  DArr<int> bk_ipiv, bk_inertia;
+  DArr<unsigned char> bk_state;
   // recover_state_adjoint + recover_slack_dual (kkt.cpp:507-532, :172-188)
   void recover(double delta_w, const double* d_pu, double* d_px, double* d_py, double* d_pz,
                double* d_ps, const double* d_rhat1 = nullptr, const double* d_rhat3 = nullptr,

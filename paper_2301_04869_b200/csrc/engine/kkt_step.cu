@@ -66,15 +66,20 @@ void KktStep::check_factor(const DArr<int>* interior_flag) {
   if (interior_flag && io.host_all(double(st_host[0]), RedOpKind::kMax) > 0)
     throw Error(kNonInterior, "iterate not strictly interior");
   idx local_sing = -1;
+  int why = 0;
   for (idx k = 0; k < d.M; ++k)
     if (st_host[size_t(k) + 1]) {
       local_sing = e.lo + k;
+      why = st_host[size_t(k) + 1];
       break;
     }
   const idx sing = io.global_first_bad(local_sing);
   if (sing >= 0)
     throw Error(kSingularBlock,
                 "singular block " + std::to_string(sing) +
+                    (why == 2 && sing == local_sing
+                         ? " (pivot growth of the shared static pivot order)"
+                         : "") +
                     " (the reference falls back to the augmented strategy, which is not on the "
                     "GPU path)",
                 sing);
@@ -95,7 +100,7 @@ bool KktStep::attempt(double dw) {
                    scal.get() + 20, e.st);
   io.allred(scal.get() + 20, 1, RedOpKind::kMax);
   io.fetch_async(scal.get() + 20, 40);
-  if (!e.factor_khat()) return false;
+  if (!e.factor_khat(dw)) return false;
   const double scale = io.pinned(40);
   // solve_with(c, first_sum): p_u, then state/adjoint and slack/dual recovery
   launch_pu_rhs(d.n_u, rhs_sum.get(), e.rhat2.get(), p[1].get(), true, e.st);

@@ -49,7 +49,10 @@ __global__ void shift_kernel(double* K, int n, int* info) {
   __syncthreads();
   const double shift = 1e-13 * fmax(1.0, red[0]);
   for (int i = threadIdx.x; i < n; i += blockDim.x) K[size_t(i) * n + i] += shift;
-  if (threadIdx.x == 0) *info = 0;
+  if (threadIdx.x == 0) {
+    *info = 0;
+    reinterpret_cast<double*>(info)[1] = red[0];  // |K|_inf
+  }
 }
 
 // Cholesky of the w x w diagonal block held in one warp's registers (lane r
@@ -58,7 +61,8 @@ __global__ void shift_kernel(double* K, int n, int* info) {
 // would keep 31 doubles live per step and spill).  Padded to 32 x 32 with the
 // identity so the loop is branch-free.  Returns 0, or 1 + the first failing
 // column (pivot not > 0 or NaN).
-__device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane, double* colbuf) {
+__device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane, double* colbuf,
+                                           double* fail_pivot = nullptr) {
   if (lane >= w) {
 #pragma unroll
     for (int c = 0; c < kNb; ++c) a[c] = (c == lane) ? 1.0 : 0.0;
@@ -68,6 +72,7 @@ __device__ __forceinline__ int warp_chol32(double (&a)[kNb], int w, int lane, do
   for (int j = 0; j < kNb; ++j) {
     const double ajj = __shfl_sync(0xffffffffu, a[j], j);
     const bool bad = !(ajj > 0.0) || isnan(ajj);
+    if (fail == 0 && bad && fail_pivot) *fail_pivot = ajj;  // the value dpotrf rejects
     fail = (fail == 0 && bad) ? j + 1 : fail;
     // rsqrt (MUFU seed + Newton, ~1 ulp) instead of the IEEE sqrt and
     // division subroutines: they were ~2/3 of the serial per-column chain
@@ -96,9 +101,13 @@ __global__ void diag_factor_kernel(double* K, int n, int c0, int* info) {
 #pragma unroll
   for (int c = 0; c < kNb; ++c)
     a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
-  const int fail = warp_chol32(a, w, r, colbuf);
+  double piv = 0.0;
+  const int fail = warp_chol32(a, w, r, colbuf, &piv);
   if (fail) {
-    if (r == 0) *info = c0 + fail;
+    if (r == 0) {
+      *info = c0 + fail;
+      reinterpret_cast<double*>(info)[2] = piv;
+    }
     return;
   }
 #pragma unroll
@@ -243,9 +252,13 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
       for (int c = 0; c < kNb; ++c)
         a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
       stamp();
-      const int f = warp_chol32(a, w, r, buf);
+      double piv = 0.0;
+      const int f = warp_chol32(a, w, r, buf, &piv);
       if (f) {
-        if (r == 0) info[0] = c0 + f;
+        if (r == 0) {
+          info[0] = c0 + f;
+          reinterpret_cast<double*>(info)[2] = piv;
+        }
       } else {
 #pragma unroll
         for (int c = 0; c < kNb; ++c)

@@ -18,6 +18,10 @@ struct DevSweep {
 // Static-pivot LU plan of G_x (host: LuPlan in host/plan.hpp).
 struct DevLu {
   int n, nnz_l, nnz_f, n_fwd, n_bwd;
+  // pivot-growth guard of the static pivot order: a scenario whose factor
+  // entries exceed growth * max|G_x| is flagged (status 2) like a singular
+  // block (engine.cu; the reference pivots per scenario, linalg.cpp:76-87)
+  double growth;
   const int *perm, *iperm;
   const int *l_ptr, *l_col;               // L strict lower, slot == position
   const int *u_ptr, *u_col, *u_slot;      // U strict upper

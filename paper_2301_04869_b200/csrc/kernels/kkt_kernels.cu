@@ -181,15 +181,19 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_kernel(DevLu P, double* F
     }
   }
   __syncthreads();
-  // pivot guard (linalg.cpp:69-73): every diagonal of U against max |G_x|
-  double bad = 0.0;
+  // pivot guard (linalg.cpp:69-73): every diagonal of U against max |G_x|;
+  // growth guard: every factor entry against growth * max |G_x|
+  double bad = 0.0, big = 0.0;
   const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
   for (int j = threadIdx.x; j < P.n; j += BLOCK) {
     const double d = Fs[P.diag[j]];
     if (!(fabs(d) >= floor_) || !isfinite(d)) bad = 1.0;
   }
+  for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) big = fmax(big, fabs(Fs[q]));
   bad = block_reduce<BLOCK>(bad, true);
-  if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
+  big = block_reduce<BLOCK>(big, true);
+  if (threadIdx.x == 0)
+    status[s] = bad > 0.0 ? 1 : (big > P.growth * fmax(scale_in[s], 1e-300) ? 2 : 0);
   // solve layouts: transposed copy and the sweep-ordered copy
   double* FTs = FT + size_t(s) * P.nnz_f;
   for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) FTs[q] = Fs[P.ft_src[q]];
@@ -466,15 +470,19 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     sync_all();  // every CTA's strips of Wn written before the next pass reads them
   }
   if (crank != 0) return;
-  // pivot guard (linalg.cpp:69-73) over every diagonal of U
-  double bad = 0.0;
+  // pivot guard (linalg.cpp:69-73): every diagonal of U against max |G_x|;
+  // growth guard: every factor entry against growth * max |G_x|
+  double bad = 0.0, big = 0.0;
   const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
   for (int j = threadIdx.x; j < P.n; j += BLOCK) {
     const double d = Fs[P.diag[j]];
     if (!(fabs(d) >= floor_) || !isfinite(d)) bad = 1.0;
   }
+  for (int q = threadIdx.x; q < P.nnz_f; q += BLOCK) big = fmax(big, fabs(Fs[q]));
   bad = block_reduce<BLOCK>(bad, true);
-  if (threadIdx.x == 0) status[s] = bad > 0.0 ? 1 : 0;
+  big = block_reduce<BLOCK>(big, true);
+  if (threadIdx.x == 0)
+    status[s] = bad > 0.0 ? 1 : (big > P.growth * fmax(scale_in[s], 1e-300) ? 2 : 0);
 }
 
 // the solve layouts after the Gauss-Jordan tail, spread over the whole GPU:
@@ -811,10 +819,12 @@ __global__ void __launch_bounds__(kDenseBlock) shift_cholesky_small_kernel(doubl
   for (int j = 0; j < n; ++j) {
     if (threadIdx.x == 0) {
       const double ajj = A[j * n + j];
-      if (!(ajj > 0.0) || isnan(ajj))
+      if (!(ajj > 0.0) || isnan(ajj)) {
         fail = j + 1;
-      else
+        reinterpret_cast<double*>(info)[2] = ajj;  // the rejected pivot (factor_khat)
+      } else {
         A[j * n + j] = sqrt(ajj);
+      }
     }
     __syncthreads();
     if (fail) break;
@@ -832,7 +842,10 @@ __global__ void __launch_bounds__(kDenseBlock) shift_cholesky_small_kernel(doubl
     __syncthreads();
   }
   for (int i = threadIdx.x; i < n * n; i += kDenseBlock) K[i] = A[i];
-  if (threadIdx.x == 0) *info = fail;
+  if (threadIdx.x == 0) {
+    *info = fail;
+    reinterpret_cast<double*>(info)[1] = mx;  // |K|_inf
+  }
 }
 
 // L L' x = b for column-major lower L: one warp, x in registers (row i on

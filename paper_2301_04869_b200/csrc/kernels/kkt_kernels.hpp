@@ -93,7 +93,14 @@ void launch_condense(const CondenseDev& c, int M, const double* W, int ldw, cons
 // Dense symmetric factor of the n x n column-major K (lower Cholesky in place)
 // with the reference's diagonal shift 1e-13 max(1, |K|_inf) (kkt.cpp:965-968).
 // info (device int): 0 when positive definite, else 1 + failing column.
+// info: 8 ints = {status (0, or the failing column + 1), pad, |K|_inf (double),
+// the rejected pivot (double), pad}
 void launch_shift_cholesky(double* K, int n, int* info, double* work, cudaStream_t st);
+// Bunch-Kaufman LDL' of the shifted K (dense_bk.cu): factor in place, ipiv
+// (LAPACK convention, 1-based), inertia[3] = pos, neg, zero; state: bk_work_bytes
+size_t bk_work_bytes(int n);
+void launch_bk_factor(double* K, int n, int* ipiv, void* state, int* inertia, cudaStream_t st);
+void launch_bk_solve(const double* F, int n, const int* ipiv, double* b, cudaStream_t st);
 void launch_cholesky_solve(const double* Lfac, int n, double* b, cudaStream_t st);
 // n above the shared-memory kernel's range (dense_chol.cu)
 void launch_blocked_cholesky(double* K, int n, int* info, cudaStream_t st);

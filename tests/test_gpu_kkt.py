@@ -107,3 +107,20 @@ def test_singular_block_reports_lowest_scenario(goldens):
     with pytest.raises(nat.SingularBlockError) as e:
         ctx.factor_gx(gx)
     assert "singular block 2" in str(e.value)
+
+
+def test_pivot_growth_guard(goldens, monkeypatch):
+    """The static pivot order is checked for element growth in every
+    refactor (max |F| <= growth * max |G_x|); a scenario that exceeds it is
+    reported like a singular block, so the reference's shim falls back to
+    its augmented strategy (ipm.cpp:502-507).  The fixtures' factors have
+    growth ~0.7: a limit of 1e10 passes, a limit of 1e-3 flags scenario 0."""
+    from conftest import case_path
+    fx = goldens["case118_N4_s005_it20"]
+    ctx = nat.Context(nat.Problem(case_path("case118"), 4, 0.05, 0))
+    ctx.factor_gx(fx["gx"])  # default limit: no error
+    monkeypatch.setenv("BIPM_GROWTH_LIMIT", "1e-3")
+    ctx2 = nat.Context(nat.Problem(case_path("case118"), 4, 0.05, 0))
+    with pytest.raises(nat.SingularBlockError) as e:
+        ctx2.factor_gx(fx["gx"])
+    assert e.value.block == 0
