@@ -583,7 +583,7 @@ void Engine::finish_reduce(double dw) {
   launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st);
 }
 
-bool Engine::factor_khat(double dw) {
+bool Engine::factor_khat(double dw, const std::function<void()>& regenerate) {
   const int n = pb.M.n_u;
   timed("cholesky", [&] { launch_shift_cholesky(khat.get(), n, chol_info.get(), nullptr, st); });
   int info[8] = {0};
@@ -599,7 +599,10 @@ bool Engine::factor_khat(double dw) {
   // reports too (neg > 0): reject without factoring again
   const double tol = 4.0 * n * 2.220446049250313e-16 * std::max(1.0, kinf);
   if (!(piv > -tol) && !force_bk) return false;
-  finish_reduce(dw);  // K_hat again: the Cholesky overwrote it
+  if (regenerate)  // K_hat again: the Cholesky overwrote it
+    regenerate();
+  else
+    finish_reduce(dw);
   timed("cholesky", [&] {
     launch_bk_factor(khat.get(), n, bk_ipiv.get(), bk_state.get(), bk_inertia.get(), st);
   });

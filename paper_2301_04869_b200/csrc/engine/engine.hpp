@@ -7,6 +7,7 @@
 // linalg.hpp:116) and run entirely on the device stream.
 #pragma once
 
+#include <functional>
 #include <map>
 #include <memory>
 #include <string>
@@ -162,7 +163,9 @@ class Engine {
   // dw) and the attempt is accepted, and later solved with the LDL' factors,
   // iff BK reports neg = 0 and zero = 0.  BIPM_FORCE_BK=1 takes that path on
   // every Cholesky failure (tests).
-  bool factor_khat(double dw);
+  // regenerate: writes K_hat again for the Bunch-Kaufman factorisation
+  // (default: finish_reduce(dw) from the partial slabs)
+  bool factor_khat(double dw, const std::function<void()>& regenerate = {});
   void solve_khat(double* d_vec);
   bool khat_bk = false;       // the accepted factor is Bunch-Kaufman (else Cholesky)
   bool force_bk = false;

@@ -1,5 +1,6 @@
 #include "kkt_step.hpp"
 
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -32,6 +33,11 @@ KktStep::KktStep(Engine& eng, int rounds) : refine_rounds(rounds), e(eng), io(en
   rhat2_part.resize(size_t(d.M) * nu);
   partial.resize(600 * 16);  // up to 592 blocks x 16 reduction slots
   scal.resize(32);
+  khat0.resize(nu * nu);
+  khat1.resize(nu * nu);
+  rhs0.resize(nu);
+  rhs1.resize(nu);
+  if (const char* v = std::getenv("BIPM_RETRY_EXACT")) exact_retries = std::atoi(v) != 0;
 }
 
 // base + sum over scenarios of part (and over ranks when sharded)
@@ -85,22 +91,45 @@ void KktStep::check_factor(const DArr<int>* interior_flag) {
                 sing);
 }
 
-bool KktStep::attempt(double dw) {
+bool KktStep::attempt(double dw, int k) {
   Engine::Bundle& bd = e.bd();
-  ++reductions;
-  // the rhs reduction only reads the factors and the condensed blocks: it runs
-  // on a side stream beside the Schur reduction (filling the SMs of its last
-  // wave) and joins before the rhs is used
-  e.reduce_rhs_fork(dw, rhs_sum.get());
-  e.reduce_local(dw);
-  e.finish_reduce(dw);
-  e.reduce_rhs_join(rhs_sum.get());
+  const size_t nn = size_t(d.n_u) * d.n_u;
+  auto copy = [&](DArr<double>& dst, const double* src, size_t n) {
+    cuda_check(cudaMemcpyAsync(dst.get(), src, n * sizeof(double), cudaMemcpyDeviceToDevice, e.st),
+               "copy");
+  };
+  const bool mix = k >= 2 && !exact_retries && dw1 != dw0;
+  const double t = mix ? (dw - dw0) / (dw1 - dw0) : 0.0;
+  auto mix_khat = [&] {
+    launch_affine_mix(khat0.get(), khat1.get(), t, (long long)nn, e.khat.get(), e.st);
+  };
+  if (mix) {
+    // K_hat(dw), rhs(dw) on the line through the first two attempts
+    mix_khat();
+    launch_affine_mix(rhs0.get(), rhs1.get(), t, d.n_u, rhs_sum.get(), e.st);
+    ++mixed;
+  } else {
+    ++reductions;
+    // the rhs reduction only reads the factors and the condensed blocks: it
+    // runs on a side stream beside the Schur reduction (filling the SMs of
+    // its last wave) and joins before the rhs is used
+    e.reduce_rhs_fork(dw, rhs_sum.get());
+    e.reduce_local(dw);
+    e.finish_reduce(dw);
+    e.reduce_rhs_join(rhs_sum.get());
+    if (k <= 1 && !exact_retries) {  // the factor overwrites K_hat: keep it
+      copy(k == 0 ? khat0 : khat1, e.khat.get(), nn);
+      copy(k == 0 ? rhs0 : rhs1, rhs_sum.get(), size_t(d.n_u));
+      (k == 0 ? dw0 : dw1) = dw;
+    }
+  }
   // refinement scale (independent of the factor) rides on the Cholesky sync
   launch_rhs_scale(d, r1x.get(), r1u.get(), e.r2.get(), bd.g.get(), e.r4.get(), partial.get(),
                    scal.get() + 20, e.st);
   io.allred(scal.get() + 20, 1, RedOpKind::kMax);
   io.fetch_async(scal.get() + 20, 40);
-  if (!e.factor_khat(dw)) return false;
+  if (!e.factor_khat(dw, mix ? std::function<void()>(mix_khat) : std::function<void()>()))
+    return false;
   const double scale = io.pinned(40);
   // solve_with(c, first_sum): p_u, then state/adjoint and slack/dual recovery
   launch_pu_rhs(d.n_u, rhs_sum.get(), e.rhat2.get(), p[1].get(), true, e.st);
@@ -170,12 +199,13 @@ void KktStep::solve(double& delta_w_last, const RegOptions& reg) {
   corrections = 0;
   refinements = 0;
   double dw = 0.0;
-  if (!attempt(0.0)) {
+  int k = 0;
+  if (!attempt(0.0, k++)) {
     dw = delta_w_last == 0 ? reg.delta_w0
                            : std::max(reg.delta_w_min, delta_w_last * reg.kappa_minus);
     for (;;) {
       ++corrections;
-      if (attempt(dw)) {
+      if (attempt(dw, k++)) {
         delta_w_last = dw;
         break;
       }

@@ -35,8 +35,15 @@ class KktStep {
   DArr<double> p[5];
   int corrections = 0, refinements = 0;
   double last_dw = 0;        // delta_w of the accepted attempt
-  long long reductions = 0;  // K_hat assemblies (every attempt)
+  long long reductions = 0;  // Schur reductions run (full K_hat assemblies)
+  long long mixed = 0;       // attempts whose K_hat came from the affine identity
   int refine_rounds = 3;
+  // K_hat and the reduced rhs are affine in delta_w (K~_xx = K_xx +
+  // diag(sigma_x + dw): K_hat(dw) = K_hat(0) + dw (I + sum T'T)),
+  // so from the third attempt of a step on they are interpolated from the
+  // first two reductions instead of re-running the reduction (kkt.cpp:954-959
+  // re-reduces every attempt).  BIPM_RETRY_EXACT=1 re-reduces every attempt.
+  bool exact_retries = false;
 
   // condense (kkt.cpp:123-170): K blocks and rhat1 / rhat2 / rhat3 (= g)
   void condense();
@@ -53,7 +60,7 @@ class KktStep {
   DevStep step_view() { return view(p); }
 
  private:
-  bool attempt(double dw);
+  bool attempt(double dw, int k);
   void condensed_u_sum(const double* part, const double* base, double* out);
   DevStep view(DArr<double>* s) {
     return DevStep{s[0].get(), s[1].get(), s[2].get(), s[3].get(), s[4].get()};
@@ -66,6 +73,8 @@ class KktStep {
   DArr<double> o1x, o1u, o2, o3, o4, o1u_part;
   DArr<double> c_rhat1, c_rhat2, rhs_sum, red_u, dd_u, rhat2_part;
   DArr<double> partial, scal;
+  DArr<double> khat0, khat1, rhs0, rhs1;  // attempts 0 and 1 of the current step
+  double dw0 = 0.0, dw1 = 0.0;
 };
 
 }  // namespace bipm

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <queue>
 
 namespace bipm {
 
@@ -15,6 +16,7 @@ int val_alloc(int count) { return count > 0 ? round16((count + 1) * 8) : 0; }
 struct Builder {
   StreamProgram& S;
   const int max_bytes;
+  std::vector<int> group;  // row -> warp of its subtree (-1: team levels); empty: none
   int warp_rr = 0;  // round-robin position of the next unit chunk (all-warp steps)
   int last_team = 16;
   struct Pending {
@@ -24,11 +26,13 @@ struct Builder {
     int val_arr = -1, val_off = 0, val_count = 0;
     int x_arr = -1, x_off = 0, x_count = 0;
     std::vector<int> levels;  // sweep steps: 4 ints per level (unit_begin, unit_end, lg, barrier)
+    std::vector<int> dir;     // warp-local sweeps: level range per consumer warp
   };
 
   // column entries are 16-bit panel rows, padded to 16 bytes
-  static int pat_bytes(int n_items, int n_ent, int n_lev = 0) {
-    return 4 * kStepHeaderInts + 16 * n_lev + 16 * n_items + 2 * ((n_ent + 7) & ~7);
+  static int pat_bytes(int n_items, int n_ent, int n_lev = 0, int dir_ints = 0) {
+    return 4 * kStepHeaderInts + round16(4 * dir_ints) + 16 * n_lev + 16 * n_items +
+           2 * ((n_ent + 7) & ~7);
   }
   // lanes per work unit: all units in one pass of `lanes` threads, and at
   // least ~3 entries per lane
@@ -52,7 +56,7 @@ struct Builder {
     const int n_col = (int(p.col.size()) + 7) & ~7;  // 16-bit entries
     StepIssue is{};
     is.pat_off = int(S.pat.size());
-    is.pat_bytes = pat_bytes(n_items, int(p.col.size()), n_lev);
+    is.pat_bytes = pat_bytes(n_items, int(p.col.size()), n_lev, int(p.dir.size()));
     const int par = (p.val_count > 0 ? ((p.val_off & 1) | (int(S.stride[p.val_arr] & 1) << 1)) : 0) |
                     (p.x_count > 0 ? (((p.x_off & 1) << 2) | (int(S.stride[p.x_arr] & 1) << 3)) : 0);
     // work units and lanes of the all-warp steps; rows become panel words
@@ -66,7 +70,7 @@ struct Builder {
       units = p.aux1 * NG;
       lg = lanes_log2(units, p.val_count / std::max(1, p.aux1), S.consumers);
     }
-    if (p.kind == kStepSweep || p.kind == kStepSpmv)
+    if (p.kind == kStepSweep || p.kind == kStepSweepW || p.kind == kStepSpmv)
       for (int it = 0; it < n_items; ++it)
         p.items[size_t(it) * 4] = panel_word(p.items[size_t(it) * 4], K);
     // columns stay panel ROWS (16 bits; the kernel forms the panel word)
@@ -80,6 +84,10 @@ struct Builder {
     int hdr[kStepHeaderInts] = {p.kind, p.flags, n_items, n_col, p.aux0, p.aux1, p.val_count,
                                 par, lg, units, warp0, n_lev};
     S.pat.insert(S.pat.end(), hdr, hdr + kStepHeaderInts);
+    if (!p.dir.empty()) {
+      S.pat.insert(S.pat.end(), p.dir.begin(), p.dir.end());
+      while (S.pat.size() & 3) S.pat.push_back(0);  // 16-byte alignment
+    }
     S.pat.insert(S.pat.end(), p.levels.begin(), p.levels.end());
     S.pat.insert(S.pat.end(), p.items.begin(), p.items.end());
     for (int i = 0; i < n_col; i += 2) {
@@ -121,6 +129,32 @@ struct Builder {
         level_diag.push_back(diag);
       }
     }
+    // the subtree rows leave the team levels for the warp-local part: per
+    // warp, its rows grouped by level (rows of one level are independent)
+    const int nw = S.consumers / 32;
+    const size_t nws = static_cast<size_t>(nw);
+    std::vector<std::vector<std::vector<Unit>>> wl(nws);
+    if (!group.empty()) {
+      std::vector<std::vector<Unit>> upper;
+      for (auto& us : levels) {
+        std::vector<std::vector<Unit>> per(nws);
+        std::vector<Unit> up;
+        for (const Unit& u : us) {
+          const int g = group[size_t(u.row)];
+          (g >= 0 ? per[size_t(g)] : up).push_back(u);
+        }
+        for (int w = 0; w < nw; ++w)
+          if (!per[size_t(w)].empty()) wl[size_t(w)].push_back(std::move(per[size_t(w)]));
+        if (!up.empty()) upper.push_back(std::move(up));
+      }
+      levels = std::move(upper);
+      level_diag.assign(levels.size(), diag);
+    }
+    bool any_wl = false;
+    for (const auto& v : wl) any_wl = any_wl || !v.empty();
+    // forward sweeps (L, U'): the subtrees first, the levels above them after;
+    // backward sweeps (U, L'): the other way round
+    if (any_wl && sw.forward) warp_local(wl, diag, sw, slot_of_t);
     if (with_tail) {  // the tail rows are independent of each other
       std::vector<Unit> us;
       for (size_t it = 0; it < sw.tail_items.size() / 4; ++it) {
@@ -207,11 +241,172 @@ struct Builder {
       }
     }
     flush();
+    if (any_wl && !sw.forward) warp_local(wl, diag, sw, slot_of_t);
     last_team = 16;  // the steps after a sweep start with an all-consumer barrier
+  }
+
+  // Warp-local part of a sweep: kStepSweepW steps, each holding the next
+  // levels of every warp (round robin, one level per warp per round, while
+  // the step fits).  The first step synchronises all consumers (the rows it
+  // reads were written by other warps); the warps then run without barriers.
+  template <typename Unit>
+  void warp_local(const std::vector<std::vector<std::vector<Unit>>>& wl, bool diag,
+                  const SweepPlan& sw, const std::vector<idx>& slot_of_t) {
+    const int K = S.K, NG = K > kStreamUnitCols ? K / kStreamUnitCols : 1;
+    const int nw = S.consumers / 32;
+    std::vector<size_t> pos(size_t(nw), 0);
+    bool first = true;
+    for (;;) {
+      struct WB {
+        std::vector<std::vector<int>> lev_items;  // per level: row, local col begin, end
+        std::vector<std::vector<int>> lev_col;
+        std::vector<std::vector<idx>> lev_slot;
+        std::vector<int> lev_lg;
+      };
+      std::vector<WB> wb(static_cast<size_t>(nw));
+      int n_items = 0, n_ent = 0, n_lev = 0;
+      for (bool progress = true; progress;) {
+        progress = false;
+        for (int w = 0; w < nw; ++w) {
+          if (pos[size_t(w)] >= wl[size_t(w)].size()) continue;
+          const auto& us = wl[size_t(w)][pos[size_t(w)]];
+          int ents = 0, max_ent = 0;
+          for (const Unit& u : us) {
+            ents += int(u.e - u.b);
+            max_ent = std::max(max_ent, int(u.e - u.b) - (diag ? 1 : 0));
+          }
+          const int bytes = pat_bytes(n_items + int(us.size()), n_ent + ents, n_lev + 1, 2 * nw) +
+                            val_alloc(n_ent + ents);
+          if (n_lev > 0 && bytes > max_bytes) continue;
+          WB& b = wb[size_t(w)];
+          std::vector<int> it, col;
+          std::vector<idx> sl;
+          for (const Unit& u : us) {
+            const int beg = int(col.size());
+            for (idx t = u.b; t < u.e; ++t) {
+              col.push_back(sw.col[size_t(t)]);
+              sl.push_back(slot_of_t[size_t(t)]);
+            }
+            it.insert(it.end(), {u.row, beg, int(col.size()), 0});
+          }
+          b.lev_items.push_back(std::move(it));
+          b.lev_col.push_back(std::move(col));
+          b.lev_slot.push_back(std::move(sl));
+          b.lev_lg.push_back(lanes_log2(int(us.size()) * NG, max_ent, 32));
+          ++pos[size_t(w)];
+          ++n_lev;
+          n_items += int(us.size());
+          n_ent += ents;
+          progress = true;
+        }
+      }
+      if (n_lev == 0) break;
+      Pending p{kStepSweepW, (diag ? kFlagDiag : 0) | (first ? kFlagPre : 0), 0, 0, {}, {}};
+      p.dir.assign(size_t(2 * nw), 0);
+      std::vector<idx> slots;
+      for (int w = 0; w < nw; ++w) {
+        const WB& b = wb[size_t(w)];
+        p.dir[size_t(2 * w)] = int(p.levels.size() / 4);
+        for (size_t L = 0; L < b.lev_items.size(); ++L) {
+          const int ub = int(p.items.size() / 4), c0 = int(p.col.size());
+          const auto& it = b.lev_items[L];
+          for (size_t q = 0; q < it.size(); q += 4)
+            p.items.insert(p.items.end(), {it[q], c0 + it[q + 1], c0 + it[q + 2], 0});
+          p.col.insert(p.col.end(), b.lev_col[L].begin(), b.lev_col[L].end());
+          slots.insert(slots.end(), b.lev_slot[L].begin(), b.lev_slot[L].end());
+          const int ue = int(p.items.size() / 4);
+          p.levels.insert(p.levels.end(), {ub * NG, ue * NG, b.lev_lg[L], 0});
+        }
+        p.dir[size_t(2 * w + 1)] = int(p.levels.size() / 4);
+      }
+      if (S.vs_src.size() & 1) S.vs_src.push_back(-1);
+      p.val_arr = kArrSweep;
+      p.val_off = int(S.vs_src.size());
+      p.val_count = int(p.col.size());
+      S.vs_src.insert(S.vs_src.end(), slots.begin(), slots.end());
+      emit(p);
+      ++S.n_sweep_steps;
+      first = false;
+    }
+    last_team = -1;  // the team levels after the subtrees start with a barrier
   }
 };
 
 }  // namespace
+
+std::vector<int> subtree_groups(const LuPlan& L, int nwarps) {
+  const idx n = L.n, t0 = L.t0;
+  std::vector<int> group(size_t(n), -1);
+  if (nwarps <= 0 || t0 <= 0) return group;
+  // elimination forest of the non-tail rows: parent(j) = first row i > j with
+  // L(i, j) != 0 (rows in the tail end the forest)
+  std::vector<idx> parent(size_t(t0), -1);
+  for (idx i = 0; i < n; ++i)
+    for (idx q = L.l_ptr[size_t(i)]; q < L.l_ptr[size_t(i) + 1]; ++q) {
+      const idx j = L.l_col[size_t(q)];
+      if (j < t0 && (parent[size_t(j)] < 0 || i < parent[size_t(j)])) parent[size_t(j)] = i;
+    }
+  const size_t t0s = static_cast<size_t>(t0);
+  std::vector<std::vector<idx>> kids(t0s);
+  std::vector<idx> roots;
+  for (idx j = 0; j < t0; ++j) {
+    if (parent[size_t(j)] >= 0 && parent[size_t(j)] < t0)
+      kids[size_t(parent[size_t(j)])].push_back(j);
+    else
+      roots.push_back(j);
+  }
+  // work of a row: its entries in the four sweeps (L, U each twice) + 1
+  std::vector<double> sub(size_t(t0), 0.0);
+  double total = 0.0;
+  for (idx j = 0; j < t0; ++j) {  // children precede parents
+    sub[size_t(j)] += 1.0 + (L.l_ptr[size_t(j) + 1] - L.l_ptr[size_t(j)]) +
+                      (L.u_ptr[size_t(j) + 1] - L.u_ptr[size_t(j)]);
+    total += 1.0 + (L.l_ptr[size_t(j) + 1] - L.l_ptr[size_t(j)]) +
+             (L.u_ptr[size_t(j) + 1] - L.u_ptr[size_t(j)]);
+    if (parent[size_t(j)] >= 0 && parent[size_t(j)] < t0) sub[size_t(parent[size_t(j)])] += sub[size_t(j)];
+  }
+  // split the heaviest subtree (its root joins the team levels) until the
+  // pieces are small enough to balance over the warps
+  static const double pieces_per_warp = [] {
+    const char* e = std::getenv("BIPM_SUBTREE_PIECES");
+    return e ? std::max(1.0, std::atof(e)) : 4.0;
+  }();
+  const double cap = total / (nwarps * pieces_per_warp);
+  auto cmp = [&](idx a, idx b) { return sub[size_t(a)] < sub[size_t(b)]; };
+  std::priority_queue<idx, std::vector<idx>, decltype(cmp)> heap(cmp);
+  for (idx r : roots) heap.push(r);
+  std::vector<idx> pieces;
+  while (!heap.empty()) {
+    const idx r = heap.top();
+    heap.pop();
+    if (sub[size_t(r)] <= cap || kids[size_t(r)].empty()) {
+      pieces.push_back(r);
+      continue;
+    }
+    for (idx c : kids[size_t(r)]) heap.push(c);  // r stays with the team levels
+  }
+  // longest processing time first onto the least loaded warp
+  std::sort(pieces.begin(), pieces.end(),
+            [&](idx a, idx b) { return sub[size_t(a)] > sub[size_t(b)]; });
+  std::vector<double> load(size_t(nwarps), 0.0);
+  std::vector<int> owner(size_t(t0), -1);
+  for (idx r : pieces) {
+    const int w = int(std::min_element(load.begin(), load.end()) - load.begin());
+    load[size_t(w)] += sub[size_t(r)];
+    owner[size_t(r)] = w;
+  }
+  // every row of a piece belongs to the piece root's warp (top-down: parents
+  // have larger indices, so walk rows from the top)
+  for (idx j = t0 - 1; j >= 0; --j) {
+    if (owner[size_t(j)] >= 0) {
+      group[size_t(j)] = owner[size_t(j)];
+      continue;
+    }
+    const idx pj = parent[size_t(j)];
+    if (pj >= 0 && pj < t0 && group[size_t(pj)] >= 0) group[size_t(j)] = group[size_t(pj)];
+  }
+  return group;
+}
 
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
@@ -234,7 +429,15 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   S.stride[kArrGuT] = gu.nnz();
   S.stride[kArrSigma] = n;
   // stride[kArrSweep] is fixed after the program is built (nnz_vs, even)
-  Builder B{S, S.max_step_bytes};
+  Builder B{S, S.max_step_bytes, {}};
+  // warp-local subtree sweeps: correct, measured no faster at 1354/256
+  // (23.5 -> 24.1 ms per reduction: the per-warp level chains, not the team
+  // barriers, bound the sweeps), so off unless BIPM_SUBTREE=1
+  static const int subtree_on = [] {
+    const char* e = std::getenv("BIPM_SUBTREE");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (subtree_on) B.group = subtree_groups(L, consumers / 32);
   using P = Builder::Pending;
 
   // factor slot of every entry of the four sweeps' direct value arrays

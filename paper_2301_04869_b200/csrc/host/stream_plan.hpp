@@ -27,13 +27,15 @@ enum StepKind : int {
   kStepSpmv = 4,      // S = -(K~_xx X) over a range of state rows
   kStepCopyBack = 5,  // X = S + K_xu V
   kStepDenseG = 6,    // X_T <- W X_T with W read from global memory (L2), one step
+  kStepSweepW = 7,    // warp-local levels of a sweep: each warp its own elimination subtrees
 };
 // kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
 enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };
 
 // Step pattern block: a 64-byte header (16 ints)
 //   {kind, flags, n_items, n_col, aux0, aux1, vcount, par, lg, n_units, warp0, n_lev, 0...}
-// then n_lev int4 level records (sweep steps), n_items int4 items and n_col
+// [warp-local sweeps: a directory of 2 ints per consumer warp = its level
+// record range] then n_lev int4 level records (sweep steps), n_items int4 items and n_col
 // 16-bit column entries (panel rows; the kernel forms the panel word).  All-warp steps (dense, spmv): a unit is (item, group of up to
 // 8 panel columns) served by 2^lg lanes, chunks of 32 >> lg units dealt to
 // the 16 consumer warps round robin from warp0.  Sweep steps: aux0 = T, the
@@ -93,6 +95,13 @@ struct StreamProgram {
   // statistics
   int n_sweep_steps = 0, n_dense_steps = 0, n_acc_steps = 0, n_spmv_steps = 0;
 };
+
+// Subtree-to-warp mapping of the non-tail elimination forest (the sweeps'
+// warp-local part): group[row] = consumer warp owning the row, -1 for rows
+// left to the team levels (the split nodes above the subtrees, the tail).
+// Every subtree is closed under the L / U' (descendants) and U / L'
+// (ancestors inside it) dependencies.  nwarps = 0: no warp-local part.
+std::vector<int> subtree_groups(const LuPlan& L, int nwarps);
 
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,

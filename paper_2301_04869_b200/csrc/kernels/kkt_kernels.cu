@@ -662,6 +662,12 @@ __global__ void sum_parts_kernel(const double* __restrict__ parts, int nparts, l
   out[j] = v;
 }
 
+__global__ void affine_mix_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                                  double t, long long len, double* out) {
+  const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (j < len) out[j] = a[j] + t * (b[j] - a[j]);
+}
+
 // ------------------------------------------------------ single-RHS kernels
 template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* scratch,
@@ -1045,6 +1051,14 @@ void launch_sum_parts(const double* parts, int nparts, long long len, double* ou
                                                           n_mat, sub_vec);
   note_launch();
   check_launch("sum_parts");
+}
+
+void launch_affine_mix(const double* a, const double* b, double t, long long len, double* out,
+                       cudaStream_t st) {
+  if (len <= 0) return;
+  affine_mix_kernel<<<int((len + 255) / 256), 256, 0, st>>>(a, b, t, len, out);
+  note_launch();
+  check_launch("affine_mix");
 }
 
 void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {

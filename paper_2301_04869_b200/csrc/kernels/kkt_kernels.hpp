@@ -44,6 +44,9 @@ void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st);
 
 // out[j] = sum_c parts[c][j] (fixed pairwise order) + (diag_add ? diag_add[u] + dw on the
 // diagonal of an n x n column-major matrix : 0); n_mat = n (0: plain vector of length len)
+// out = a + t (b - a) over len doubles (the inertia loop's affine K_hat(dw))
+void launch_affine_mix(const double* a, const double* b, double t, long long len, double* out,
+                       cudaStream_t st);
 void launch_sum_parts(const double* parts, int nparts, long long len, double* out,
                       const double* diag_add, double dw, int n_mat, const double* sub_vec,
                       cudaStream_t st);

@@ -37,7 +37,7 @@ void check_launch(const char* what) {
 }
 
 enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5,
-             kDenseG = 6 };
+             kDenseG = 6, kSweepW = 7 };
 constexpr int kStepHeaderIntsDev = 16;  // host/stream_plan.hpp kStepHeaderInts
 constexpr int kArrDenseDev = 1;         // host/stream_plan.hpp kArrDense
 
@@ -298,6 +298,63 @@ __device__ __forceinline__ void step_sweep(const Hdr& h, unsigned lev, unsigned 
     tr(200 + L);
     if (e.w && !(dbg & 2)) team_sync<C>(T);
     tr(300 + L);
+  }
+}
+
+// warp-local part of a triangular sweep (host/stream_plan.cpp, subtree
+// mapping): warp w runs its own levels [dir[w].x, dir[w].y) -- rows of the
+// elimination subtrees assigned to it -- separated by __syncwarp only.  The
+// subtrees are disjoint and closed under the sweep's dependencies, so no
+// other warp reads or writes these rows until the next all-consumer barrier.
+template <int K, int C>
+__device__ __forceinline__ void step_sweep_w(const Hdr& h, unsigned dir, unsigned lev,
+                                             unsigned items, unsigned col, unsigned v,
+                                             unsigned xb, int tid) {
+  using Pn = Panel<K>;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int dg = h.flags & 1;
+  const int2 d = make_int2(ldsi(dir + 8 * warp), ldsi(dir + 8 * warp + 4));
+  for (int L = d.x; L < d.y; ++L) {
+    const int4 e = ldsi4(lev + 16 * L);  // unit begin, unit end, lg
+    const int lg = e.z, g = 1 << lg, upw = 32 >> lg;
+    const int nch = (e.y - e.x + upw - 1) >> (5 - lg);
+    const int sub = lane & (g - 1);
+    for (int c = 0; c < nch; ++c) {
+      const int unit = e.x + c * upw + (lane >> lg);
+      const bool active = unit < e.y;
+      const int item = Pn::NG == 1 ? unit : unit / Pn::NG;
+      const int cg = Pn::NG == 1 ? 0 : unit % Pn::NG;
+      double a[Pn::CW];
+#pragma unroll
+      for (int q = 0; q < Pn::CW; ++q) a[q] = 0.0;
+      int4 m = make_int4(0, 0, 0, 0);
+      if (active) {
+        m = ldsi4(items + 16 * item);
+        int t = m.y + dg + sub;
+        for (; t + g < m.z; t += 2 * g) {
+          const int w0 = colw<K>(col, t), w1 = colw<K>(col, t + g);
+          const double v0 = lds1(v + 8 * t), v1 = lds1(v + 8 * (t + g));
+          Pn::fma(a, v0, xb, w0, cg);
+          Pn::fma(a, v1, xb, w1, cg);
+        }
+        if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, colw<K>(col, t), cg);
+      }
+      reduce_lanes<Pn::CW>(a, g);
+      if (active && sub == 0) {
+        double x[Pn::CW];
+        Pn::load(x, xb, m.x, cg);
+        if (dg) {
+          const double r = 1.0 / lds1(v + 8 * m.y);
+#pragma unroll
+          for (int q = 0; q < Pn::CW; ++q) x[q] = (x[q] - a[q]) * r;
+        } else {
+#pragma unroll
+          for (int q = 0; q < Pn::CW; ++q) x[q] -= a[q];
+        }
+        Pn::store(x, xb, m.x, cg);
+      }
+    }
+    __syncwarp();
   }
 }
 
@@ -606,7 +663,9 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
       const int4 h0 = ldsi4(base), h1 = ldsi4(base + 16), h2 = ldsi4(base + 32);
       h = Hdr{h0.x, h0.y, h0.z, h0.w, h1.x, h1.y, h1.z, h1.w, h2.x, h2.y, h2.z, h2.w};
     }
-    const unsigned lev = base + 4 * kStepHeaderIntsDev;
+    // warp-local sweeps carry a per-warp directory (2 ints per consumer warp)
+    const unsigned dir = base + 4 * kStepHeaderIntsDev;
+    const unsigned lev = dir + (h.kind == kSweepW ? ((8 * (C / 32) + 15) & ~15) : 0);
     const unsigned items = lev + 16 * h.n_lev;
     const unsigned col = items + 16 * h.n_items;
     const unsigned vals = col + 2 * h.n_col;
@@ -639,6 +698,9 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
       }
       case kSweep:
         step_sweep<K, C>(h, lev, items, col, v, xb, tid, tr, a.debug);
+        break;
+      case kSweepW:
+        step_sweep_w<K, C>(h, dir, lev, items, col, v, xb, tid);
         break;
       case kDense:
         step_dense<K, C>(h, v, xb, temp, a.t0, a.tl, tid);

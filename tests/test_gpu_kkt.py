@@ -40,6 +40,40 @@ def test_reduce_matches_reference_fixture(goldens, name):
         assert rerr <= KHAT_RTOL, f"{name} dw={dw}: rhs rel err {rerr:.3e}"
 
 
+@pytest.mark.parametrize("name", ["case1354pegase_N4_s005_it40", "case9241pegase_N2_s005_it2"])
+def test_reduce_matches_reference_fixture_pegase(goldens, name):
+    """K_hat and rhs at pegase scale on the reference's own near-convergence
+    (1354, iterate 40 of 55) and early (9241, iterate 2) values -- real,
+    ill-conditioned K_hat, not synthetic.  The 9241 fixture stores K_hat
+    compactly (tests/golden: four full columns, the diagonal, a +-1
+    projection and max|K_hat|; the whole matrix is 67 MB)."""
+    if name not in goldens:
+        pytest.skip(f"{name} not generated (tests/golden/make_golden.py --dumps2)")
+    fx = goldens[name]
+    m = fx.meta
+    p = nat.Problem(case_path(m["case"]), m["N"], m["sigma"], m["seed"])
+    ctx = nat.Context(p)
+    ctx.factor_gx(fx["gx"])
+    for sfx, dw in (("0", 0.0), ("dw", m["dw_probe"])):
+        khat, rhs = ctx.reduce(dw, **cond_arrays(fx))
+        ref_r = fx["rhs_" + sfx]
+        if ("khat_" + sfx) in fx:
+            ref_k = fx["khat_" + sfx].T
+            scale = np.abs(ref_k).max()
+            err = np.abs(khat - ref_k).max() / scale
+        else:
+            key = "khat_" + sfx + "__"
+            scale = float(fx[key + "absmax"][0])
+            n = khat.shape[0]
+            w = np.where(np.random.default_rng(12345).random(n) < 0.5, -1.0, 1.0)
+            err = max(np.abs(khat[:, fx[key + "colidx"]].T - fx[key + "cols"]).max(),
+                      np.abs(np.diag(khat) - fx[key + "diag"]).max(),
+                      np.abs(khat @ w - fx[key + "proj"]).max() / n) / scale
+        assert err <= KHAT_RTOL, f"{name} dw={dw}: K_hat rel err {err:.3e}"
+        rerr = np.abs(rhs - ref_r).max() / max(1.0, np.abs(ref_r).max())
+        assert rerr <= KHAT_RTOL, f"{name} dw={dw}: rhs rel err {rerr:.3e}"
+
+
 def synthetic_condensed(p, N, seed):
     """Seeded values on the problem's real patterns: diagonally weighted G_x
     (nonsingular), symmetric K_xx with a positive diagonal."""
