@@ -715,8 +715,14 @@ void Engine::upload_ad() {
   A.gs_ref = Mo.gs_ref;
   A.br_ref = keep(ad_i, P.branch_ref);
   A.gen_ref_other = keep(ad_i, P.gen_ref_other);
+  // the owned scenarios' constants, element-major ([width][M]) for the
+  // scenario-fastest AD kernels
   auto slice = [&](const std::vector<double>& all, idx width) {
-    return std::vector<double>(all.begin() + long(lo) * width, all.begin() + long(hi) * width);
+    std::vector<double> t(size_t(width) * size_t(M));
+    for (idx s = 0; s < M; ++s)
+      for (idx k = 0; k < width; ++k)
+        t[size_t(k) * size_t(M) + size_t(s)] = all[size_t(lo + s) * size_t(width) + size_t(k)];
+    return t;
   };
   pd_v.upload(slice(Mo.pd, Mo.nbus));
   qd_v.upload(slice(Mo.qd, Mo.nbus));
@@ -760,6 +766,9 @@ void Engine::upload_ad() {
   A.wxx = gat(P.wxx);
   A.wxu = gat(P.wxu);
   A.wuu = gat(P.wuu);
+  xt.resize(size_t(M) * size_t(Mo.n_x));
+  yt.resize(size_t(M) * size_t(Mo.n_x));
+  zt.resize(size_t(M) * size_t(std::max(1, Mo.m)));
   psi.resize(size_t(M) * size_t(A.n_b));
   dpart.resize(size_t(M) * size_t(std::max(1, A.n_dp)));
   wlane.resize(size_t(M) * size_t(A.n_b));
@@ -777,6 +786,9 @@ idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const d
   b.Y = dY;
   b.Z = dZ;
   b.obj_w = obj_w;
+  b.Xt = xt.get();
+  b.Yt = yt.get();
+  b.Zt = zt.get();
   b.psi = psi.get();
   b.dp = dpart.get();
   b.w = wlane.get();
@@ -805,6 +817,7 @@ idx Engine::eval_values(const double* dX, const double* du, double* df, double* 
   AdBuffers b{};
   b.X = dX;
   b.u = du;
+  b.Xt = xt.get();
   b.psi = psi.get();
   b.dp = dpart.get();
   b.f = df;

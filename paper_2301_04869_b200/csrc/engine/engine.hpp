@@ -101,7 +101,8 @@ class Engine {
   std::vector<DArr<int>> ad_i;
   std::vector<DArr<double>> ad_d;
   DevAd ad{};
-  DArr<double> psi, dpart, wlane, contrib;
+  DArr<double> psi, dpart, wlane, contrib;  // element-major AD scratch
+  DArr<double> xt, yt, zt;                   // element-major copies of the AD inputs
   DArr<int> bad;
   DArr<double> pd_v, qd_v, status_v;
   DArr<double> kxx, kxu, kuu;                  // condensed blocks

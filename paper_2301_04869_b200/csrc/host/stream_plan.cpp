@@ -65,7 +65,11 @@ struct Builder {
       max_ent = std::max(max_ent, p.items[size_t(it) * 4 + 2] - p.items[size_t(it) * 4 + 1]);
     if (p.kind == kStepSpmv) {
       units = n_items * NG;
-      lg = lanes_log2(units, max_ent, S.consumers);
+      static const int spmv_lanes = [] {
+        const char* e = std::getenv("BIPM_SPMV_LANES");
+        return e ? std::max(32, std::atoi(e)) : 0;
+      }();
+      lg = lanes_log2(units, max_ent, spmv_lanes > 0 ? spmv_lanes : S.consumers);
     } else if (p.kind == kStepDense) {
       units = p.aux1 * NG;
       lg = lanes_log2(units, p.val_count / std::max(1, p.aux1), S.consumers);

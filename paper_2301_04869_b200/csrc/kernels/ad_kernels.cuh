@@ -18,7 +18,7 @@ struct DevAd {
   double gs_ref;
   const double* brc;  // per branch: gff bff gft bft gtf btf gtt btt
   const int *br_ref, *gen_ref_other;
-  const double *pd_v, *qd_v, *status;  // [M][nbus], [M][nbus], [M][nbr]
+  const double *pd_v, *qd_v, *status;  // element-major: [nbus][M], [nbus][M], [nbr][M]
   const int *Lf_ptr, *Lf_ind, *Lg_ptr, *Lg_ind, *Lh_ptr, *Lh_ind;
   const double *Lf_val, *Lg_val, *Lh_val;
   int n_dp, n_c, c_bus, c_gen, c_slack, nsd;
@@ -30,7 +30,8 @@ struct DevAd {
 struct AdBuffers {
   const double *X, *u, *Y, *Z;  // [M][n_x], [n_u], [M][n_x], [M][m]
   double obj_w;
-  double *psi, *dp, *w, *c;     // scratch
+  double *Xt, *Yt, *Zt;         // element-major copies of X, Y, Z (scratch)
+  double *psi, *dp, *w, *c;     // element-major scratch: [n_b][M], [n_dp][M], [n_b][M], [n_c][M]
   double *f, *g, *h;            // [M], [M][n_x], [M][m]
   double *gx, *gu, *hx, *hu, *wxx, *wxu, *wuu, *grad;  // [M][nnz], grad [M][n_d]
   int* bad;                     // [M] non-finite flags
