@@ -206,7 +206,7 @@ def bench_ours(a, rank, world):
     if dist:
         dist.barrier()
     c1 = nat.counters()
-    groups = ["ad_bundle", "ad_values", "condense", "lu_refactor", "reduce_tiles", "reduce_rhs",
+    groups = ["ad_bundle", "ad_values", "condense", "lu_refactor", "reduce_pre", "reduce_tiles", "reduce_rhs",
               "cholesky", "recover_state"]
     kt = {g: ctx.kernel_time(g) for g in groups}
     ctx.profile(False)

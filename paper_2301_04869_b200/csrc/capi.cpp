@@ -103,6 +103,14 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
       {"lu_ft_src", &P.LU.ft_src},     {"lu_a_src", &P.LU.a_src},
       {"lu_dense_src0", &P.LU.dense_src[0]}, {"lu_dense_src1", &P.LU.dense_src[1]}};
   if (auto it = lu_more.find(name); it != lu_more.end()) return ints(*it->second);
+  if (name.rfind("reach_", 0) == 0) {  // presolved forward half (ReachPlan)
+    static thread_local ReachPlan R;
+    R = build_reach_plan(P.LU, P.D.g.u, P.D.g.u.cols);
+    const std::map<std::string, const std::vector<idx>*> rv = {
+        {"reach_yn_ptr", &R.yn_ptr}, {"reach_yn_row", &R.yn_row}, {"reach_op_ptr", &R.op_ptr},
+        {"reach_ops", &R.ops},       {"reach_ent", &R.ent}};
+    if (auto it = rv.find(name); it != rv.end()) return ints(*it->second);
+  }
   const std::map<std::string, const SweepPlan*> sweeps = {
       {"sL", &P.LU.sL}, {"sU", &P.LU.sU}, {"sUt", &P.LU.sUt}, {"sLt", &P.LU.sLt}};
   for (const auto& [pre, sw] : sweeps) {

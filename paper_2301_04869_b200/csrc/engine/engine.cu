@@ -277,6 +277,8 @@ void Engine::setup_stream() {
   // the same latency whatever its width, and smaller rings mean more steps.
   int cap = 1;
   while (cap < 32 && cap < n_u) cap *= 2;
+  if (const char* e = std::getenv("BIPM_PRESOLVE")) presolve = std::atoi(e) != 0;
+  if (presolve) rplan = build_reach_plan(L, D.g.u, n_u);
   const Csr gut = D.g.u.transpose_pattern(), kxut = D.kxu.out.transpose_pattern();
   if (const char* e = std::getenv("BIPM_STREAM_K")) cap = std::max(1, std::min(cap, std::atoi(e)));
   int force_c = 0;
@@ -285,7 +287,8 @@ void Engine::setup_stream() {
     int lc = 0;
     for (int j0 = 0; j0 < n_u; j0 += K) {
       const int j1 = std::min(n_u, j0 + K);
-      const int a = gut.ptr[size_t(j1)] - gut.ptr[size_t(j0)];
+      const int a = presolve ? rplan.yn_ptr[size_t(j1)] - rplan.yn_ptr[size_t(j0)]
+                             : gut.ptr[size_t(j1)] - gut.ptr[size_t(j0)];
       const int b = kxut.ptr[size_t(j1)] - kxut.ptr[size_t(j0)];
       lc = std::max(lc, ((a + 1) & ~1) + ((b + 1) & ~1));
     }
@@ -314,7 +317,25 @@ void Engine::setup_stream() {
   }
   const int K = best.K, ring = best.ring, list_cap = best.list_cap;
   sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, best.C, ring,
-                               kStreamLookahead);
+                               kStreamLookahead, presolve);
+  if (presolve) {
+    rp_op_ptr.upload(rplan.op_ptr);
+    rp_ops.upload(rplan.ops.empty() ? std::vector<idx>(4, 0) : rplan.ops);
+    rp_ent.upload(rplan.ent.empty() ? std::vector<idx>(2, 0) : rplan.ent);
+    rp_yn_ptr.upload(rplan.yn_ptr);
+    rp_yn_row.upload(rplan.yn_row.empty() ? std::vector<idx>{0} : rplan.yn_row);
+    int ymax = 1;
+    for (idx u = 0; u < n_u; ++u)
+      ymax = std::max(ymax, int(rplan.yn_ptr[size_t(u) + 1] - rplan.yn_ptr[size_t(u)]));
+    rdev = ReachDev{int(n_u), int(L.tl), int(rplan.ldy), int(rplan.nnz_yn), ymax,
+                    rp_op_ptr.get(), reinterpret_cast<const int4*>(rp_ops.get()),
+                    reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get()};
+    const size_t Ms = size_t(M);
+    YN.resize(Ms * size_t(std::max<idx>(1, rplan.nnz_yn)));
+    YT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
+    XT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
+    XT.zero(st);
+  }
   sp_pat.upload(sprog.pat);
   {
     std::vector<int> iss;
@@ -367,6 +388,13 @@ void Engine::setup_stream() {
   sl.kxu = kxu_p.v;
   sl.kuu = kuu_p.v;
   sl.iperm = lu.iperm;
+  sl.presolved = presolve ? 1 : 0;
+  sl.ldy = int(rplan.ldy);
+  sl.nnz_yn = int(rplan.nnz_yn);
+  sl.yn_ptr = presolve ? rp_yn_ptr.get() : nullptr;
+  sl.yn_row = presolve ? rp_yn_row.get() : nullptr;
+  sl.yn_v = presolve ? YN.get() : nullptr;
+  sl.xt = presolve ? XT.get() : nullptr;
   const int tiles = (n_u + K - 1) / K;
   sp_scratch.resize(size_t(tiles) * sl.nchunks * (size_t(n_x) * K + size_t(list_cap)));
 }
@@ -435,6 +463,18 @@ void Engine::reduce_local(double dw) {
     const DerivPlan& D = pb.D;
     const int n_u = pb.M.n_u;
     double* kuu_part = red_partial.get() + size_t(sl.nchunks) * n_u * n_u;
+    if (presolve) {
+      // forward half for all columns: y_N, y_T (reach_solve), X_T = W y_T
+      timed("reduce_pre", [&] {
+        launch_reach_solve(rdev, M, F.get(), pb.LU.nnz_f, bd().gu.get(), nnz(D.g.u), YN.get(),
+                           YT.get(), st);
+        const int tl = int(pb.LU.tl);
+        GemmTN g{tl, n_u, tl, int(M), Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
+                 YT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
+                 XT.get(), rplan.ldy, (long long)n_u * rplan.ldy};
+        launch_gemm_tn(g, st);
+      });
+    }
     timed("reduce_tiles", [&] {
       launch_gather_values(kxu.get(), nnz(D.kxu.out), sp_kxu_slot.get(), int(nnz(D.kxu.out)),
                            kxu_t.get(), nnz(D.kxu.out), M, st);

@@ -19,6 +19,7 @@
 #include "../host/stream_plan.hpp"
 #include "../kernels/ad_launch.hpp"
 #include "../kernels/kkt_kernels.hpp"
+#include "../kernels/reach_gemm.hpp"
 #include "../kernels/reduce_stream.hpp"
 #include "comm.hpp"
 #include "device_array.hpp"
@@ -118,6 +119,14 @@ class Engine {
   StreamLaunch sl{};
   DArr<int> sp_pat, sp_issue, sp_ring, sp_vs_src, sp_kxu_slot, sp_gu_slot, kuu_row, kuu_col;
   DArr<double> VS, Dp, kxu_t, gu_t, sp_scratch;  // Dp: W, W' with padded rows
+  // presolved forward half (host/stream_plan.hpp ReachPlan, reach_gemm.cu):
+  // y_N [M][nnz_yn], y_T and X_T = W y_T [M][n_u][ldy]; BIPM_PRESOLVE=0 runs
+  // the L sweep and the first dense product inside every column tile instead
+  bool presolve = true;
+  ReachPlan rplan;
+  ReachDev rdev{};
+  DArr<int> rp_op_ptr, rp_ops, rp_ent, rp_yn_ptr, rp_yn_row;
+  DArr<double> YN, YT, XT;
   int red_parts = 0;  // partial K_hat slabs summed by finish_reduce
   // ---- reduction workspace (tile kernel, BIPM_REDUCE=tiles)
   ReduceLaunch red{};

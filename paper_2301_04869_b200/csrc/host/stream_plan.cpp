@@ -412,9 +412,81 @@ std::vector<int> subtree_groups(const LuPlan& L, int nwarps) {
   return group;
 }
 
+ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u) {
+  ReachPlan R;
+  const idx n = L.n, t0 = L.t0;
+  R.n_u = n_u;
+  R.t0 = t0;
+  R.tl = L.tl;
+  R.ldy = dense_ld(L.tl);
+  const Csr gut = gu.transpose_pattern();  // column u -> (state row, G_u slot)
+  R.yn_ptr.assign(size_t(n_u) + 1, 0);
+  R.op_ptr.assign(size_t(n_u) + 1, 0);
+  std::vector<idx> local(size_t(n), -1), b_of(size_t(n), -1);
+  std::vector<std::vector<std::pair<idx, idx>>> in(static_cast<size_t>(n));  // row -> (col, slot)
+  std::vector<idx> reach, touched_tail;
+  for (idx u = 0; u < n_u; ++u) {
+    reach.clear();
+    touched_tail.clear();
+    for (idx k = gut.ptr[size_t(u)]; k < gut.ptr[size_t(u) + 1]; ++k) {
+      const idx r = L.iperm[size_t(gut.ind[size_t(k)])];
+      b_of[size_t(r)] = idx(gut.val[size_t(k)]);
+      if (r < t0 && local[size_t(r)] < 0) {
+        local[size_t(r)] = 0;
+        reach.push_back(r);
+      }
+      if (r >= t0) touched_tail.push_back(r);
+    }
+    // reach of the G_u rows in the graph of L (column c feeds rows r > c with
+    // L(r, c) != 0), the non-tail part only; ascending order is a topological
+    // order of the lower-triangular dependencies
+    for (size_t h = 0; h < reach.size(); ++h) {
+      const idx c = reach[h];
+      for (idx q = L.lt_ptr[size_t(c)]; q < L.lt_ptr[size_t(c) + 1]; ++q) {
+        const idx r = L.lt_row[size_t(q)];
+        if (r < t0 && local[size_t(r)] < 0) {
+          local[size_t(r)] = 0;
+          reach.push_back(r);
+        }
+      }
+    }
+    std::sort(reach.begin(), reach.end());
+    for (size_t k = 0; k < reach.size(); ++k) local[size_t(reach[k])] = idx(k);
+    for (idx c : reach)
+      for (idx q = L.lt_ptr[size_t(c)]; q < L.lt_ptr[size_t(c) + 1]; ++q) {
+        const idx r = L.lt_row[size_t(q)];
+        if (r >= t0 && in[size_t(r)].empty() && b_of[size_t(r)] < 0) touched_tail.push_back(r);
+        in[size_t(r)].push_back({c, L.lt_slot[size_t(q)]});
+      }
+    std::sort(touched_tail.begin(), touched_tail.end());
+    touched_tail.erase(std::unique(touched_tail.begin(), touched_tail.end()), touched_tail.end());
+    auto emit_op = [&](idx r, idx dest) {
+      auto& e = in[size_t(r)];
+      std::sort(e.begin(), e.end());  // row order of L, like the full sweep
+      const idx eb = idx(R.ent.size() / 2);
+      for (const auto& [c, slot] : e) R.ent.insert(R.ent.end(), {local[size_t(c)], slot});
+      R.ops.insert(R.ops.end(), {dest, b_of[size_t(r)], eb, idx(R.ent.size() / 2)});
+      R.fmas += idx(e.size());
+      e.clear();
+    };
+    for (size_t k = 0; k < reach.size(); ++k) {
+      emit_op(reach[k], idx(k));
+      R.yn_row.push_back(reach[k]);
+    }
+    for (idx t : touched_tail) emit_op(t, -1 - (t - t0));
+    R.yn_ptr[size_t(u) + 1] = idx(R.yn_row.size());
+    R.op_ptr[size_t(u) + 1] = idx(R.ops.size() / 4);
+    for (idx r : reach) local[size_t(r)] = -1;
+    for (idx k = gut.ptr[size_t(u)]; k < gut.ptr[size_t(u) + 1]; ++k)
+      b_of[size_t(L.iperm[size_t(gut.ind[size_t(k)])])] = -1;
+  }
+  R.nnz_yn = idx(R.yn_row.size());
+  return R;
+}
+
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
-                                   int lookahead_max) {
+                                   int lookahead_max, bool presolved) {
   StreamProgram S;
   S.K = K;
   S.consumers = consumers;
@@ -539,9 +611,13 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   };
 
   // scatter and copy-back synchronise internally (before) and after
-  B.emit(P{kStepScatter, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
-  B.sweep(L.sL, slot_L, false, true, 0);
-  dense(0);
+  if (presolved) {
+    B.emit(P{kStepScatterY, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+  } else {
+    B.emit(P{kStepScatter, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+    B.sweep(L.sL, slot_L, false, true, 0);
+    dense(0);
+  }
   B.sweep(L.sU, slot_U, true, false, 0);
   acc(kxu, S.kxu_t_slot);
   spmv();

@@ -28,6 +28,7 @@ enum StepKind : int {
   kStepCopyBack = 5,  // X = S + K_xu V
   kStepDenseG = 6,    // X_T <- W X_T with W read from global memory (L2), one step
   kStepSweepW = 7,    // warp-local levels of a sweep: each warp its own elimination subtrees
+  kStepScatterY = 8,  // X = (y_N, X_T) tile columns (presolved forward half, ReachPlan)
 };
 // kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
 enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };
@@ -103,8 +104,34 @@ struct StreamProgram {
 // (ancestors inside it) dependencies.  nwarps = 0: no warp-local part.
 std::vector<int> subtree_groups(const LuPlan& L, int nwarps);
 
+// Forward half of X = G_x^{-1} P G_u solved once per scenario for all n_u
+// columns (kernels/reach_gemm.cu), ahead of the streamed reduction:
+//   y_N = L_NN^{-1} (P G_u)_N     sparse: column u is nonzero only on the
+//                                 reach of its G_u rows in the graph of L
+//   y_T = (P G_u)_T - L_TN y_N    the tail rows (dense, ldy per column)
+//   X_T = W y_T                   one batched DMMA GEMM (W = (L_TT U_TT)^{-1})
+// A column tile of the reduction then starts from (y_N, X_T) instead of
+// running the L sweep over all rows and the first dense product per tile:
+// the reach of one G_u column is a few etree paths (1354: 63 rows of 2140 per
+// 8-column tile), and W is read once per scenario instead of once per tile.
+struct ReachPlan {
+  idx n_u = 0, t0 = 0, tl = 0, ldy = 0;
+  idx nnz_yn = 0;                // y_N entries per scenario (column-major by u)
+  std::vector<idx> yn_ptr;       // [n_u + 1]
+  std::vector<idx> yn_row;       // permuted state row (< t0) of each entry
+  // per column u, ops [op_ptr[u], op_ptr[u+1]) in dependency order:
+  // {dest, G_u slot or -1, entry begin, entry end}; dest >= 0: y_N entry
+  // yn_ptr[u] + dest, dest < 0: tail row -1 - dest (y_T); entries
+  // {source y_N entry (local to the column), factor slot of L}
+  std::vector<idx> op_ptr, ops, ent;
+  long long fmas = 0;            // entries per scenario (work measure)
+};
+ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u);
+
+// presolved: the program starts from (y_N, X_T) (ReachPlan) -- a scatter of
+// the tile's columns of both, no L sweep, no first dense product
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
-                                   int lookahead_max);
+                                   int lookahead_max, bool presolved = false);
 
 }  // namespace bipm

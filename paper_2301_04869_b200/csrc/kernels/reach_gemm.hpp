@@ -1,0 +1,39 @@
+// Forward half of the Schur reduction solved once per scenario for all
+// control columns (host/stream_plan.hpp ReachPlan), and the batched FP64
+// tensor-core GEMM that applies the dense tail inverse to it.
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace bipm {
+
+struct ReachDev {
+  int n_u, tl, ldy, nnz_yn;
+  int ymax;           // largest column reach (y_N entries of one column)
+  const int* op_ptr;  // [n_u + 1]
+  const int4* ops;    // {dest, G_u slot or -1, entry begin, entry end}
+  const int2* ent;    // {source y_N entry (column-local), L factor slot}
+  const int* yn_ptr;  // [n_u + 1]
+};
+
+// y_N [M][nnz_yn] and y_T [M][n_u][ldy] (rows >= tl zero) from the factors
+// F [M][nnz_f] and the G_u values [M][gu_nnz]
+void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz_f,
+                        const double* gu, long long gu_nnz, double* yn, double* yt,
+                        cudaStream_t st);
+
+// C[b](i, j) = sum_k A[b][i lda + k] B[b][j ldb + k]  (both operands
+// k-contiguous, C column-major: C[b][j ldc + i]), i < m, j < n, k < kd;
+// FP64 on the tensor pipe (DMMA m8n8k4).  lda, ldb even; A, B 16-byte aligned.
+struct GemmTN {
+  int m, n, kd, batch;
+  const double* A;
+  long long lda, sa;
+  const double* B;
+  long long ldb, sb;
+  double* C;
+  long long ldc, sc;
+};
+void launch_gemm_tn(const GemmTN& g, cudaStream_t st);
+
+}  // namespace bipm

@@ -37,7 +37,7 @@ void check_launch(const char* what) {
 }
 
 enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5,
-             kDenseG = 6, kSweepW = 7 };
+             kDenseG = 6, kSweepW = 7, kScatterY = 8 };
 constexpr int kStepHeaderIntsDev = 16;  // host/stream_plan.hpp kStepHeaderInts
 constexpr int kArrDenseDev = 1;         // host/stream_plan.hpp kArrDense
 
@@ -557,7 +557,9 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
   double* cta_scratch =
       a.scratch + size_t(chunk * gridDim.x + tile) * (size_t(a.n_x) * K + a.list_cap);
   int2* gu_list = reinterpret_cast<int2*>(cta_scratch + size_t(a.n_x) * K);
-  const int n_gu = a.gu.t_ptr[j0 + k] - a.gu.t_ptr[j0];
+  // presolved: the "G_u" list holds the tile's y_N entries instead
+  const int n_gu = a.presolved ? a.yn_ptr[j0 + k] - a.yn_ptr[j0]
+                               : a.gu.t_ptr[j0 + k] - a.gu.t_ptr[j0];
   const int n_kxu = a.kxu.t_ptr[j0 + k] - a.kxu.t_ptr[j0];
   int2* kxu_list = gu_list + ((n_gu + 1) & ~1);
   unsigned char* ring = reinterpret_cast<unsigned char*>(ring_off + ((P + 3) & ~3));
@@ -575,11 +577,20 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int j = tid; j < P; j += kThreads) ring_off[j] = a.ring_off[j];
-  for (int e = tid; e < n_gu; e += kThreads) {
-    const int q = a.gu.t_ptr[j0] + e;
-    int c = 0;
-    while (a.gu.t_ptr[j0 + c + 1] <= q) ++c;
-    gu_list[e] = make_int2(Pn::elem(a.iperm[a.gu.t_row[q]], c), a.gu.t_slot[q]);
+  if (a.presolved) {
+    for (int e = tid; e < n_gu; e += kThreads) {
+      const int q = a.yn_ptr[j0] + e;
+      int c = 0;
+      while (a.yn_ptr[j0 + c + 1] <= q) ++c;
+      gu_list[e] = make_int2(Pn::elem(a.yn_row[q], c), q);
+    }
+  } else {
+    for (int e = tid; e < n_gu; e += kThreads) {
+      const int q = a.gu.t_ptr[j0] + e;
+      int c = 0;
+      while (a.gu.t_ptr[j0 + c + 1] <= q) ++c;
+      gu_list[e] = make_int2(Pn::elem(a.iperm[a.gu.t_row[q]], c), a.gu.t_slot[q]);
+    }
   }
   for (int e = tid; e < n_kxu; e += kThreads) {
     const int q = a.kxu.t_ptr[j0] + e;
@@ -693,6 +704,43 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
 #pragma unroll
           for (int u = 0; u < 4; ++u)
             if (e0 + u * C < n_gu) sts1(xb + l[u].x, g[u]);
+        }
+        break;
+      }
+      case kScatterY: {
+        // X = 0; X[y_N rows, c] = y_N; X[tail, c] = X_T[:, j0 + c]
+        if constexpr (K == 1) {
+          for (int i = tid; i < a.n_x; i += C) sts1(xb + 8 * i, 0.0);
+        } else {
+          for (int i = tid; i < nxk2; i += C) sts2(xb + 16 * i, 0.0, 0.0);
+        }
+        consumer_sync<C>();
+        const double* yv = a.yn_v + size_t(s) * a.nnz_yn;
+        for (int e0 = tid; e0 < n_gu; e0 += 4 * C) {
+          int2 l[4];
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) l[u] = e0 + u * C < n_gu ? gu_list[e0 + u * C] : make_int2(0, 0);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) g[u] = e0 + u * C < n_gu ? yv[l[u].y] : 0.0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (e0 + u * C < n_gu) sts1(xb + l[u].x, g[u]);
+        }
+        const double* xt = a.xt + (size_t(s) * a.n_u + j0) * a.ldy;
+        const int nt = a.tl * k;
+        for (int e0 = tid; e0 < nt; e0 += 4 * C) {
+          double g[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * C;
+            g[u] = e < nt ? xt[size_t(e / a.tl) * a.ldy + e % a.tl] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int e = e0 + u * C;
+            if (e < nt) sts1(xb + Pn::elem(a.t0 + e % a.tl, e / a.tl), g[u]);
+          }
         }
         break;
       }

@@ -28,6 +28,12 @@ struct StreamLaunch {
   const int* iperm;
   const double *gu_v, *kxu_v, *kuu_v;
   double dw;
+  // presolved forward half (ReachPlan, reach_gemm.cu): the tile starts from
+  // y_N (reach rows, [M][nnz_yn], column-major by control) and X_T
+  // ([M][n_u][ldy]) instead of G_u
+  int presolved, ldy, nnz_yn;
+  const int *yn_ptr, *yn_row;
+  const double *yn_v, *xt;
   double* partial;   // [nchunks][n_u * n_u] column-major
   double* scratch;   // per CTA: n_x * K (S = K~_xx T + K_xu V staging)
   long long* phase;  // optional: clock64 per step of CTA 0's first scenario
