@@ -315,7 +315,8 @@ int bipm_ctx_kernel_time(bipm_ctx* c, const char* name, double* ms, int64_t* cou
 /* debug: clock64 stamps of the reduction phases of CTA (0,0) (16 slots) */
 int bipm_ctx_phase_stamps(bipm_ctx* c, int32_t enable, int64_t out[16]);
 /* out = reduce tile width, scenarios per CTA, chunks, panel-in-smem, nnz(L),
- * nnz(L+U), LU multiply-adds, SM count */
+ * nnz(L+U), LU multiply-adds, SM count, reduction flags (1 streamed, 2
+ * presolved forward half, 4 adjoint identity), steps, ring bytes, nnz(VS) */
 int bipm_ctx_info(bipm_ctx* c, int64_t out[12]);
 /* debug: (step kind, clock64 before its data wait, after it) of every step of
    the streamed reduction's first scenario in CTA (0,0) from the previous

@@ -522,7 +522,12 @@ class Context:
         check(lib().bipm_ctx_info(self._h, out))
         keys = ("tile_cols", "chunk", "nchunks", "panel_in_smem", "nnz_l", "nnz_f", "lu_madds",
                 "sm_count", "streamed", "steps", "ring_bytes", "nnz_vs")
-        return dict(zip(keys, list(out)))
+        d = dict(zip(keys, list(out)))
+        # streamed bits: 1 streamed reduction, 2 presolved forward half,
+        # 4 adjoint identity (host/stream_plan.hpp)
+        d["presolve"], d["adj_identity"] = int(bool(d["streamed"] & 2)), int(bool(d["streamed"] & 4))
+        d["streamed"] &= 1
+        return d
 
     def __del__(self):
         _destroy(self, "bipm_ctx_destroy")

@@ -749,7 +749,7 @@ int bipm_ctx_info(bipm_ctx* c, int64_t out[12]) {
     out[5] = e.pb.LU.nnz_f;
     out[6] = (int64_t)e.pb.LU.mul_l.size();
     out[7] = e.sm_count;
-    out[8] = e.use_stream ? 1 : 0;
+    out[8] = e.use_stream ? 1 | (e.presolve ? 2 : 0) | (e.adj_identity ? 4 : 0) : 0;
     out[9] = e.use_stream ? e.sprog.steps : 0;
     out[10] = e.use_stream ? e.sl.ring_bytes : 0;
     out[11] = e.use_stream ? e.sprog.nnz_vs : 0;

@@ -316,8 +316,20 @@ void Engine::setup_stream() {
     return;
   }
   const int K = best.K, ring = best.ring, list_cap = best.list_cap;
+  // adjoint identity (stream_plan.hpp): the L' sweep and W' product give way
+  // to a y_N' z_N accumulation and an n_u x tl product against X_T -- a win
+  // while n_u x tl stays small against the sweep it removes
+  // (BIPM_ADJ_IDENTITY=0/1 overrides)
+  bool adj = false;
+  if (presolve) {
+    long long lt_ent = 0;
+    for (idx i = 0; i < L.t0; ++i) lt_ent += L.lt_ptr[size_t(i) + 1] - L.lt_ptr[size_t(i)];
+    adj = rplan.nnz_yn < lt_ent;  // measured: 1354 and 2869 gain, 9241 loses
+    if (const char* e = std::getenv("BIPM_ADJ_IDENTITY")) adj = std::atoi(e) != 0;
+  }
+  adj_identity = adj;
   sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, best.C, ring,
-                               kStreamLookahead, presolve);
+                               kStreamLookahead, presolve ? &rplan : nullptr, adj);
   if (presolve) {
     rp_op_ptr.upload(rplan.op_ptr);
     rp_ops.upload(rplan.ops.empty() ? std::vector<idx>(4, 0) : rplan.ops);
@@ -331,7 +343,7 @@ void Engine::setup_stream() {
                     rp_op_ptr.get(), reinterpret_cast<const int4*>(rp_ops.get()),
                     reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get()};
     const size_t Ms = size_t(M);
-    YN.resize(Ms * size_t(std::max<idx>(1, rplan.nnz_yn)));
+    YN.resize(Ms * size_t(std::max<idx>(1, rplan.nnz_yn)) + 2);  // + the bulk copies' 16-byte rounding
     YT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
     XT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
     XT.zero(st);
@@ -478,8 +490,9 @@ void Engine::reduce_local(double dw) {
     timed("reduce_tiles", [&] {
       launch_gather_values(kxu.get(), nnz(D.kxu.out), sp_kxu_slot.get(), int(nnz(D.kxu.out)),
                            kxu_t.get(), nnz(D.kxu.out), M, st);
-      launch_gather_values(bd().gu.get(), nnz(D.g.u), sp_gu_slot.get(), int(nnz(D.g.u)),
-                           gu_t.get(), nnz(D.g.u), M, st);
+      if (!adj_identity)  // the G_u' Y accumulation reads column-order G_u
+        launch_gather_values(bd().gu.get(), nnz(D.g.u), sp_gu_slot.get(), int(nnz(D.g.u)),
+                             gu_t.get(), nnz(D.g.u), M, st);
       launch_kuu_sum(kuu.get(), nnz(D.kuu.out), kuu_row.get(), kuu_col.get(),
                      int(nnz(D.kuu.out)), M, n_u, kuu_part, st);
       sl.arr[kArrSweep] = VS.get();
@@ -488,6 +501,7 @@ void Engine::reduce_local(double dw) {
       sl.arr[kArrKxuT] = kxu_t.get();
       sl.arr[kArrGuT] = gu_t.get();
       sl.arr[kArrSigma] = sigma_x.get();
+      sl.arr[kArrYN] = presolve ? YN.get() : nullptr;
       sl.gu_v = bd().gu.get();
       sl.kxu_v = kxu.get();
       sl.kuu_v = kuu.get();

@@ -123,6 +123,7 @@ class Engine {
   // y_N [M][nnz_yn], y_T and X_T = W y_T [M][n_u][ldy]; BIPM_PRESOLVE=0 runs
   // the L sweep and the first dense product inside every column tile instead
   bool presolve = true;
+  bool adj_identity = false;  // adjoint half via y_N' z_N + X_T' z_T (stream_plan.hpp)
   ReachPlan rplan;
   ReachDev rdev{};
   DArr<int> rp_op_ptr, rp_ops, rp_ent, rp_yn_ptr, rp_yn_row;

@@ -486,7 +486,10 @@ ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u) {
 
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
-                                   int lookahead_max, bool presolved) {
+                                   int lookahead_max, const ReachPlan* reach,
+                                   bool adjoint_identity) {
+  const bool presolved = reach != nullptr;
+  adjoint_identity = adjoint_identity && presolved;
   StreamProgram S;
   S.K = K;
   S.consumers = consumers;
@@ -504,6 +507,7 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   S.stride[kArrKxuT] = kxu.nnz();
   S.stride[kArrGuT] = gu.nnz();
   S.stride[kArrSigma] = n;
+  S.stride[kArrYN] = presolved ? reach->nnz_yn : 0;
   // stride[kArrSweep] is fixed after the program is built (nnz_vs, even)
   Builder B{S, S.max_step_bytes, {}};
   // warp-local subtree sweeps: correct, measured no faster at 1354/256
@@ -623,9 +627,45 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   spmv();
   B.emit(P{kStepCopyBack, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
   B.sweep(L.sUt, slot_Ut, true, true, 1);  // the diagonal is not part of the tail gather
-  dense(1);
-  B.sweep(L.sLt, slot_Lt, false, false, 0);
-  acc(gu, S.gu_t_slot);
+  if (adjoint_identity) {
+    // acc -= y_N' z_N: items per control u = its reach rows (panel rows),
+    // values y_N[yn_ptr[u] ..] (kArrYN)
+    bool first_acc = true;
+    int u0 = 0;
+    while (u0 < n_u) {
+      int u1 = u0, ents = 0;
+      while (u1 < n_u) {
+        const int add = reach->yn_ptr[size_t(u1) + 1] - reach->yn_ptr[size_t(u1)];
+        if (u1 > u0 &&
+            Builder::step_bytes(u1 - u0 + 1, ents + add, ents + add, 0) > S.max_step_bytes)
+          break;
+        ents += add;
+        ++u1;
+      }
+      P p{kStepAcc, first_acc ? kFlagPre : 0, 0, u0, {}, {}};
+      for (int u = u0; u < u1; ++u) {
+        const int beg = int(p.col.size());
+        for (idx k = reach->yn_ptr[size_t(u)]; k < reach->yn_ptr[size_t(u) + 1]; ++k)
+          p.col.push_back(reach->yn_row[size_t(k)]);
+        p.items.insert(p.items.end(), {u, beg, int(p.col.size()), 0});
+      }
+      p.val_arr = kArrYN;
+      p.val_off = reach->yn_ptr[size_t(u0)];
+      p.val_count = reach->yn_ptr[size_t(u1)] - reach->yn_ptr[size_t(u0)];
+      if (p.val_count > 0) {
+        B.emit(p);
+        ++S.n_acc_steps;
+        first_acc = false;
+      }
+      u0 = u1;
+    }
+    // acc -= X_T' z_T (reads the tail rows the U' sweep's gather finished)
+    if (tl > 0) B.emit(P{kStepAccTail, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+  } else {
+    dense(1);
+    B.sweep(L.sLt, slot_Lt, false, false, 0);
+    acc(gu, S.gu_t_slot);
+  }
 
   if (S.vs_src.size() & 1) S.vs_src.push_back(-1);
   if (S.vs_src.empty()) S.vs_src.assign(2, -1);

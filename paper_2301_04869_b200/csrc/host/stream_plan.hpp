@@ -29,6 +29,7 @@ enum StepKind : int {
   kStepDenseG = 6,    // X_T <- W X_T with W read from global memory (L2), one step
   kStepSweepW = 7,    // warp-local levels of a sweep: each warp its own elimination subtrees
   kStepScatterY = 8,  // X = (y_N, X_T) tile columns (presolved forward half, ReachPlan)
+  kStepAccTail = 9,   // acc -= X_T' Z_T (all controls, the tile's columns; DMMA, X_T from L2)
 };
 // kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
 enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };
@@ -68,7 +69,8 @@ enum ValArray : int {
   kArrKxuT = 3,   // K_xu values in column (control) order
   kArrGuT = 4,    // G_u values in column (control) order
   kArrSigma = 5,  // sigma_x
-  kNumValArrays = 6
+  kArrYN = 6,     // y_N (ReachPlan, column-major by control)
+  kNumValArrays = 7
 };
 
 // producer record of one step (12 ints)
@@ -90,7 +92,7 @@ struct StreamProgram {
   std::vector<idx> vs_src;       // VS position -> factor slot (F), -1: padding
   idx nnz_vs = 0;
   std::vector<idx> kxu_t_slot, gu_t_slot;  // column-order gathers of K_xu, G_u values
-  long long stride[kNumValArrays] = {0, 0, 0, 0, 0, 0};
+  long long stride[kNumValArrays] = {0, 0, 0, 0, 0, 0, 0};
   int nq = 0;                    // accumulator registers per consumer thread
   int max_step_bytes = 0;
   // statistics
@@ -128,10 +130,17 @@ struct ReachPlan {
 };
 ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u);
 
-// presolved: the program starts from (y_N, X_T) (ReachPlan) -- a scatter of
-// the tile's columns of both, no L sweep, no first dense product
+// reach != nullptr: the program starts from (y_N, X_T) (ReachPlan) -- a
+// scatter of the tile's columns of both, no L sweep, no first dense product.
+// adjoint_identity (with reach): the adjoint half ends after the U' sweep.
+// With y^ = L^{-1} P G_u and z^ = U^{-T} S,
+//   G_u' G_x^{-T} S = y^' z^ = y_N' z_N + X_T' z_T
+// (y^_T' U_TT^{-T} = (U_TT^{-1} L_TT^{-1} y_T)' = X_T'), so the W' product,
+// the L' sweep and the G_u' Y accumulation become a sparse accumulation over
+// y_N's pattern and one dense n_u x tl product against X_T.
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
-                                   int lookahead_max, bool presolved = false);
+                                   int lookahead_max, const ReachPlan* reach = nullptr,
+                                   bool adjoint_identity = false);
 
 }  // namespace bipm

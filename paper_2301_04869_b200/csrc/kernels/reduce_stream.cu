@@ -37,7 +37,7 @@ void check_launch(const char* what) {
 }
 
 enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5,
-             kDenseG = 6, kSweepW = 7, kScatterY = 8 };
+             kDenseG = 6, kSweepW = 7, kScatterY = 8, kAccTail = 9 };
 constexpr int kStepHeaderIntsDev = 16;  // host/stream_plan.hpp kStepHeaderInts
 constexpr int kArrDenseDev = 1;         // host/stream_plan.hpp kArrDense
 
@@ -398,21 +398,25 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 // temp = W X_T for the whole tail on the FP64 tensor pipe (DMMA m8n8k4):
 // warp = 8 output rows x all K columns; A = W rows from global memory (L2,
 // eight k-steps of loads in flight), B = X_T from the panel in shared memory
+// (general form: temp[i K + c] = sum_k A(i, k) X[t0 + k, c] for i < m, k < tl,
+// A rows k-contiguous with stride lda (a multiple of 16 doubles))
 template <int K, int C>
 __device__ __forceinline__ void step_dense_global(const double* __restrict__ W, unsigned xb,
-                                                  double* temp, int t0, int tl, int tid) {
+                                                  double* temp, int t0, int tl, int tid,
+                                                  int m = -1, int lda = -1) {
   using Pn = Panel<K>;
   constexpr int NT = K >= 8 ? K / 8 : 1;  // 8-column tiles
   const int lane = tid & 31, warp = tid >> 5;
   const int gm = lane >> 2, gk = lane & 3;
-  const int ldw = (tl + 15) & ~15;  // host/stream_plan.hpp dense_ld
-  const int mtiles = (tl + 7) >> 3;
+  if (m < 0) m = tl;
+  const int ldw = lda >= 0 ? lda : (tl + 15) & ~15;  // host/stream_plan.hpp dense_ld
+  const int mtiles = (m + 7) >> 3;
   for (int mt = warp; mt < mtiles; mt += C / 32) {
     const int i = mt * 8 + gm;
     // lane (gm, gk) reads W(i, k0 + 4 gk .. +3) as one 32-byte vector: the 4
     // lanes of a row cover one 128-byte line, and DMMA step j of the chunk
     // takes k = k0 + 4 gk + j (any k order works when A and B agree)
-    const double* __restrict__ wr = W + size_t(i < tl ? i : 0) * ldw + 4 * gk;
+    const double* __restrict__ wr = W + size_t(i < m ? i : 0) * ldw + 4 * gk;
     double acc[NT][2];
 #pragma unroll
     for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = 0.0;
@@ -452,7 +456,7 @@ __device__ __forceinline__ void step_dense_global(const double* __restrict__ W, 
       chunk(k0 + 32, r2);
       ld(k0 + 80, r2);
     }
-    if (i < tl) {
+    if (i < m) {
 #pragma unroll
       for (int n = 0; n < NT; ++n)
 #pragma unroll
@@ -778,6 +782,19 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
       case kAcc:
         step_acc<K, C>(h, items, col, v, xb, acc, tid);
         break;
+      case kAccTail: {
+        // acc -= X_T' Z_T: temp[u K + c] = sum_t X_T[t, u] Z[t0 + t, c] (the
+        // temp index of (u, c) is the owner's tid + q C)
+        step_dense_global<K, C>(a.xt + size_t(s) * a.n_u * a.ldy, xb, temp, a.t0, a.tl, tid,
+                                a.n_u, a.ldy);
+        consumer_sync<C>();
+#pragma unroll
+        for (int q = 0; q < kMaxQ; ++q) {
+          const int it = tid + q * C;
+          if (q < a.nq && it < a.n_u * K) acc[q] -= temp[it];
+        }
+        break;
+      }
       case kSpmv: {
         const int xoff = h.vcount > 0 ? ((h.vcount + 1) * 8 + 15) & ~15 : 0;
         const int xshift = ((h.par >> 2) & 1) ^ ((h.par >> 3) & s & 1);

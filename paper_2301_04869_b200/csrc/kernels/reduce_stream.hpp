@@ -11,7 +11,7 @@
 
 namespace bipm {
 
-constexpr int kStreamArrays = 6;
+constexpr int kStreamArrays = 7;
 
 struct StreamLaunch {
   int n_x, n_u, M, K, nq, steps, ring_bytes, t0, tl;
