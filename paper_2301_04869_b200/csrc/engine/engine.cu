@@ -255,7 +255,7 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   if (const char* e = std::getenv("BIPM_FORCE_COMM")) force_comm = std::atoi(e) != 0;
   if (use_stream) setup_stream();
   if (use_stream) {
-    red_parts = sl.nchunks + 1;  // + the K_uu slab
+    red_parts = sl.nchunks + 1 + tail_splits;  // + the K_uu slab + the tail GEMM's
     red_partial.resize(size_t(red_parts) * Mo.n_u * Mo.n_u);
     red_partial.zero(st);
   } else {
@@ -328,8 +328,10 @@ void Engine::setup_stream() {
     if (const char* e = std::getenv("BIPM_ADJ_IDENTITY")) adj = std::atoi(e) != 0;
   }
   adj_identity = adj;
+  if (const char* e = std::getenv("BIPM_TAIL_DEFER")) defer_tail = std::atoi(e) != 0;
+  defer_tail = defer_tail && adj && L.tl > 0;
   sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, best.C, ring,
-                               kStreamLookahead, presolve ? &rplan : nullptr, adj);
+                               kStreamLookahead, presolve ? &rplan : nullptr, adj, defer_tail);
   if (presolve) {
     rp_op_ptr.upload(rplan.op_ptr);
     rp_ops.upload(rplan.ops.empty() ? std::vector<idx>(4, 0) : rplan.ops);
@@ -339,7 +341,10 @@ void Engine::setup_stream() {
     int ymax = 1;
     for (idx u = 0; u < n_u; ++u)
       ymax = std::max(ymax, int(rplan.yn_ptr[size_t(u) + 1] - rplan.yn_ptr[size_t(u)]));
-    rdev = ReachDev{int(n_u), int(L.tl), int(rplan.ldy), int(rplan.nnz_yn), ymax,
+    // lanes per column ~ the mean entries per op (1354: 4.5 -> 4, 9241: 42 -> 32)
+    const double per_op = double(rplan.fmas) / std::max<size_t>(1, rplan.ops.size() / 4);
+    const int grp = per_op <= 6 ? 4 : per_op <= 14 ? 8 : per_op <= 28 ? 16 : 32;
+    rdev = ReachDev{int(n_u), int(L.tl), int(rplan.ldy), int(rplan.nnz_yn), ymax, grp,
                     rp_op_ptr.get(), reinterpret_cast<const int4*>(rp_ops.get()),
                     reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get()};
     const size_t Ms = size_t(M);
@@ -347,6 +352,13 @@ void Engine::setup_stream() {
     YT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
     XT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
     XT.zero(st);
+    if (defer_tail) {
+      ZT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
+      ZT.zero(st);
+      // about three waves of 64 x 64 tiles of K_hat over the SMs
+      const long long t = (long long)((n_u + 63) / 64) * ((n_u + 63) / 64);
+      tail_splits = int(std::max(1LL, std::min<long long>(M, (3LL * sm_count + t / 2) / t)));
+    }
   }
   sp_pat.upload(sprog.pat);
   {
@@ -407,6 +419,7 @@ void Engine::setup_stream() {
   sl.yn_row = presolve ? rp_yn_row.get() : nullptr;
   sl.yn_v = presolve ? YN.get() : nullptr;
   sl.xt = presolve ? XT.get() : nullptr;
+  sl.zt = defer_tail ? ZT.get() : nullptr;
   const int tiles = (n_u + K - 1) / K;
   sp_scratch.resize(size_t(tiles) * sl.nchunks * (size_t(n_x) * K + size_t(list_cap)));
 }
@@ -481,7 +494,7 @@ void Engine::reduce_local(double dw) {
         launch_reach_solve(rdev, M, F.get(), pb.LU.nnz_f, bd().gu.get(), nnz(D.g.u), YN.get(),
                            YT.get(), st);
         const int tl = int(pb.LU.tl);
-        GemmTN g{tl, n_u, tl, int(M), Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
+        GemmTN g{tl, n_u, tl, int(M), 0, 1.0, Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
                  YT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
                  XT.get(), rplan.ldy, (long long)n_u * rplan.ldy};
         launch_gemm_tn(g, st);
@@ -516,6 +529,18 @@ void Engine::reduce_local(double dw) {
       sl.debug = dbg;
       launch_reduce_stream(sl, st);
     });
+    if (defer_tail) {
+      // -sum_s X_T' Z_T into the tail slabs (after the K_uu slab)
+      timed("reduce_post", [&] {
+        const int tl = int(pb.LU.tl);
+        const long long nn = (long long)n_u * n_u;
+        GemmTN g{n_u, n_u, tl, int(M), tail_splits, -1.0,
+                 XT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
+                 ZT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
+                 red_partial.get() + size_t(sl.nchunks + 1) * nn, n_u, nn};
+        launch_gemm_tn(g, st);
+      });
+    }
     return;
   }
   red.F = F.get();

@@ -127,7 +127,12 @@ class Engine {
   ReachPlan rplan;
   ReachDev rdev{};
   DArr<int> rp_op_ptr, rp_ops, rp_ent, rp_yn_ptr, rp_yn_row;
-  DArr<double> YN, YT, XT;
+  DArr<double> YN, YT, XT, ZT;
+  // adjoint identity with a deferred tail: -sum_s X_T' Z_T by one batch-sum
+  // GEMM into tail_splits slabs after the kuu slab (BIPM_TAIL_DEFER=0: the
+  // product runs inside every tile instead)
+  bool defer_tail = true;
+  int tail_splits = 0;
   int red_parts = 0;  // partial K_hat slabs summed by finish_reduce
   // ---- reduction workspace (tile kernel, BIPM_REDUCE=tiles)
   ReduceLaunch red{};

@@ -487,7 +487,7 @@ ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u) {
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
                                    int lookahead_max, const ReachPlan* reach,
-                                   bool adjoint_identity) {
+                                   bool adjoint_identity, bool defer_tail) {
   const bool presolved = reach != nullptr;
   adjoint_identity = adjoint_identity && presolved;
   StreamProgram S;
@@ -660,7 +660,8 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
       u0 = u1;
     }
     // acc -= X_T' z_T (reads the tail rows the U' sweep's gather finished)
-    if (tl > 0) B.emit(P{kStepAccTail, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
+    if (tl > 0)
+      B.emit(P{defer_tail ? kStepStoreTail : kStepAccTail, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
   } else {
     dense(1);
     B.sweep(L.sLt, slot_Lt, false, false, 0);

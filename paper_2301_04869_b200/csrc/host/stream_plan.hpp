@@ -30,6 +30,7 @@ enum StepKind : int {
   kStepSweepW = 7,    // warp-local levels of a sweep: each warp its own elimination subtrees
   kStepScatterY = 8,  // X = (y_N, X_T) tile columns (presolved forward half, ReachPlan)
   kStepAccTail = 9,   // acc -= X_T' Z_T (all controls, the tile's columns; DMMA, X_T from L2)
+  kStepStoreTail = 10,  // Z_T (tail rows of the panel) -> global, for the batch-sum GEMM
 };
 // kFlagBarrier: consumers synchronise after the step; kFlagPre: before it
 enum StepFlag : int { kFlagDiag = 1, kFlagCommit = 2, kFlagBarrier = 4, kFlagPre = 8 };
@@ -137,10 +138,12 @@ ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u);
 //   G_u' G_x^{-T} S = y^' z^ = y_N' z_N + X_T' z_T
 // (y^_T' U_TT^{-T} = (U_TT^{-1} L_TT^{-1} y_T)' = X_T'), so the W' product,
 // the L' sweep and the G_u' Y accumulation become a sparse accumulation over
-// y_N's pattern and one dense n_u x tl product against X_T.
+// y_N's pattern and one dense n_u x tl product against X_T -- inside the tile
+// (kStepAccTail), or with defer_tail, Z_T stored (kStepStoreTail) and
+// sum_s X_T' Z_T formed by one batch-sum GEMM after the tiles (reach_gemm.cu).
 StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kxx, const Csr& kxu,
                                    idx n_u, int K, int consumers, int ring_bytes,
                                    int lookahead_max, const ReachPlan* reach = nullptr,
-                                   bool adjoint_identity = false);
+                                   bool adjoint_identity = false, bool defer_tail = true);
 
 }  // namespace bipm

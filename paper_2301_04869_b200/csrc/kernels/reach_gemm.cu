@@ -26,76 +26,86 @@ void check_launch(const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-constexpr int kReachWarps = 8;
-constexpr int kReachSeg = 256;  // staged entries per warp
+constexpr int kReachWarps = 4;
 
-// dynamic shared memory per warp: y_N of its column (ymax doubles), then the
-// staged segment (kReachSeg factor values + kReachSeg source indices)
+// One group of G lanes per (scenario, column): the column's ops run in order,
+// each op's entries split over the group's lanes and summed by shuffles
+// within the group; 32 / G columns per warp.  Dynamic shared memory per
+// group: y_N of its column (ymax doubles), then the staged segment (SEG
+// factor values + SEG source indices, SEG = 8 G) so a segment's loads are all
+// in flight before its dependent ops run.
+template <int G>
 __global__ void __launch_bounds__(32 * kReachWarps)
     reach_solve_kernel(ReachDev p, const double* __restrict__ F, long long nnz_f,
                        const double* __restrict__ gu, long long gu_nnz, double* __restrict__ yn,
                        double* __restrict__ yt) {
+  constexpr int SEG = 8 * G, NG = 32 / G;
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x * kReachWarps + warp, s = blockIdx.y;
-  if (u >= p.n_u) return;
+  const int grp = lane / G, gl = lane % G;
+  const unsigned gmask = G == 32 ? 0xffffffffu : ((1u << G) - 1u) << (grp * G);
+  const int u = (blockIdx.x * kReachWarps + warp) * NG + grp, s = blockIdx.y;
+  if (u >= p.n_u) return;  // the whole group leaves together
   const int ymax = p.ymax;
-  unsigned char* wb = smem + size_t(warp) * (size_t(ymax) * 8 + kReachSeg * 12);
+  unsigned char* wb =
+      smem + size_t(warp * NG + grp) * (size_t(ymax) * 8 + SEG * 12);
   double* y = reinterpret_cast<double*>(wb);
   double* fv = y + ymax;
-  int* src = reinterpret_cast<int*>(fv + kReachSeg);
+  int* src = reinterpret_cast<int*>(fv + SEG);
   const double* Fs = F + size_t(s) * nnz_f;
   const double* gs = gu + size_t(s) * gu_nnz;
   double* ts = yt + (size_t(s) * p.n_u + u) * p.ldy;
-  for (int i = lane; i < p.ldy; i += 32) ts[i] = 0.0;
+  for (int i = gl; i < p.ldy; i += G) ts[i] = 0.0;
   const int ob = p.op_ptr[u], oe = p.op_ptr[u + 1];
   for (int o = ob; o < oe;) {
-    // segment: up to 32 ops whose entries fit the staging buffer (an op with
+    // segment: up to G ops whose entries fit the staging buffer (an op with
     // more entries than that runs alone, straight from global memory)
-    const int4 rec = o + lane < oe ? p.ops[o + lane] : make_int4(0, -1, 0, 0x7fffffff);
-    const int e0 = __shfl_sync(0xffffffffu, rec.z, 0);
+    const bool valid = o + gl < oe;
+    const int4 rec = valid ? p.ops[o + gl] : make_int4(0, -1, 0, 0x7fffffff);
+    const int e0 = __shfl_sync(gmask, rec.z, 0, G);
     // entries are contiguous and increasing over the ops: a prefix of lanes fits
-    const unsigned fits = __ballot_sync(0xffffffffu, o + lane < oe && rec.w - e0 <= kReachSeg);
+    const unsigned fits =
+        (__ballot_sync(gmask, valid && rec.w - e0 <= SEG) >> (grp * G)) & (gmask >> (grp * G));
     const bool staged = (fits & 1u) != 0;
     const int nseg = staged ? __popc(fits) : 1;
     const double bval = rec.y >= 0 ? gs[rec.y] : 0.0;
-    const int e1 = __shfl_sync(0xffffffffu, rec.w, nseg - 1);
+    const int e1 = __shfl_sync(gmask, rec.w, nseg - 1, G);
     if (staged) {
-      for (int e = e0 + lane; e < e1; e += 32) {
+      for (int e = e0 + gl; e < e1; e += G) {
         const int2 en = p.ent[e];
         src[e - e0] = en.x;
         fv[e - e0] = Fs[en.y];
       }
-      __syncwarp();
+      __syncwarp(gmask);
     }
     for (int i = 0; i < nseg; ++i) {
-      const int dest = __shfl_sync(0xffffffffu, rec.x, i);
-      const int eb = __shfl_sync(0xffffffffu, rec.z, i), ee = __shfl_sync(0xffffffffu, rec.w, i);
-      const double b = __shfl_sync(0xffffffffu, bval, i);
+      const int dest = __shfl_sync(gmask, rec.x, i, G);
+      const int eb = __shfl_sync(gmask, rec.z, i, G), ee = __shfl_sync(gmask, rec.w, i, G);
+      const double b = __shfl_sync(gmask, bval, i, G);
       double a = 0.0;
       if (staged) {
-        for (int e = eb - e0 + lane; e < ee - e0; e += 32) a += fv[e] * y[src[e]];
+        for (int e = eb - e0 + gl; e < ee - e0; e += G) a += fv[e] * y[src[e]];
       } else {
-        for (int e = eb + lane; e < ee; e += 32) {
+        for (int e = eb + gl; e < ee; e += G) {
           const int2 en = p.ent[e];
           a += Fs[en.y] * y[en.x];
         }
       }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-      if (lane == 0) {
+      for (int off = G / 2; off > 0; off >>= 1) a += __shfl_xor_sync(gmask, a, off, G);
+      if (gl == 0) {
         if (dest >= 0)
           y[dest] = b - a;
         else
           ts[-1 - dest] = b - a;
       }
-      __syncwarp();
+      __syncwarp(gmask);
     }
     o += nseg;
   }
   double* ys = yn + size_t(s) * p.nnz_yn + p.yn_ptr[u];
   const int ny = p.yn_ptr[u + 1] - p.yn_ptr[u];
-  for (int i = lane; i < ny; i += 32) ys[i] = y[i];
+  for (int i = gl; i < ny; i += G) ys[i] = y[i];
 }
 
 // ------------------------------------------------------------- DMMA GEMM
@@ -114,17 +124,28 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes
 }
 
 // 64 x 64 tile of C per CTA, four warps of 32 x 32 (4 x 4 DMMA tiles), k in
-// chunks of 16 double-buffered with cp.async (zero fill past m, n, kd)
+// chunks of 16 double-buffered with cp.async (zero fill past m, n, kd).
+// Batched (g.splits == 0): blockIdx.z is the batch.  Batch sum (g.splits >
+// 0): blockIdx.z is a split of the batches, the CTA sums its batches' products
+// (fixed order) into slab z of C.
 __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
   __shared__ __align__(16) double As[2][kGM][kGPad];
   __shared__ __align__(16) double Bs[2][kGN][kGPad];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gm = lane >> 2, gk = lane & 3;
-  const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN, b = blockIdx.z;
-  const double* A = g.A + size_t(b) * g.sa;
-  const double* B = g.B + size_t(b) * g.sb;
+  const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN, z = blockIdx.z;
+  int b0 = z, nb = 1;
+  if (g.splits > 0) {
+    const int per = (g.batch + g.splits - 1) / g.splits;
+    b0 = z * per;
+    nb = min(g.batch, b0 + per) - b0;
+  }
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
-  auto load = [&](int k0, int buf) {
+  const int nk = (g.kd + kGK - 1) / kGK;
+  auto load = [&](int c, int buf) {
+    const int b = b0 + c / nk, k0 = (c % nk) * kGK;
+    const double* A = g.A + size_t(b) * g.sa;
+    const double* B = g.B + size_t(b) * g.sb;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = tid + q * 128, row = e >> 3, k = k0 + 2 * (e & 7);
@@ -147,12 +168,12 @@ __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int nk = (g.kd + kGK - 1) / kGK;
-  load(0, 0);
-  for (int c = 0; c < nk; ++c) {
+  const int nc = nb * nk;
+  if (nc > 0) load(0, 0);
+  for (int c = 0; c < nc; ++c) {
     const int buf = c & 1;
-    if (c + 1 < nk) {
-      load((c + 1) * kGK, buf ^ 1);
+    if (c + 1 < nc) {
+      load(c + 1, buf ^ 1);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -173,7 +194,7 @@ __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
     }
     __syncthreads();
   }
-  double* C = g.C + size_t(b) * g.sc;
+  double* C = g.C + size_t(z) * g.sc;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + wm + i * 8 + gm;
@@ -183,29 +204,46 @@ __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int col = n0 + wn + j * 8 + 2 * gk + v;
-        if (col < g.n) C[size_t(col) * g.ldc + r] = acc[i][j][v];
+        if (col < g.n) C[size_t(col) * g.ldc + r] = g.alpha * acc[i][j][v];
       }
   }
 }
 
 }  // namespace
 
+template <int G>
+static void launch_reach_g(const ReachDev& p, int M, const double* F, long long nnz_f,
+                           const double* gu, long long gu_nnz, double* yn, double* yt,
+                           cudaStream_t st) {
+  constexpr int NG = 32 / G, SEG = 8 * G;
+  const size_t smem = size_t(kReachWarps) * NG * (size_t(p.ymax) * 8 + SEG * 12);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(reach_solve_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  const int cols_per_cta = kReachWarps * NG;
+  reach_solve_kernel<G><<<dim3((p.n_u + cols_per_cta - 1) / cols_per_cta, M), 32 * kReachWarps,
+                          smem, st>>>(p, F, nnz_f, gu, gu_nnz, yn, yt);
+}
+
 void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz_f,
                         const double* gu, long long gu_nnz, double* yn, double* yt,
                         cudaStream_t st) {
   if (M <= 0 || p.n_u <= 0) return;
-  const size_t smem = size_t(kReachWarps) * (size_t(p.ymax) * 8 + kReachSeg * 12);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(reach_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  reach_solve_kernel<<<dim3((p.n_u + kReachWarps - 1) / kReachWarps, M), 32 * kReachWarps, smem,
-                       st>>>(p, F, nnz_f, gu, gu_nnz, yn, yt);
+  switch (p.group) {
+    case 4: launch_reach_g<4>(p, M, F, nnz_f, gu, gu_nnz, yn, yt, st); break;
+    case 8: launch_reach_g<8>(p, M, F, nnz_f, gu, gu_nnz, yn, yt, st); break;
+    case 16: launch_reach_g<16>(p, M, F, nnz_f, gu, gu_nnz, yn, yt, st); break;
+    default: launch_reach_g<32>(p, M, F, nnz_f, gu, gu_nnz, yn, yt, st); break;
+  }
   note_launch();
   check_launch("reach_solve");
 }
 
 void launch_gemm_tn(const GemmTN& g, cudaStream_t st) {
   if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return;
-  gemm_tn_kernel<<<dim3((g.m + kGM - 1) / kGM, (g.n + kGN - 1) / kGN, g.batch), 128, 0, st>>>(g);
+  gemm_tn_kernel<<<dim3((g.m + kGM - 1) / kGM, (g.n + kGN - 1) / kGN,
+                       g.splits > 0 ? g.splits : g.batch),
+                   128, 0, st>>>(g);
   note_launch();
   check_launch("gemm_tn");
 }

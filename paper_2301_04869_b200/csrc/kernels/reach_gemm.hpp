@@ -10,6 +10,7 @@ namespace bipm {
 struct ReachDev {
   int n_u, tl, ldy, nnz_yn;
   int ymax;           // largest column reach (y_N entries of one column)
+  int group;          // lanes per column (4, 8, 16 or 32: ~ entries per op)
   const int* op_ptr;  // [n_u + 1]
   const int4* ops;    // {dest, G_u slot or -1, entry begin, entry end}
   const int2* ent;    // {source y_N entry (column-local), L factor slot}
@@ -22,11 +23,14 @@ void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz
                         const double* gu, long long gu_nnz, double* yn, double* yt,
                         cudaStream_t st);
 
-// C[b](i, j) = sum_k A[b][i lda + k] B[b][j ldb + k]  (both operands
+// C[b](i, j) = alpha sum_k A[b][i lda + k] B[b][j ldb + k]  (both operands
 // k-contiguous, C column-major: C[b][j ldc + i]), i < m, j < n, k < kd;
 // FP64 on the tensor pipe (DMMA m8n8k4).  lda, ldb even; A, B 16-byte aligned.
+// splits > 0: batch sum instead -- C[z] = alpha sum over the z-th of `splits`
+// contiguous batch ranges of A[b]' B[b] (C[z] at C + z sc; fixed order).
 struct GemmTN {
-  int m, n, kd, batch;
+  int m, n, kd, batch, splits;
+  double alpha;
   const double* A;
   long long lda, sa;
   const double* B;

@@ -37,7 +37,8 @@ void check_launch(const char* what) {
 }
 
 enum : int { kScatter = 0, kSweep = 1, kDense = 2, kAcc = 3, kSpmv = 4, kCopyBack = 5,
-             kDenseG = 6, kSweepW = 7, kScatterY = 8, kAccTail = 9 };
+             kDenseG = 6, kSweepW = 7, kScatterY = 8, kAccTail = 9,
+             kStoreTail = 10 };
 constexpr int kStepHeaderIntsDev = 16;  // host/stream_plan.hpp kStepHeaderInts
 constexpr int kArrDenseDev = 1;         // host/stream_plan.hpp kArrDense
 
@@ -782,6 +783,16 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
       case kAcc:
         step_acc<K, C>(h, items, col, v, xb, acc, tid);
         break;
+      case kStoreTail: {
+        // Z_T of the tile's columns for the batch-sum GEMM (acc -= X_T' Z_T)
+        double* zt = a.zt + (size_t(s) * a.n_u + j0) * a.ldy;
+        const int nt = a.tl * k;
+        for (int e = tid; e < nt; e += C) {
+          const int c = e / a.tl, t = e - c * a.tl;
+          zt[size_t(c) * a.ldy + t] = lds1(xb + Pn::elem(a.t0 + t, c));
+        }
+        break;
+      }
       case kAccTail: {
         // acc -= X_T' Z_T: temp[u K + c] = sum_t X_T[t, u] Z[t0 + t, c] (the
         // temp index of (u, c) is the owner's tid + q C)

@@ -34,6 +34,7 @@ struct StreamLaunch {
   int presolved, ldy, nnz_yn;
   const int *yn_ptr, *yn_row;
   const double *yn_v, *xt;
+  double* zt;  // [M][n_u][ldy]: Z_T of every column (kStoreTail)
   double* partial;   // [nchunks][n_u * n_u] column-major
   double* scratch;   // per CTA: n_x * K (S = K~_xx T + K_xu V staging)
   long long* phase;  // optional: clock64 per step of CTA 0's first scenario

@@ -23,7 +23,7 @@ ctx.profile(True)
 for _ in range(reps):
     ctx.reduce(0.5, **args)
 ctx.factor_gx(v["gx"])
-out = {g: ctx.kernel_time(g) for g in ("reduce_pre", "reduce_tiles", "reduce_rhs", "lu_refactor")}
+out = {g: ctx.kernel_time(g) for g in ("reduce_pre", "reduce_tiles", "reduce_post", "reduce_rhs", "lu_refactor")}
 ctx.profile(False)
 print(json.dumps({"case": case, "N": N, "info": ctx.info(), "tl": int(p.array("lu_shape")[4]),
                   "ms_per_call": {g: (t / max(1, n)) for g, (t, n) in out.items()}}))

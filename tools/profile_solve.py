@@ -24,7 +24,7 @@ ctx.profile(True)
 t3 = time.time()
 r = s.solve()
 t4 = time.time()
-groups = ["ad_bundle", "ad_values", "condense", "lu_refactor", "reduce_pre", "reduce_tiles", "reduce_rhs",
+groups = ["ad_bundle", "ad_values", "condense", "lu_refactor", "reduce_pre", "reduce_tiles", "reduce_post", "reduce_rhs",
           "cholesky", "khat_solve", "recover_state"]
 kt = {g: ctx.kernel_time(g) for g in groups}
 it = r["iterations"]
