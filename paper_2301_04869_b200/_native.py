@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libbipm_gpu.so")
+# BIPM_LIB: A/B experiments against another build (tools/); default the in-tree one
+LIB_PATH = os.environ.get("BIPM_LIB") or os.path.join(_HERE, "_lib", "libbipm_gpu.so")
 
 STATUS = {
     0: "OK",
