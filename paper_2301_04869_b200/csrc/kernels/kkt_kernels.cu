@@ -289,7 +289,6 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   double* Rb = Cb + size_t(tp) * kLb;       // [kB][ldr]  W[P, :]
   double* R2 = Rb + size_t(kB) * ldr;       // [kB][ldr]  A11^{-1} W[P, :], pivot cols A11^{-1}
   double* Ai = R2 + size_t(kB) * ldr;       // [kB][kLb]  A11^{-1}
-  const int npass = (tl + kB - 1) / kB;
   double* const Wbase = D + size_t(s) * 2 * tt;  // slot b at Wbase + b tt
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gm = lane >> 2, gk = lane & 3;
@@ -297,7 +296,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   constexpr int kJ = kGjMaxTail / 32;  // a row's columns over the lanes
   {
     // S from the factor: every load of a row in flight at once
-    double* W = Wbase + (npass & 1) * tt;
+    double* W = Wbase;
     for (int i = crank * kWarps + warp; i < tl; i += kWarps * ncl) {
       int src[kJ];
 #pragma unroll
@@ -315,9 +314,13 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   }
   sync_all();
   for (int k0 = 0, pass = 0; k0 < tl; k0 += kB, ++pass) {
+    // in place: every element's update reads only itself and the staged
+    // C' / R2, so slot 0 serves every pass (the working set of the CTAs in
+    // flight, 148 x tl^2 doubles, then stays in L2 instead of ping-ponging
+    // two slots through HBM)
     const int bb = min(kB, tl - k0);
-    const double* W = Wbase + ((npass - pass) & 1) * tt;
-    double* Wn = Wbase + ((npass - pass - 1) & 1) * tt;
+    const double* W = Wbase;
+    double* Wn = Wbase;
     {
       // C' and W[P, :]: all of a thread's loads in flight, then the stores
       constexpr int kQ = (kGjMaxTail * kB + BLOCK - 1) / BLOCK;
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       }
     }
     __syncthreads();
+    if (ncl > 1) cluster.sync();  // no CTA overwrites W before every CTA staged C', W[P, :]
     // A11^{-1} by Gauss-Jordan in one warp (lane = column), pivots to the factor
     if (warp == 0) {
       // padded with the identity beyond bb: a branch-free loop keeps the
