@@ -77,9 +77,14 @@ struct Builder {
     if (p.kind == kStepSweep || p.kind == kStepSweepW || p.kind == kStepSpmv)
       for (int it = 0; it < n_items; ++it)
         p.items[size_t(it) * 4] = panel_word(p.items[size_t(it) * 4], K);
-    // columns stay panel ROWS (16 bits; the kernel forms the panel word)
-    for (int c : p.col)
-      if (c < 0 || c > 0xffff) throw std::runtime_error("stream program: panel row exceeds 16 bits");
+    // column entries are 16 bits: the panel word / 16 for K >= 2 (the word of
+    // row r is a multiple of 16; r K / 2 + sw(r) < 2^16 whenever the panel
+    // fits in shared memory), the panel row for K = 1 (word = 8 r)
+    for (int& c : p.col) {
+      if (c < 0) throw std::runtime_error("stream program: negative panel row");
+      if (K >= 2) c = panel_word(c, K) >> 4;
+      if (c > 0xffff) throw std::runtime_error("stream program: column entry exceeds 16 bits");
+    }
     const int warp0 = warp_rr;
     if (units > 0) {
       const int upw = 32 >> lg;

@@ -177,12 +177,13 @@ __device__ __forceinline__ void acc_add(double (&acc)[kMaxQ], int q, double v) {
     if (r == q) acc[r] += v;
 }
 
-// column entry t of a step: a 16-bit panel row -> its panel word
+// column entry t of a step -> its panel word: the entry holds word / 16
+// (K >= 2) or the panel row (K = 1, word 8 r) (host/stream_plan.cpp emit)
 template <int K>
 __device__ __forceinline__ int colw(unsigned col, int t) {
   unsigned short r;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(col + 2 * t));
-  return Panel<K>::word(int(r));
+  return K == 1 ? int(r) << 3 : int(r) << 4;
 }
 
 // Step header (host/stream_plan.hpp): 16 ints
