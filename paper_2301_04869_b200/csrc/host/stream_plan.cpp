@@ -118,18 +118,34 @@ struct Builder {
   // sized to its units x lanes; consecutive levels with the same team and
   // diagonal mode share a step and are separated by team barriers (named
   // barrier, or __syncwarp for one warp).  Values are appended to VS.
+  // pre_t0 >= 0 (backward sweeps U, L', whose tail rows are final before the
+  // sweep starts): every row's entries in the tail columns (>= pre_t0, the
+  // end of each row) form one independent level ahead of the schedule, so
+  // the dependent levels carry only the non-tail entries (1354: half of the
+  // U sweep's off-diagonal entries, all of its first level's)
   void sweep(const SweepPlan& sw, const std::vector<idx>& slot_of_t, bool diag, bool with_tail,
-             int tail_skip) {
+             int tail_skip, idx pre_t0 = -1) {
     const int K = S.K, NG = K > kStreamUnitCols ? K / kStreamUnitCols : 1;
     struct Unit { idx row, b, e; };
     std::vector<std::vector<Unit>> levels;
     std::vector<char> level_diag;
+    std::vector<Unit> pre;
     const idx nl = idx(sw.lvl_ptr.size()) - 1;
     for (idx l = 0; l < nl; ++l) {
       std::vector<Unit> us;
       for (idx it = sw.lvl_ptr[size_t(l)]; it < sw.lvl_ptr[size_t(l) + 1]; ++it) {
-        const idx row = sw.items[size_t(it) * 4], b = sw.items[size_t(it) * 4 + 1],
-                  e = sw.items[size_t(it) * 4 + 2];
+        const idx row = sw.items[size_t(it) * 4], b = sw.items[size_t(it) * 4 + 1];
+        idx e = sw.items[size_t(it) * 4 + 2];
+        if (pre_t0 >= 0) {
+          idx sp = e;
+          for (idx t = b + (diag ? 1 : 0); t < e; ++t)
+            if (sw.col[size_t(t)] >= pre_t0) {
+              sp = t;
+              break;
+            }
+          if (sp < e) pre.push_back({row, sp, e});
+          e = sp;
+        }
         if (!diag && e <= b) continue;  // nothing to subtract
         us.push_back({row, b, e});
       }
@@ -137,6 +153,10 @@ struct Builder {
         levels.push_back(std::move(us));
         level_diag.push_back(diag);
       }
+    }
+    if (!pre.empty()) {
+      levels.insert(levels.begin(), std::move(pre));
+      level_diag.insert(level_diag.begin(), 0);
     }
     // the subtree rows leave the team levels for the warp-local part: per
     // warp, its rows grouped by level (rows of one level are independent)
@@ -627,7 +647,14 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
     B.sweep(L.sL, slot_L, false, true, 0);
     dense(0);
   }
-  B.sweep(L.sU, slot_U, true, false, 0);
+  static const int pre_tail = [] {
+    const char* e = std::getenv("BIPM_PRE_TAIL");
+    return e ? std::atoi(e) : 1;
+  }();
+  // measured (same box): 1354/256 -0.7 %, 2869/64 -0.4 % per tile kernel with
+  // the adjoint identity; +1 % at 9241 (K = 1, no identity): there off
+  const idx pre_t0 = pre_tail && tl > 0 && adjoint_identity ? t0 : -1;
+  B.sweep(L.sU, slot_U, true, false, 0, pre_t0);
   acc(kxu, S.kxu_t_slot);
   spmv();
   B.emit(P{kStepCopyBack, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
@@ -669,7 +696,7 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
       B.emit(P{defer_tail ? kStepStoreTail : kStepAccTail, kFlagPre | kFlagBarrier, 0, 0, {}, {}});
   } else {
     dense(1);
-    B.sweep(L.sLt, slot_Lt, false, false, 0);
+    B.sweep(L.sLt, slot_Lt, false, false, 0, pre_t0);
     acc(gu, S.gu_t_slot);
   }
 
