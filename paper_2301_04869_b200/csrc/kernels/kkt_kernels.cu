@@ -489,6 +489,174 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     status[s] = bad > 0.0 ? 1 : (big > P.growth * fmax(scale_in[s], 1e-300) ? 2 : 0);
 }
 
+// Cluster-resident Gauss-Jordan (opt-in, BIPM_GJ_CLUSTER_RESIDENT=1): a cluster
+// of R CTAs holds W of one scenario in distributed shared memory, CTA r
+// owning rows [r rb, r rb + rb) (rb a multiple of the 16-pivot block), so no
+// pass touches global memory (the global-memory kernel above streams the
+// whole tl x tl block through L2/HBM twice per pass: 4.9 GB per refactor at
+// 1354/256).  Pass p, pivots P = [16 p, 16 p + 16) owned by CTA o:
+//   o:   A11^{-1} (one warp; its pivots are U_TT's diagonal, written to the
+//        factor for the guard), R2 = A11^{-1} W[P, :] with the pivot columns
+//        replaced by A11^{-1}, into R2 slot p & 1;      cluster barrier
+//   all: copy o's R2 slot over DSMEM, stage C' = own rows' pivot columns
+//        (pivot rows -e_p), own rows <- W' - C' R2 on DMMA (8 x 32 strips),
+//        W' = W with the pivot rows and columns zeroed
+// Two R2 slots: one cluster barrier per pass (pass p + 2 reuses slot p & 1
+// only after every CTA crossed pass p + 1's barrier, i.e. finished copying).
+// Measured slower than the global-memory kernel (1354/256: 5.9 against 3.0 ms
+// per refactor; pushing R2 with DSMEM stores instead of pulling it: 7.2 ms):
+// the per-pass chain (one warp's A11 inverse, R2, the DSMEM transfer, the
+// cluster barrier) is serial while 6 of 7 CTAs wait, and only 2 clusters of
+// 7-8 one-CTA-per-SM members fit a GPC.  Kept for the record, not the default.
+constexpr int kCgjLdb = 20;
+inline __host__ __device__ int cgj_ldr(int tl) { return ((tl + 15) & ~15) + 4; }
+inline size_t cgj_smem_bytes(int tl, int rb) {
+  return (size_t(rb) * cgj_ldr(tl) + size_t(2) * kGjB * cgj_ldr(tl) + size_t(rb) * kCgjLdb +
+          size_t(kGjB) * kCgjLdb) *
+         sizeof(double);
+}
+
+template <int BLOCK>
+__global__ void __launch_bounds__(BLOCK)
+    refactor_tail_cgj_kernel(DevLu P, double* F, double* D, const double* __restrict__ scale_in,
+                             int* status, double piv_tol, int rb) {
+  constexpr int kB = kGjB, kLb = kCgjLdb, kWarps = BLOCK / 32;
+  extern __shared__ double cgj[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int R = int(cluster.num_blocks()), cr = int(cluster.block_rank());
+  const int s = blockIdx.x / R;
+  double* Fs = F + size_t(s) * P.nnz_f;
+  const int tl = P.tl, tt = tl * tl, t0 = P.t0;
+  const int ldr = cgj_ldr(tl);
+  double* Wl = cgj;                        // [rb][ldr] own rows of W
+  double* R2s = Wl + size_t(rb) * ldr;     // [2][kB][ldr]
+  double* Cp = R2s + size_t(2) * kB * ldr;  // [rb][kLb] C'
+  double* Ai = Cp + size_t(rb) * kLb;      // [kB][kLb] A11^{-1}
+  const int r0 = cr * rb, nr = max(0, min(rb, tl - r0));
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gm = lane >> 2, gk = lane & 3;
+  // own rows of S from the factor (zero beyond tl: padding columns stay 0)
+  for (int i = warp; i < rb; i += kWarps) {
+    const int gi = r0 + i;
+    for (int j = lane; j < ldr; j += 32) {
+      double v = 0.0;
+      if (i < nr && j < tl) {
+        const int src = gi > j ? P.dense_src[j * tl + gi] : P.dense_src[tt + j * tl + gi];
+        v = src >= 0 ? Fs[src] : 0.0;
+      }
+      Wl[i * ldr + j] = v;
+    }
+  }
+  cluster.sync();
+  const int npass = (tl + kB - 1) / kB, ntp = (tl + 7) / 8, nch = (tl + 31) / 32;
+  for (int p = 0; p < npass; ++p) {
+    const int k0 = p * kB, bb = min(kB, tl - k0), o = k0 / rb;
+    double* R2 = R2s + size_t(p & 1) * kB * ldr;
+    if (cr == o) {
+      const int lr0 = k0 - r0;
+      if (warp == 0) {  // A11^{-1} by Gauss-Jordan, lane = column (identity-padded)
+        double col[kB], inv[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+          col[r] = (lane < bb && r < bb) ? Wl[(lr0 + r) * ldr + k0 + lane] : (r == lane ? 1.0 : 0.0);
+          inv[r] = (r == lane) ? 1.0 : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+          const double piv = __shfl_sync(0xffffffffu, col[k], k);
+          if (lane == 0 && k < bb) Fs[P.diag[t0 + k0 + k]] = piv;
+          const double rp = 1.0 / piv;
+          col[k] *= rp;
+          inv[k] *= rp;
+#pragma unroll
+          for (int r = 0; r < kB; ++r) {
+            const double f = __shfl_sync(0xffffffffu, col[r], k);
+            if (r != k) {
+              col[r] -= f * col[k];
+              inv[r] -= f * inv[k];
+            }
+          }
+        }
+        if (lane < kB)
+#pragma unroll
+          for (int r = 0; r < kB; ++r) Ai[r * kLb + lane] = inv[r];
+      }
+      __syncthreads();
+      // R2 = A11^{-1} W[P, :] (2 x ntp fragments), pivot columns A11^{-1}
+      for (int t = warp; t < 2 * ntp; t += kWarps) {
+        const int I = t & 1, J = t >> 1;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < kB; kk += 4)
+          gj_dmma(d0, d1, Ai[(I * 8 + gm) * kLb + kk + gk], Wl[(lr0 + kk + gk) * ldr + J * 8 + gm]);
+        const int r = I * 8 + gm, c = J * 8 + 2 * gk;
+        R2[r * ldr + c] = (c >= k0 && c < k0 + bb) ? Ai[r * kLb + c - k0] : d0;
+        R2[r * ldr + c + 1] = (c + 1 >= k0 && c + 1 < k0 + bb) ? Ai[r * kLb + c + 1 - k0] : d1;
+      }
+    }
+    cluster.sync();  // R2 of pass p complete in o's slot
+    if (cr != o) {
+      const double2* src = reinterpret_cast<const double2*>(cluster.map_shared_rank(R2, o));
+      double2* dst = reinterpret_cast<double2*>(R2);
+      for (int q = tid; q < kB * ldr / 2; q += BLOCK) dst[q] = src[q];
+    }
+    for (int q = tid; q < rb * kB; q += BLOCK) {
+      const int i = q / kB, pp = q % kB, gi = r0 + i;
+      double v = 0.0;
+      if (pp < bb && i < nr)
+        v = (gi >= k0 && gi < k0 + bb) ? (gi - k0 == pp ? -1.0 : 0.0) : Wl[i * ldr + k0 + pp];
+      Cp[i * kLb + pp] = v;
+    }
+    __syncthreads();
+    // own rows <- W' - C' R2 (in place: an element's update reads itself and
+    // the staged operands only)
+    for (int it = warp; it < (nr + 7) / 8 * nch; it += kWarps) {
+      const int I = it / nch, ch = it % nch;
+      const int r = I * 8 + gm, gi = r0 + r;
+      double af[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) af[kk] = Cp[r * kLb + 4 * kk + gk];
+      const double* r2 = R2 + gk * ldr + ch * 32 + gm;
+      double d[4][2];
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        d[jj][0] = d[jj][1] = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          gj_dmma(d[jj][0], d[jj][1], af[kk], r2[4 * kk * ldr + 8 * jj]);
+      }
+      const bool prow = gi >= k0 && gi < k0 + bb;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int c = ch * 32 + 8 * jj + 2 * gk + v;
+          if (r < nr && c < ldr) {
+            const bool z = prow || (c >= k0 && c < k0 + bb);
+            Wl[r * ldr + c] = (z ? 0.0 : Wl[r * ldr + c]) - d[jj][v];
+          }
+        }
+    }
+    __syncthreads();  // the next pass's pivot rows are final before o reads them
+  }
+  // W (row-major) to D's W slot
+  double* W = D + size_t(s) * 2 * tt;
+  for (int i = warp; i < nr; i += kWarps)
+    for (int j = lane; j < tl; j += 32) W[size_t(r0 + i) * tl + j] = Wl[i * ldr + j];
+  cluster.sync();  // every owner's pivots are in the factor before the guard
+  if (cr != 0) return;
+  double bad = 0.0, big = 0.0;
+  const double floor_ = piv_tol * fmax(scale_in[s], 1e-300);
+  for (int j = tid; j < P.n; j += BLOCK) {
+    const double dd = Fs[P.diag[j]];
+    if (!(fabs(dd) >= floor_) || !isfinite(dd)) bad = 1.0;
+  }
+  for (int q = tid; q < P.nnz_f; q += BLOCK) big = fmax(big, fabs(Fs[q]));
+  bad = block_reduce<BLOCK>(bad, true);
+  big = block_reduce<BLOCK>(big, true);
+  if (tid == 0) status[s] = bad > 0.0 ? 1 : (big > P.growth * fmax(scale_in[s], 1e-300) ? 2 : 0);
+}
+
 // the solve layouts after the Gauss-Jordan tail, spread over the whole GPU:
 // FT and VS gathers from F, W' = transpose(W)
 __global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, double* FT,
@@ -914,6 +1082,50 @@ size_t single_rhs_smem(int n_x) {
   return b <= 200 * 1024 ? b : 0;
 }
 
+// the cluster-resident Gauss-Jordan (opt-in) when a cluster of <= 16 CTAs
+// holds the tail (rb = 48 or 32 rows per CTA); false: the global-memory kernel
+static bool cgj_launch(const DevLu& P, int M, double* F, double* D, const double* scale,
+                       int* status, double piv_tol, cudaStream_t st) {
+  static const int resident = [] {
+    const char* e = std::getenv("BIPM_GJ_CLUSTER_RESIDENT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (!resident || P.tl <= 0) return false;
+  int rb = 0;
+  for (int cand : {48, 32})
+    if (cgj_smem_bytes(P.tl, cand) <= 227 * 1024 && (P.tl + cand - 1) / cand <= 16) {
+      rb = cand;
+      break;
+    }
+  if (rb == 0) return false;
+  const int R = (P.tl + rb - 1) / rb;
+  const size_t smem = cgj_smem_bytes(P.tl, rb);
+  cudaFuncSetAttribute(refactor_tail_cgj_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       int(smem));
+  if (R > 8)
+    cudaFuncSetAttribute(refactor_tail_cgj_kernel<512>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr{};
+  cfg.gridDim = dim3(M * R);
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = R;
+  attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, refactor_tail_cgj_kernel<512>, P, F, D, scale, status, piv_tol,
+                         rb) != cudaSuccess) {
+    cudaGetLastError();  // cluster shape not launchable here: the global-memory kernel
+    return false;
+  }
+  note_launch();
+  check_launch("refactor_tail_cgj");
+  return true;
+}
+
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
                         int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st) {
@@ -927,6 +1139,9 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status,
                                                               piv_tol, vs_src, nnz_vs, VS);
+  } else if (cgj_launch(P, M, F, D, scale, status, piv_tol, st)) {
+    refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
+                                                     M);
   } else {
     const size_t gsm = gj_smem_bytes(P.tl);
     cudaFuncSetAttribute(refactor_tail_gj_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
