@@ -433,7 +433,10 @@ LuPlan make_lu_plan(const Csr& A) {
   // dense tail: move the top levels of the etree to the end of the order
   // (same elimination tree, same fill) and redo the symbolic pass
   {
-    idx width = kTailWidth, max_rows = kMaxTail;
+    // large grids (n >= kWideTailN): the wide tail (measured, round 2, with the
+    // presolved reduction: 9241/16 345 -> 300 ms and 2869/64 40.5 -> 35.6 ms per
+    // reduction + refactor; at 1354 the tl^3 Gauss-Jordan outgrows the gain)
+    idx width = n >= kWideTailN ? 32 : kTailWidth, max_rows = n >= kWideTailN ? kMaxTailLimit : kMaxTail;
     if (const char* e = std::getenv("BIPM_TAIL_WIDTH")) width = std::atoi(e);
     if (const char* e = std::getenv("BIPM_TAIL_MAX"))
       max_rows = std::max<idx>(0, std::min<idx>(kMaxTailLimit, std::atoi(e)));

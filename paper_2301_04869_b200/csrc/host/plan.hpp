@@ -126,6 +126,7 @@ struct LuPlan {
 constexpr idx kTailWidth = 16;
 constexpr idx kMaxTail = 320;
 constexpr idx kMaxTailLimit = 512;  // the Gauss-Jordan kernel's limit (env BIPM_TAIL_MAX up to it)
+constexpr idx kWideTailN = 4000;    // n >= this: width 32, up to kMaxTailLimit rows
 
 std::vector<idx> min_degree_order(const Csr& sym_pattern);
 LuPlan make_lu_plan(const Csr& gx_pattern);
