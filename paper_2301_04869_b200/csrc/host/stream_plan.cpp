@@ -18,7 +18,7 @@ struct Builder {
   const int max_bytes;
   std::vector<int> group;  // row -> warp of its subtree (-1: team levels); empty: none
   int warp_rr = 0;  // round-robin position of the next unit chunk (all-warp steps)
-  int last_team = 16;
+  int last_team = 16;  // reset to the all-consumer team (consumers / 32) by build_stream_program
   struct Pending {
     int kind, flags, aux0, aux1;
     std::vector<int> items;  // 4 ints per item
@@ -271,7 +271,7 @@ struct Builder {
     }
     flush();
     if (any_wl && !sw.forward) warp_local(wl, diag, sw, slot_of_t);
-    last_team = 16;  // the steps after a sweep start with an all-consumer barrier
+    last_team = S.consumers / 32;  // the steps after a sweep start with an all-consumer barrier
   }
 
   // Warp-local part of a sweep: kStepSweepW steps, each holding the next
@@ -535,6 +535,7 @@ StreamProgram build_stream_program(const LuPlan& L, const Csr& gu, const Csr& kx
   S.stride[kArrYN] = presolved ? reach->nnz_yn : 0;
   // stride[kArrSweep] is fixed after the program is built (nnz_vs, even)
   Builder B{S, S.max_step_bytes, {}};
+  B.last_team = consumers / 32;
   // warp-local subtree sweeps: correct, measured no faster at 1354/256
   // (23.5 -> 24.1 ms per reduction: the per-warp level chains, not the team
   // barriers, bound the sweeps), so off unless BIPM_SUBTREE=1
