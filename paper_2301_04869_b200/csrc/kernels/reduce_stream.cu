@@ -475,7 +475,7 @@ __device__ __forceinline__ void step_dense_global(const double* __restrict__ W, 
 template <int K, int C>
 __device__ __forceinline__ void step_spmv(const Hdr& h, unsigned items, unsigned col, unsigned v,
                                           unsigned sig, unsigned xb, char* S, double dw,
-                                          int tid) {
+                                          int tid, int dbg = 0) {
   using Pn = Panel<K>;
   UNIT_LOOP(h, tid, {
     const int item = Pn::NG == 1 ? unit : unit / Pn::NG;
@@ -496,7 +496,7 @@ _Pragma("unroll")
       if (t < m.z) Pn::fma(a, lds1(v + 8 * t), xb, colw<K>(col, t), cg);
     }
     reduce_lanes<Pn::CW>(a, g);
-    if (active && sub == 0) {
+    if (active && sub == 0 && !(dbg & 4)) {  // dbg 4: timing experiment without the S stores
       double x[Pn::CW];
       Pn::load(x, xb, m.x, cg);
       const double d = lds1(sig + 8 * m.w) + dw;
@@ -810,7 +810,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
       case kSpmv: {
         const int xoff = h.vcount > 0 ? ((h.vcount + 1) * 8 + 15) & ~15 : 0;
         const int xshift = ((h.par >> 2) & 1) ^ ((h.par >> 3) & s & 1);
-        step_spmv<K, C>(h, items, col, v, vals + xoff + 8 * xshift, xb, S, a.dw, tid);
+        step_spmv<K, C>(h, items, col, v, vals + xoff + 8 * xshift, xb, S, a.dw, tid, a.debug);
         break;
       }
       case kCopyBack: {

@@ -38,7 +38,7 @@ struct StreamLaunch {
   double* partial;   // [nchunks][n_u * n_u] column-major
   double* scratch;   // per CTA: n_x * K (S = K~_xx T + K_xu V staging)
   long long* phase;  // optional: clock64 per step of CTA 0's first scenario
-  int debug;         // timing experiments only (BIPM_STREAM_DEBUG): 1 skip sweeps, 2 no team barriers
+  int debug;         // timing experiments only (BIPM_STREAM_DEBUG): 1 skip sweeps, 2 no team barriers, 4 no K~_xx product stores
 };
 
 // largest consumer count per CTA (one producer warp is added)
