@@ -108,7 +108,8 @@ const void* lookup(bipm_problem* bp, const std::string& name, int64_t* count, in
     R = build_reach_plan(P.LU, P.D.g.u, P.D.g.u.cols);
     const std::map<std::string, const std::vector<idx>*> rv = {
         {"reach_yn_ptr", &R.yn_ptr}, {"reach_yn_row", &R.yn_row}, {"reach_op_ptr", &R.op_ptr},
-        {"reach_ops", &R.ops},       {"reach_ent", &R.ent}};
+        {"reach_ops", &R.ops},       {"reach_ent", &R.ent},
+        {"reach_yt_ptr", &R.yt_ptr}, {"reach_yt_row", &R.yt_row}};
     if (auto it = rv.find(name); it != rv.end()) return ints(*it->second);
   }
   const std::map<std::string, const SweepPlan*> sweeps = {

@@ -447,6 +447,7 @@ ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u) {
   const Csr gut = gu.transpose_pattern();  // column u -> (state row, G_u slot)
   R.yn_ptr.assign(size_t(n_u) + 1, 0);
   R.op_ptr.assign(size_t(n_u) + 1, 0);
+  R.yt_ptr.assign(size_t(n_u) + 1, 0);
   std::vector<idx> local(size_t(n), -1), b_of(size_t(n), -1);
   std::vector<std::vector<std::pair<idx, idx>>> in(static_cast<size_t>(n));  // row -> (col, slot)
   std::vector<idx> reach, touched_tail;
@@ -498,7 +499,11 @@ ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u) {
       emit_op(reach[k], idx(k));
       R.yn_row.push_back(reach[k]);
     }
-    for (idx t : touched_tail) emit_op(t, -1 - (t - t0));
+    for (idx t : touched_tail) {
+      emit_op(t, -1 - (t - t0));
+      R.yt_row.push_back(t - t0);
+    }
+    R.yt_ptr[size_t(u) + 1] = idx(R.yt_row.size());
     R.yn_ptr[size_t(u) + 1] = idx(R.yn_row.size());
     R.op_ptr[size_t(u) + 1] = idx(R.ops.size() / 4);
     for (idx r : reach) local[size_t(r)] = -1;

@@ -127,6 +127,9 @@ struct ReachPlan {
   // yn_ptr[u] + dest, dest < 0: tail row -1 - dest (y_T); entries
   // {source y_N entry (local to the column), factor slot of L}
   std::vector<idx> op_ptr, ops, ent;
+  // pattern of y_T: column u is nonzero only on the tail rows its ops write
+  // (1354: 27 of 307), so X_T = W y_T is a sparse-dense product
+  std::vector<idx> yt_ptr, yt_row;  // [n_u + 1], tail-local rows (ascending)
   long long fmas = 0;            // entries per scenario (work measure)
 };
 ReachPlan build_reach_plan(const LuPlan& L, const Csr& gu, idx n_u);

@@ -23,6 +23,13 @@ void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz
                         const double* gu, long long gu_nnz, double* yn, double* yt,
                         cudaStream_t st);
 
+// X_T = W y_T for every scenario with y_T's column pattern (yt_ptr, yt_row,
+// tail-local rows): WT = W' = W transposed, rows of ldw doubles, scenario
+// stride sw; yt, xt [M][n_u][ldy]
+void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* yt, int ldy,
+                      const int* yt_ptr, const int* yt_row, int n_u, int tl, int M, double* xt,
+                      cudaStream_t st);
+
 // C[b](i, j) = alpha sum_k A[b][i lda + k] B[b][j ldb + k]  (both operands
 // k-contiguous, C column-major: C[b][j ldc + i]), i < m, j < n, k < kd;
 // FP64 on the tensor pipe (DMMA m8n8k4).  lda, ldb even; A, B 16-byte aligned.

@@ -41,7 +41,8 @@ def test_reach_plan_matches_dense_forward_solve(case):
     yn_ptr, yn_row = p.array("reach_yn_ptr"), p.array("reach_yn_row")
     op_ptr = p.array("reach_op_ptr")
     ops, ent = p.array("reach_ops").reshape(-1, 4), p.array("reach_ent").reshape(-1, 2)
-    assert len(yn_ptr) == n_u + 1
+    yt_ptr, yt_row = p.array("reach_yt_ptr"), p.array("reach_yt_row")
+    assert len(yn_ptr) == n_u + 1 and len(yt_ptr) == n_u + 1
     scale = np.abs(yN).max(initial=0.0) + np.abs(yT).max(initial=0.0)
     for u in range(n_u):
         rows = yn_row[yn_ptr[u]:yn_ptr[u + 1]]
@@ -59,3 +60,9 @@ def test_reach_plan_matches_dense_forward_solve(case):
                 t[-1 - dest] = v
         assert np.abs(y - yN[rows, u]).max(initial=0.0) <= 1e-13 * scale
         assert np.abs(t - yT[:, u]).max(initial=0.0) <= 1e-13 * scale
+        # y_T's pattern (the sparse X_T = W y_T product): exactly the rows the ops write
+        pat = yt_row[yt_ptr[u]:yt_ptr[u + 1]]
+        assert np.all(np.diff(pat) > 0)
+        off_t = np.ones(tl, bool)
+        off_t[pat] = False
+        assert np.all(yT[off_t, u] == 0.0), "y_T pattern incomplete"
