@@ -19,5 +19,5 @@ for c in "case1354pegase 256" "case1354pegase 32" "case2869pegase 512" "case118 
   timeout 900 python tools/profile_solve.py $1 $2 > $OUT/profile_$1_N$2.json 2>&1
 done
 timeout 900 python tools/profile_solve.py case9241pegase 128 0.05 3 > $OUT/profile_case9241pegase_N128.json 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"reduce_stream|reach_solve|gemm_tn" -c 3 -o $OUT/ncu_reduce_1354 python tools/micro_reduce.py case1354pegase 256 1 > $OUT/ncu_reduce.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"reduce_stream|reach_solve|gemm_tn|xt_sparse" -c 4 -o $OUT/ncu_reduce_1354 python tools/micro_reduce.py case1354pegase 256 1 > $OUT/ncu_reduce.log 2>&1
 ls -la $OUT
