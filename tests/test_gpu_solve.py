@@ -177,3 +177,29 @@ def test_case9241_N128_first_iterations_match_reference():
         assert int(g["corr"]) == c["corr"], (k, g["corr"], c["corr"])
         for key in ("objective", "inf_pr", "inf_du", "alpha_p", "alpha_d", "mu"):
             assert abs(g[key] - c[key]) <= 1e-6 * max(1.0, abs(c[key])), (k, key, g[key], c[key])
+
+
+def test_case2869_N512_full_solve_matches_reference():
+    """BASELINE configs[3] workload, the whole solve on one GPU: status,
+    iteration count, objective, controls, the per-iteration barrier schedule
+    and inertia corrections, and the final primal/dual iterate against the
+    reference's full run (tests/golden/make_golden.py --long: ~3 h of
+    reference CPU on 8 threads)."""
+    big = json.load(open(os.path.join(GOLDEN, "solves_large.json")))
+    key = "case2869pegase_N512_s0.05_seed0"
+    if key not in big:
+        pytest.skip("full case2869pegase/512 reference solve not generated")
+    ref = big[key]
+    p = nat.Problem(case_path("case2869pegase"), 512, 0.05, 0)
+    s = nat.Solver(nat.Context(p))
+    r = s.solve()
+    assert r["status_name"] == ref["status"] == "Optimal"
+    assert r["iterations"] == ref["iterations"]
+    assert abs(r["objective"] - ref["objective"]) <= 1e-6 * abs(ref["objective"])
+    u_ref = np.array(ref["u"])
+    assert np.abs(r["u"] - u_ref).max() <= 1e-6 * max(1.0, np.abs(u_ref).max())
+    for k, (g, c) in enumerate(zip(r["logs"], ref["logs"])):
+        assert int(g["corr"]) == c["corr"], (k, g["corr"], c["corr"])
+        assert g["mu"] == pytest.approx(c["mu"], rel=1e-9), k
+        assert g["objective"] == pytest.approx(c["objective"], rel=1e-6), k
+    compare(s.iterate(), iterate_golden("case2869pegase_N512_s005"))
