@@ -17,6 +17,7 @@
 // barrier per step.  Nothing on the consumers' critical path touches global
 // memory except the per-scenario scatter and the S round trip.
 #include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -945,7 +946,24 @@ void plan_stream_chunks(StreamLaunch& a, int sm_count) {
       best_n = ncc;
     }
   }
+  // then two scenarios per CTA when that plan is within 2 % of the cost:
+  // half the partial K_hat slabs (each chunk writes one, finish_reduce reads
+  // them all: 4.3 GB at 2869/512 with one scenario per CTA) and the producer
+  // prefetches across the scenario boundary (1354/256: 12.96 against 13.05 ms
+  // per tile kernel; 4 per CTA measured 13.14)
+  for (int nc = (a.M + 1) / 2; nc < best_n; ++nc) {
+    const int chunk = (a.M + nc - 1) / nc;
+    if (chunk > 2) continue;
+    const int ncc = (a.M + chunk - 1) / chunk;
+    const long long waves = (tiles * (long long)ncc + sm_count - 1) / sm_count;
+    if (waves * chunk * 50 <= best * 51) {
+      best_n = ncc;
+      break;
+    }
+  }
   a.chunk = (a.M + best_n - 1) / best_n;
+  if (const char* e = std::getenv("BIPM_STREAM_CHUNK"))  // experiments: scenarios per CTA
+    a.chunk = std::max(1, std::min(a.M, std::atoi(e)));
   a.nchunks = (a.M + a.chunk - 1) / a.chunk;
 }
 
