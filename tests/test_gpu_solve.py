@@ -163,16 +163,20 @@ def test_case2869_N512_first_iterations_match_reference():
             assert abs(g[key] - c[key]) <= 1e-6 * max(1.0, abs(c[key])), (k, key, g[key], c[key])
 
 
-def test_case9241_N128_first_iterations_match_reference():
+@pytest.mark.parametrize("its", [3, 10])
+def test_case9241_N128_first_iterations_match_reference(its):
     """BASELINE configs[4] (the large-n_u stress config, one GPU): the first
-    three interior-point iterations against the reference's log (the
+    3 (and 10) interior-point iterations against the reference's log (the
     reference CPU needs ~20 min per iteration on 8 threads here, so the golden
     is capped; tests/golden/make_golden.py --long)."""
-    ref = json.load(open(os.path.join(GOLDEN, "solves_large.json")))[
-        "case9241pegase_N128_s0.05_seed0_it3"]
+    big = json.load(open(os.path.join(GOLDEN, "solves_large.json")))
+    key = f"case9241pegase_N128_s0.05_seed0_it{its}"
+    if key not in big:
+        pytest.skip(f"{key} not generated")
+    ref = big[key]
     p = nat.Problem(case_path("case9241pegase"), 128, 0.05, 0)
-    r = nat.Solver(nat.Context(p), max_iter=3).solve()
-    assert r["status_name"] == "MaxIter" and r["iterations"] == ref["iterations"] == 3
+    r = nat.Solver(nat.Context(p), max_iter=its).solve()
+    assert r["status_name"] == "MaxIter" and r["iterations"] == ref["iterations"] == its
     for k, (g, c) in enumerate(zip(r["logs"], ref["logs"])):
         assert int(g["corr"]) == c["corr"], (k, g["corr"], c["corr"])
         for key in ("objective", "inf_pr", "inf_du", "alpha_p", "alpha_d", "mu"):
