@@ -1,0 +1,69 @@
+"""Every alternative path of the round-2 reduction and refactor stays at
+reference parity: each environment switch (read once per process, so each
+configuration runs in its own interpreter) is checked on the reference's
+case118 (iterate 20) and case1354pegase (N=4, iterate 40 of 55) fixtures --
+K_hat and the reduced rhs at delta_w = 0 and at the probe delta_w within the
+north-star 1e-9 of the reference."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+from conftest import case_path, GOLDEN
+from oracle.fixtures import load_npz
+from paper_2301_04869_b200 import _native as nat
+out = {}
+for name in ("case118_N4_s005_it20", "case1354pegase_N4_s005_it40"):
+    fx = load_npz(f"{GOLDEN}/{name}.npz")
+    m = fx.meta
+    ctx = nat.Context(nat.Problem(case_path(m["case"]), m["N"], m["sigma"], m["seed"]))
+    ctx.factor_gx(fx["gx"])
+    errs = []
+    for sfx, dw in (("0", 0.0), ("dw", m["dw_probe"])):
+        arrays = {k: fx[k] for k in ("gu", "kxx", "kxu", "kuu", "sigma_x", "rhat1", "rhat3",
+                                     "sigma_u", "rhat2")}
+        khat, rhs = ctx.reduce(dw, **arrays)
+        ref_k, ref_r = fx["khat_" + sfx].T, fx["rhs_" + sfx]
+        errs.append(float(np.abs(khat - ref_k).max() / np.abs(ref_k).max()))
+        errs.append(float(np.abs(rhs - ref_r).max() / max(1.0, np.abs(ref_r).max())))
+    out[name] = {"err": max(errs), "info": ctx.info()}
+print(json.dumps(out))
+"""
+
+CONFIGS = [
+    {},
+    {"BIPM_PRESOLVE": "0"},
+    {"BIPM_ADJ_IDENTITY": "0"},
+    {"BIPM_ADJ_IDENTITY": "1"},
+    {"BIPM_TAIL_DEFER": "0"},
+    {"BIPM_XT_SPARSE": "0"},
+    {"BIPM_XT_SPARSE": "1"},
+    {"BIPM_PRE_TAIL": "0"},
+    {"BIPM_STREAM_CHUNK": "1"},
+    {"BIPM_GJ_CLUSTER_RESIDENT": "1"},
+]
+
+
+@pytest.mark.parametrize("env", CONFIGS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items())
+                         or "default")
+def test_reduction_path_matches_reference(env):
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT], capture_output=True, text=True,
+                       env=dict(os.environ, **env), timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, v in res.items():
+        assert v["err"] <= 1e-9, (env, name, v)
+    if env.get("BIPM_PRESOLVE") == "0":
+        assert all(v["info"]["presolve"] == 0 for v in res.values())
+    if env.get("BIPM_ADJ_IDENTITY") == "1":
+        assert all(v["info"]["adj_identity"] == 1 for v in res.values())
