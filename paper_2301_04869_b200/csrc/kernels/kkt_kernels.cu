@@ -432,11 +432,13 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
         }
     };
     const int it0 = crank * kWarps + warp, its = kWarps * ncl;
-    double old[kSJ][2];
+    // two strips' loads in flight ahead of the current one
+    double old[kSJ][2], nx1[kSJ][2];
     load_strip(it0, old);
+    load_strip(it0 + its, nx1);
     for (int it = it0; it < nit; it += its) {
       double nxt[kSJ][2];
-      load_strip(it + its, nxt);
+      load_strip(it + 2 * its, nxt);
       const int I = it / nch, ch = it % nch;
       const int r = I * 8 + gm;
       double af[4];
@@ -467,8 +469,10 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       }
 #pragma unroll
       for (int jj = 0; jj < kSJ; ++jj) {
-        old[jj][0] = nxt[jj][0];
-        old[jj][1] = nxt[jj][1];
+        old[jj][0] = nx1[jj][0];
+        old[jj][1] = nx1[jj][1];
+        nx1[jj][0] = nxt[jj][0];
+        nx1[jj][1] = nxt[jj][1];
       }
     }
     sync_all();  // every CTA's strips of Wn written before the next pass reads them
