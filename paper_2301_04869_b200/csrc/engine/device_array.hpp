@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -24,9 +25,10 @@ inline void cuda_check(cudaError_t e, const char* what) {
 
 // Blocks freed by an owner may still be read by kernels in flight (owners
 // do not know their streams): they wait in `pending` until the next
-// allocation, which first synchronises the device once (allocations happen
-// at setup) and only then recycles them.  Cached bytes are capped; beyond the
-// cap blocks go back to the driver.
+// allocation, which first synchronises their device once (allocations happen
+// at setup) and only then recycles them.  Blocks are keyed by (rounded size,
+// device).  Cached bytes are capped; beyond the cap blocks go back to the
+// driver.
 class DeviceCache {
  public:
   static DeviceCache& get() {
@@ -35,13 +37,24 @@ class DeviceCache {
   }
   void* alloc(size_t bytes) {
     const size_t b = round(bytes);
+    int dev = 0;
+    cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(m_);
     if (!pending_.empty()) {
-      cudaDeviceSynchronize();
-      for (auto& pb : pending_) free_.emplace(pb.first, pb.second);
+      // synchronise every device the pending blocks live on, once
+      std::vector<int> devs;
+      for (const auto& pb : pending_)
+        if (std::find(devs.begin(), devs.end(), pb.first.second) == devs.end())
+          devs.push_back(pb.first.second);
+      for (int d : devs) {
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+      }
+      cudaSetDevice(dev);
+      for (const auto& pb : pending_) free_.emplace(pb.first, pb.second);
       pending_.clear();
     }
-    auto it = free_.find(b);
+    auto it = free_.find(Key{b, dev});
     if (it != free_.end()) {
       void* p = it->second;
       cached_ -= b;
@@ -60,13 +73,17 @@ class DeviceCache {
   void release(void* p, size_t bytes) {
     if (!p) return;
     const size_t b = round(bytes);
+    cudaPointerAttributes at{};
+    int dev = 0;
+    if (cudaPointerGetAttributes(&at, p) == cudaSuccess) dev = at.device;
+    cudaGetLastError();
     std::lock_guard<std::mutex> g(m_);
     if (cached_ + b > kCap) {
       cudaFree(p);  // synchronising, like the plain allocator
       return;
     }
     cached_ += b;
-    pending_.emplace_back(b, p);
+    pending_.emplace_back(Key{b, dev}, p);
   }
 
  private:
@@ -76,16 +93,25 @@ class DeviceCache {
     return (n + q - 1) / q * q;
   }
   void trim_locked() {
-    cudaDeviceSynchronize();
-    for (auto& pb : pending_) cudaFree(pb.second);
-    for (auto& kv : free_) cudaFree(kv.second);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (auto& pb : pending_) {
+      cudaSetDevice(pb.first.second);
+      cudaFree(pb.second);  // cudaFree synchronises its device
+    }
+    for (auto& kv : free_) {
+      cudaSetDevice(kv.first.second);
+      cudaFree(kv.second);
+    }
+    cudaSetDevice(dev);
     pending_.clear();
     free_.clear();
     cached_ = 0;
   }
+  using Key = std::pair<size_t, int>;  // (rounded bytes, device)
   std::mutex m_;
-  std::multimap<size_t, void*> free_;
-  std::vector<std::pair<size_t, void*>> pending_;
+  std::multimap<Key, void*> free_;
+  std::vector<std::pair<Key, void*>> pending_;
   size_t cached_ = 0;
 };
 

@@ -451,12 +451,20 @@ Engine::~Engine() {
 
 void Engine::sync() { cuda_check(cudaStreamSynchronize(st), "stream sync"); }
 
+// the padded dense slot the streamed reduction reads: both without the
+// adjoint identity (W for the first dense product, W' for the second); with
+// it, W for the X_T GEMM or W' for the sparse X_T product
+int Engine::dp_slot() const {
+  if (!use_stream || !presolve || !adj_identity) return -1;
+  return xt_sparse ? 1 : 0;
+}
+
 void Engine::factor_gx_launch() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st);
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot());
   });
 }
 
@@ -465,7 +473,7 @@ idx Engine::factor_gx() {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st);
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot());
   });
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);

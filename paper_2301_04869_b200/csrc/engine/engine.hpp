@@ -128,6 +128,7 @@ class Engine {
   ReachDev rdev{};
   DArr<int> rp_op_ptr, rp_ops, rp_ent, rp_yn_ptr, rp_yn_row, rp_yt_ptr, rp_yt_row;
   bool xt_sparse = true;  // X_T = W y_T over y_T's pattern (BIPM_XT_SPARSE=0: dense DMMA GEMM)
+  int dp_slot() const;    // which of Dp's W / W' slots the reduction reads (-1: both)
   DArr<double> YN, YT, XT, ZT;
   // adjoint identity with a deferred tail: -sum_s X_T' Z_T by one batch-sum
   // GEMM into tail_splits slabs after the kuu slab (BIPM_TAIL_DEFER=0: the

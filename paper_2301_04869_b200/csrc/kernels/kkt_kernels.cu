@@ -691,13 +691,19 @@ __global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, d
 }
 
 // W, W' (row-major tl x tl, two per scenario) -> rows padded to ldw doubles
+// (slot >= 0: that slot only, n then counts [M][tl][ldw])
 __global__ void pad_dense_kernel(const double* __restrict__ D, double* __restrict__ Dp, int tl,
-                                 int ldw, long long n) {
+                                 int ldw, long long n, int slot) {
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
        q += (long long)gridDim.x * blockDim.x) {
-    const long long row = q / ldw;  // over [M][2][tl]
+    long long row = q / ldw;  // over [M][2][tl] (or [M][tl] for one slot)
     const int j = int(q % ldw);
-    Dp[q] = j < tl ? D[row * tl + j] : 0.0;
+    long long o = q;
+    if (slot >= 0) {
+      row = (row / tl) * 2 * tl + slot * tl + row % tl;
+      o = row * ldw + j;
+    }
+    Dp[o] = j < tl ? D[row * tl + j] : 0.0;
   }
 }
 
@@ -1132,7 +1138,8 @@ static bool cgj_launch(const DevLu& P, int M, double* F, double* D, const double
 
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st) {
+                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st,
+                        int dp_slot) {
   if (M <= 0) return;
   refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
@@ -1199,9 +1206,9 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
   check_launch("refactor_tail");
   if (Dp && P.tl > 0) {
     const int ldw = (P.tl + 15) & ~15;
-    const long long n = (long long)M * 2 * P.tl * ldw;
+    const long long n = (long long)M * (dp_slot >= 0 ? 1 : 2) * P.tl * ldw;
     pad_dense_kernel<<<int(std::min<long long>((n + 255) / 256, 8 * 148)), 256, 0, st>>>(
-        D, Dp, P.tl, ldw, n);
+        D, Dp, P.tl, ldw, n, dp_slot);
     note_launch();
     check_launch("pad_dense");
   }

@@ -20,8 +20,10 @@ namespace bipm {
 // (tl + 15) & ~15 doubles, zero-filled, for the streamed reduction's dense step.
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
-                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st);
-// scale: [M] doubles of scratch (per-scenario max |G_x| for the pivot guard)
+                        int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st,
+                        int dp_slot = -1);
+// scale: [M] doubles of scratch (per-scenario max |G_x| for the pivot guard);
+// dp_slot >= 0: only W (0) or W' (1) is padded into Dp (the other is unread)
 
 struct ReduceLaunch {
   DevLu lu;
