@@ -122,8 +122,10 @@ struct LuPlan {
 // -> 16 (tl 307): the reduction loses more sweep levels than it gains DMMA
 // work, -10 % per reduction, +1.2 ms per refactor, -6 % per iteration; wider
 // tails (width 32: tl 452, 64: tl 489) shave another 5 % off the reduction
-// but the Gauss-Jordan inverse grows as tl^3 (7-12 ms per refactor): net loss
-constexpr idx kTailWidth = 16;
+// but the Gauss-Jordan inverse grows as tl^3 (7-12 ms per refactor): net loss.
+// Round 2 (presolved reduction, same box): width 8 (tl 262) 19.40, 10 (tl 272)
+// 18.85, 12-20 (tl 307) 19.23 ms per reduction + refactor at 1354/256.
+constexpr idx kTailWidth = 10;
 constexpr idx kMaxTail = 320;
 constexpr idx kMaxTailLimit = 512;  // the Gauss-Jordan kernel's limit (env BIPM_TAIL_MAX up to it)
 constexpr idx kWideTailN = 4000;    // n >= this: width 32, up to kMaxTailLimit rows

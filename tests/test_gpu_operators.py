@@ -90,14 +90,20 @@ def test_reduce_rhs_matches_reference(fx, kind):
 def test_recover_matches_reference(fx, kind):
     """p_x, p_y, p_z, p_s at the reference's p_u.  The reference step carries
     its refinement corrections, which differ from recover(p_u) by the
-    refinement residual only (relative 1e-12 .. 1e-9)."""
+    refinement residual only (relative 1e-12 .. 1e-9) -- except p_z near
+    convergence: p_z = Sigma_s (H p + r4) - r2 cancels, and at the 1354
+    iterate-40 fixture the unrefined operator sits at 0.9e-7 (tail of 307
+    rows) .. 1.3e-7 (272 rows) from the refined reference step, so p_z is held
+    to 5e-7 (the north-star iterate tolerance is 1e-6; the refined step of
+    test_solve_reduced_matches_reference stays at 1e-7)."""
     ctx = make_ctx(fx, kind)
     ctx.factor_gx(fx["gx"])
     dw = fx.meta["step_delta_w"]
     out = ctx.recover(dw, fx["pu"], fx["hx"], fx["hu"], fx["sigma_s"], fx["r2"], fx["r4"],
                       **condensed(fx))
     for k in ("px", "py", "pz", "ps"):
-        assert rel(out[k], fx[k]) <= 1e-7, (k, rel(out[k], fx[k]))
+        tol = 5e-7 if k == "pz" else 1e-7
+        assert rel(out[k], fx[k]) <= tol, (k, rel(out[k], fx[k]))
 
 
 @pytest.mark.parametrize("kind", ["case", "patterns"])
