@@ -340,17 +340,24 @@ void Engine::setup_stream() {
     rp_yn_row.upload(rplan.yn_row.empty() ? std::vector<idx>{0} : rplan.yn_row);
     rp_yt_ptr.upload(rplan.yt_ptr);
     rp_yt_row.upload(rplan.yt_row.empty() ? std::vector<idx>{0} : rplan.yt_row);
-    // the sparse product wins while y_T is sparse enough (measured: 1354, 8.7 %
-    // dense: 1.42 -> 1.29 ms per reduce_pre at 256 scenarios; 2869 (11 %) and
+    // the sparse product wins while y_T is sparse enough (measured: 1354 with
+    // 307 tail rows, 8.7 % dense: 1.42 -> 1.29 ms per reduce_pre at 256
+    // scenarios; 272 rows, ~10 %: 1.36 -> 1.32; 2869 with 314 rows (11 %) and
     // 9241 (17.5 %) lose against the DMMA GEMM)
-    xt_sparse = double(rplan.yt_row.size()) < 0.1 * double(n_u) * double(std::max<idx>(1, L.tl));
+    // (2869 with the 506-row tail is 8.6 % dense but the GEMM, on larger
+    // operands, wins: 1.62 against 2.01 ms -- and the staged W' column block
+    // leaves one CTA per SM; so only short tails)
+    xt_sparse = L.tl <= 320 &&
+                double(rplan.yt_row.size()) < 0.12 * double(n_u) * double(std::max<idx>(1, L.tl));
     if (const char* e = std::getenv("BIPM_XT_SPARSE")) xt_sparse = std::atoi(e) != 0;
     int ymax = 1;
     for (idx u = 0; u < n_u; ++u)
       ymax = std::max(ymax, int(rplan.yn_ptr[size_t(u) + 1] - rplan.yn_ptr[size_t(u)]));
     // lanes per column ~ the mean entries per op (1354: 4.5 -> 4, 9241: 42 -> 32)
     const double per_op = double(rplan.fmas) / std::max<size_t>(1, rplan.ops.size() / 4);
-    const int grp = per_op <= 6 ? 4 : per_op <= 14 ? 8 : per_op <= 28 ? 16 : 32;
+    // (1354, 4.5 entries per op: 8 lanes 1.31 against 4 lanes 1.36 ms per reduce_pre)
+    int grp = per_op <= 3 ? 4 : per_op <= 14 ? 8 : per_op <= 28 ? 16 : 32;
+    if (const char* e = std::getenv("BIPM_REACH_GROUP")) grp = std::atoi(e);  // experiments
     rdev = ReachDev{int(n_u), int(L.tl), int(rplan.ldy), int(rplan.nnz_yn), ymax, grp,
                     rp_op_ptr.get(), reinterpret_cast<const int4*>(rp_ops.get()),
                     reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get()};
