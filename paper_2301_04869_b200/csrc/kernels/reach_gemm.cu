@@ -5,12 +5,14 @@
 // The reference solves every column of every tile with the whole L factor
 // (reduce_group, kkt.cpp:388-404: spsm over n_x rows per column); column u
 // of L^{-1} P G_u is nonzero only on the reach of G_u's rows in the graph of
-// L, a few etree paths.  reach_solve_kernel walks exactly those rows (one
-// warp per (scenario, column), the column's y_N in shared memory, factor
-// values staged a segment at a time with all loads in flight), then gathers
-// the tail rows y_T = (P G_u)_T - L_TN y_N.  gemm_tn_kernel then forms
-// X_T = W y_T for all n_u columns at once (W read once per scenario instead
-// of once per column tile of the reduction).
+// L, a few etree paths.  reach_solve_kernel walks exactly those rows (a
+// group of 4-32 lanes per (scenario, column), the column's y_N in shared
+// memory, factor values staged a segment at a time with all loads in
+// flight), then gathers the tail rows y_T = (P G_u)_T - L_TN y_N.  X_T = W y_T
+// is then formed for all n_u columns at once -- by gemm_tn_kernel (FP64 DMMA)
+// or, when y_T is sparse enough, by xt_sparse_kernel -- so W is read once per
+// scenario instead of once per column tile of the reduction.  gemm_tn_kernel
+// also forms the batch-sum tail product -sum_s X_T' Z_T after the tiles.
 #include <stdexcept>
 #include <string>
 
