@@ -215,6 +215,30 @@ __global__ void ad_slack_kernel(DevAd A, AdBuffers b) {
 }
 
 // f = L_f psi, g = L_g psi, h = L_h psi
+// The objective row (~2 ngen terms: 520 at 1354) as one lane's sequential
+// loop was the values kernel's long pole (65 dependent rounds of loads).  Here
+// a warp per scenario forms the products in parallel, 256 at a time, and one
+// lane adds them in the reference's order (autodiff.cpp:265-279): the same
+// rounded products, the same sequence of rounded sums (-fmad=false).
+constexpr int kObjChunk = 256;
+__global__ void __launch_bounds__(256) ad_objective_kernel(DevAd A, AdBuffers b) {
+  __shared__ double prod[8][kObjChunk];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int s = blockIdx.x * 8 + warp;
+  if (s >= A.M) return;
+  const int e0 = A.Lf_ptr[0], e1 = A.Lf_ptr[1];
+  double v = 0.0;
+  for (int c = e0; c < e1; c += kObjChunk) {
+    const int n = min(kObjChunk, e1 - c);
+    for (int k = lane; k < n; k += 32) prod[warp][k] = A.Lf_val[c + k] * b.psi[em(A, A.Lf_ind[c + k], s)];
+    __syncwarp();
+    if (lane == 0)
+      for (int k = 0; k < n; ++k) v += prod[warp][k];
+    __syncwarp();
+  }
+  if (lane == 0) b.f[s] = v;
+}
+
 __global__ void __launch_bounds__(256) ad_values_kernel(DevAd A, AdBuffers b) {
   const int R = 1 + A.n_x + A.m;
   tile_rows(
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(256) ad_values_kernel(DevAd A, AdBuffers b) {
         const double* val;
         int row;
         if (r == 0) {
-          ptr = A.Lf_ptr, ind = A.Lf_ind, val = A.Lf_val, row = 0;
+          return 0.0;  // ad_objective_kernel
         } else if (r <= A.n_x) {
           row = r - 1;
           ptr = A.Lg_ptr, ind = A.Lg_ind, val = A.Lg_val;
@@ -251,7 +275,7 @@ __global__ void __launch_bounds__(256) ad_values_kernel(DevAd A, AdBuffers b) {
       },
       [&](int r, int s, double v) {
         if (r == 0)
-          b.f[s] = v;
+          return;
         else if (r <= A.n_x)
           b.g[size_t(s) * A.n_x + (r - 1)] = v;
         else
@@ -499,7 +523,8 @@ void launch_ad_bundle(const DevAd& A, const AdBuffers& b, cudaStream_t st) {
   ad_slack_kernel<true><<<blocks(M * (A.nsd + 1)), kB, 0, st>>>(A, b);
   note_launch();
   ad_values_kernel<<<tiles(1 + A.n_x + A.m, A.M), 256, 0, st>>>(A, b);
-  note_launch();
+  ad_objective_kernel<<<int((M + 7) / 8), 256, 0, st>>>(A, b);
+  note_launch(2);
   ad_jacobian_kernel<<<tiles(A.gx.n + A.gu.n + A.hx.n + A.hu.n, A.M), 256, 0, st>>>(A, b);
   note_launch();
   ad_weights_kernel<<<blocks(M * A.n_b), kB, 0, st>>>(A, b);
@@ -519,7 +544,8 @@ void launch_ad_values(const DevAd& A, const AdBuffers& b, cudaStream_t st) {
   ad_slack_kernel<false><<<blocks(M * (A.nsd + 1)), kB, 0, st>>>(A, b);
   note_launch();
   ad_values_kernel<<<tiles(1 + A.n_x + A.m, A.M), 256, 0, st>>>(A, b);
-  note_launch();
+  ad_objective_kernel<<<int((M + 7) / 8), 256, 0, st>>>(A, b);
+  note_launch(2);
   check("ad_values");
 }
 
