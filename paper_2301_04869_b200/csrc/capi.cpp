@@ -327,6 +327,7 @@ void upload_condensed(Engine& e, const bipm_condensed* in) {
     throw Error(kInvalidArgument, "condensed system: null array");
   const size_t Ms = size_t(e.M), nx = Ms * size_t(e.pb.M.n_x);
   const DerivPlan& D = e.pb.D;
+  e.invalidate_reach();  // G_u changes: the reach solve of the last factor is stale
   e.bd().gu.copy_from(in->gu, Ms * size_t(D.g.u.nnz()), e.st);
   e.kxx.copy_from(in->kxx, Ms * size_t(D.kxx.out.nnz()), e.st);
   e.kxu.copy_from(in->kxu, Ms * size_t(D.kxu.out.nnz()), e.st);
@@ -353,6 +354,7 @@ void upload_augmented(Engine& e, KktStep& k, const bipm_augmented* a) {
                   e.lo + idx(i / size_t(std::max(1, e.pb.M.m))));
   Engine::Bundle& b = e.bd();
   const size_t nx = size_t(e.M) * size_t(e.pb.M.n_x);
+  e.invalidate_reach();
   b.gx.copy_from(a->gx, b.gx.size(), e.st);
   b.gu.copy_from(a->gu, b.gu.size(), e.st);
   b.hx.copy_from(a->hx, b.hx.size(), e.st);

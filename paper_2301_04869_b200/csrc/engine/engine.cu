@@ -101,6 +101,8 @@ Engine::Engine(const Problem& problem, int dev, idx lo_, idx hi_)
   cuda_check(cudaStreamCreateWithFlags(&st_rhs, cudaStreamNonBlocking), "stream");
   cuda_check(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming), "event");
   cuda_check(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_levels, cudaEventDisableTiming), "event");
+  cuda_check(cudaEventCreateWithFlags(&ev_reach, cudaEventDisableTiming), "event");
   if (const char* e = std::getenv("BIPM_NO_OVERLAP")) overlap_rhs = std::atoi(e) == 0;
   const DerivPlan& D = pb.D;
   const LuPlan& L = pb.LU;
@@ -450,6 +452,8 @@ Engine::~Engine() {
   for (cudaEvent_t e : event_pool) cudaEventDestroy(e);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_levels) cudaEventDestroy(ev_levels);
+  if (ev_reach) cudaEventDestroy(ev_reach);
   if (st) {
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -466,13 +470,36 @@ int Engine::dp_slot() const {
   return xt_sparse ? 1 : 0;
 }
 
+bool Engine::reach_overlap() const { return use_stream && presolve && overlap_rhs && st_rhs; }
+
+void Engine::invalidate_reach() {
+  // a stale reach still in flight on st_rhs must not overlap what st does
+  // next with G_u, y_N, y_T
+  if (reach_ready) cuda_check(cudaStreamWaitEvent(st, ev_reach, 0), "reach join");
+  reach_ready = false;
+}
+
+void Engine::launch_reach_async() {
+  invalidate_reach();
+  if (!reach_overlap()) return;
+  cuda_check(cudaStreamWaitEvent(st_rhs, ev_levels, 0), "reach wait");
+  timed("reduce_pre", [&] {
+    launch_reach_solve(rdev, M, F.get(), pb.LU.nnz_f, bd().gu.get(), nnz(pb.D.g.u), YN.get(),
+                       YT.get(), st_rhs);
+  }, st_rhs);
+  cuda_check(cudaEventRecord(ev_reach, st_rhs), "reach record");
+  reach_ready = true;
+}
+
 void Engine::factor_gx_launch() {
   timed("lu_refactor", [&] {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot());
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot(),
+                       reach_overlap() ? ev_levels : nullptr);
   });
+  launch_reach_async();
 }
 
 idx Engine::factor_gx() {
@@ -480,8 +507,10 @@ idx Engine::factor_gx() {
     launch_lu_refactor(lu, M, bd().gx.get(), pb.D.g.x.nnz(), F.get(), FT.get(), Dt.get(),
                        lu_status.get(), 1e-12, use_stream ? sp_vs_src.get() : nullptr,
                        int(sprog.nnz_vs), use_stream ? VS.get() : nullptr,
-                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot());
+                       use_stream ? Dp.get() : nullptr, lu_scale.get(), st, dp_slot(),
+                       reach_overlap() ? ev_levels : nullptr);
   });
+  launch_reach_async();
   std::vector<int> s(static_cast<size_t>(M));
   lu_status.download(s.data(), s.size(), st);
   sync();
@@ -511,10 +540,13 @@ void Engine::reduce_local(double dw) {
     const int n_u = pb.M.n_u;
     double* kuu_part = red_partial.get() + size_t(sl.nchunks) * n_u * n_u;
     if (presolve) {
-      // forward half for all columns: y_N, y_T (reach_solve), X_T = W y_T
+      // forward half for all columns: y_N, y_T (reach_solve, already issued
+      // beside the refactor's dense tail when reach_ready), X_T = W y_T
+      if (reach_ready) cuda_check(cudaStreamWaitEvent(st, ev_reach, 0), "reach join");
       timed("reduce_pre", [&] {
-        launch_reach_solve(rdev, M, F.get(), pb.LU.nnz_f, bd().gu.get(), nnz(D.g.u), YN.get(),
-                           YT.get(), st);
+        if (!reach_ready)
+          launch_reach_solve(rdev, M, F.get(), pb.LU.nnz_f, bd().gu.get(), nnz(D.g.u), YN.get(),
+                             YT.get(), st);
         const int tl = int(pb.LU.tl);
         if (xt_sparse) {
           // W' = W transposed is Dp's second slot (rows padded to dense_ld)
@@ -888,6 +920,9 @@ idx Engine::eval_bundle(Bundle& out, const double* dX, const double* du, const d
                         const double* dZ, double obj_w, bool check) {
   if (!pb.has_model())
     throw Error(kInvalidArgument, "eval_bundle: the problem was built from patterns only");
+  // a reach solve still reading a bundle's G_u must finish before any bundle
+  // is rewritten (the async one reads bd(); a trial bundle becomes bd() on swap)
+  invalidate_reach();
   AdBuffers b{};
   b.X = dX;
   b.u = du;

@@ -97,7 +97,10 @@ class Engine {
   int cur = 0;
   Bundle& bd() { return bundles[cur]; }
   Bundle& trial() { return bundles[1 - cur]; }
-  void swap_bundles() { cur = 1 - cur; }
+  void swap_bundles() {
+    cur = 1 - cur;
+    invalidate_reach();
+  }
   // AD program + scratch
   std::vector<DArr<int>> ad_i;
   std::vector<DArr<double>> ad_d;
@@ -129,6 +132,16 @@ class Engine {
   DArr<int> rp_op_ptr, rp_ops, rp_ent, rp_yn_ptr, rp_yn_row, rp_yt_ptr, rp_yt_row;
   bool xt_sparse = true;  // X_T = W y_T over y_T's pattern (BIPM_XT_SPARSE=0: dense DMMA GEMM)
   int dp_slot() const;    // which of Dp's W / W' slots the reduction reads (-1: both)
+  // the reach solve (y_N, y_T) of the current factor and G_u, issued on
+  // st_rhs right after the refactor's non-tail levels so it runs beside the
+  // dense-tail Gauss-Jordan (whose second wave leaves SMs idle); reduce_local
+  // waits on ev_reach.  Invalidated when G_u changes (operator uploads,
+  // bundle swap) -- reduce_local then solves it on st itself.
+  bool reach_ready = false;
+  cudaEvent_t ev_levels = nullptr, ev_reach = nullptr;
+  void launch_reach_async();
+  void invalidate_reach();
+  bool reach_overlap() const;
   DArr<double> YN, YT, XT, ZT;
   // adjoint identity with a deferred tail: -sum_s X_T' Z_T by one batch-sum
   // GEMM into tail_splits slabs after the kuu slab (BIPM_TAIL_DEFER=0: the

@@ -1139,11 +1139,12 @@ static bool cgj_launch(const DevLu& P, int M, double* F, double* D, const double
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
                         int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st,
-                        int dp_slot) {
+                        int dp_slot, cudaEvent_t after_levels) {
   if (M <= 0) return;
   refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
   check_launch("refactor_levels");
+  if (after_levels) cudaEventRecord(after_levels, st);
   const size_t smem = size_t(2) * P.tl * P.tl * sizeof(double);
   if (smem <= 200 * 1024) {
     cudaFuncSetAttribute(refactor_tail_kernel<kLuBlock>,

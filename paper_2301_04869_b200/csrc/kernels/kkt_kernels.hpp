@@ -21,9 +21,11 @@ namespace bipm {
 void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, double* F,
                         double* FT, double* D, int* status, double piv_tol, const int* vs_src,
                         int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st,
-                        int dp_slot = -1);
+                        int dp_slot = -1, cudaEvent_t after_levels = nullptr);
 // scale: [M] doubles of scratch (per-scenario max |G_x| for the pivot guard);
-// dp_slot >= 0: only W (0) or W' (1) is padded into Dp (the other is unread)
+// dp_slot >= 0: only W (0) or W' (1) is padded into Dp (the other is unread);
+// after_levels: recorded on st once the non-tail factor (L_NN, L_TN, U_N*)
+// is final, before the dense tail (the reach solve needs nothing more)
 
 struct ReduceLaunch {
   DevLu lu;
