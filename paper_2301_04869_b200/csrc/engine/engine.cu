@@ -519,11 +519,12 @@ idx Engine::factor_gx() {
   return -1;
 }
 
-void Engine::condense_blocks() {
-  timed("condense", [&] { condense_launch(); });
+void Engine::condense_blocks(cudaStream_t on) {
+  timed("condense", [&] { condense_launch(on); }, on);
 }
 
-void Engine::condense_launch() {
+void Engine::condense_launch(cudaStream_t on) {
+  cudaStream_t st = on ? on : this->st;
   const DerivPlan& D = pb.D;
   const int m = pb.M.m;
   launch_condense(cxx.v, M, bd().wxx.get(), D.wxx.nnz(), bd().hx.get(), D.h.x.nnz(), bd().hx.get(), D.h.x.nnz(),

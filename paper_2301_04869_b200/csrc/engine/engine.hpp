@@ -170,8 +170,8 @@ class Engine {
   idx factor_gx();
   void factor_gx_launch();  // refactor only; statuses stay in lu_status
   // condense (kkt.cpp:123-170) of the K blocks from the bundle and sigma_s
-  void condense_blocks();
-  void condense_launch();
+  void condense_blocks(cudaStream_t on = nullptr);
+  void condense_launch(cudaStream_t on = nullptr);
   // local part of reduce (kkt.cpp:371-466): khat/rhs partial sums over the
   // owned scenarios, without the sigma_u / rhat2 terms.
   void reduce_local(double delta_w);

@@ -62,6 +62,39 @@ void KktStep::condense() {
   condensed_u_sum(rhat2_part.get(), r1u.get(), e.rhat2.get());
 }
 
+void KktStep::condense_begin() {
+  if (!e.overlap_rhs || !e.st_rhs) {
+    cond_forked = false;
+    return;
+  }
+  if (!ev_cond0) {
+    cuda_check(cudaEventCreateWithFlags(&ev_cond0, cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_cond1, cudaEventDisableTiming), "event");
+  }
+  Engine::Bundle& bd = e.bd();
+  cudaStream_t s = e.st_rhs;
+  cuda_check(cudaEventRecord(ev_cond0, e.st), "fork");
+  cuda_check(cudaStreamWaitEvent(s, ev_cond0, 0), "fork");
+  cuda_check(cudaMemcpyAsync(e.rhat3.get(), bd.g.get(), e.rhat3.size() * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s),
+             "rhat3");
+  e.condense_blocks(s);
+  launch_condensed_rhs(d, e.hx_p.v, e.hu_p.v, bd.hx.get(), bd.hu.get(), e.sigma_s.get(),
+                       e.r4.get(), e.r2.get(), r1x.get(), e.rhat1.get(), rhat2_part.get(), s);
+  cuda_check(cudaEventRecord(ev_cond1, s), "join");
+  cond_forked = true;
+}
+
+void KktStep::condense_end() {
+  if (!cond_forked) {
+    condense();
+    return;
+  }
+  cuda_check(cudaStreamWaitEvent(e.st, ev_cond1, 0), "join");
+  condensed_u_sum(rhat2_part.get(), r1u.get(), e.rhat2.get());
+  cond_forked = false;
+}
+
 void KktStep::factor_launch() { e.factor_gx_launch(); }
 
 void KktStep::check_factor(const DArr<int>* interior_flag) {

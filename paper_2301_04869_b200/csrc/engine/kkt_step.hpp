@@ -47,6 +47,12 @@ class KktStep {
 
   // condense (kkt.cpp:123-170): K blocks and rhat1 / rhat2 / rhat3 (= g)
   void condense();
+  // the same split around the refactor: condense_begin forks the per-scenario
+  // part onto the engine's side stream (it only reads the bundle and writes
+  // the condensed blocks, so it runs beside the refactor's levels kernel);
+  // condense_end joins it and does the cross-scenario rhat2 sum on st
+  void condense_begin();
+  void condense_end();
   // batched refactor of G_x (statuses stay on the device until check_factor)
   void factor_launch();
   // one host round trip for the refactor statuses and, when given, a device
@@ -75,6 +81,17 @@ class KktStep {
   DArr<double> partial, scal;
   DArr<double> khat0, khat1, rhs0, rhs1;  // attempts 0 and 1 of the current step
   double dw0 = 0.0, dw1 = 0.0;
+  // condense_begin / condense_end (events owned here, destroyed with the step)
+  cudaEvent_t ev_cond0 = nullptr, ev_cond1 = nullptr;
+  bool cond_forked = false;
+
+ public:
+  KktStep(const KktStep&) = delete;
+  KktStep& operator=(const KktStep&) = delete;
+  ~KktStep() {
+    if (ev_cond0) cudaEventDestroy(ev_cond0);
+    if (ev_cond1) cudaEventDestroy(ev_cond1);
+  }
 };
 
 }  // namespace bipm

@@ -158,8 +158,9 @@ void Solver::compute_step(const DevIter& it) {
   launch_assemble_xs(d, it, b, bd.grad.get(), bd.h.get(), mu, e.sigma_x.get(), kkt.r1x.get(),
                      e.sigma_s.get(), e.r2.get(), e.r4.get(), flag.get(), e.st);
   launch_assemble_u(d, it, b, gsum_u.get(), mu, e.sigma_u.get(), kkt.r1u.get(), flag.get(), e.st);
-  kkt.condense();
+  kkt.condense_begin();  // per-scenario condensation beside the refactor (side stream)
   kkt.factor_launch();
+  kkt.condense_end();
   kkt.check_factor(&flag);  // one round trip: interiority flag + refactor statuses
   kkt.solve(delta_w_last, o.reg);
   reductions = kkt.reductions;
