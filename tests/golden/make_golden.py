@@ -214,7 +214,8 @@ def dumps2():
 LONG = [  # (case, N, sigma, seed, max_iter, keep the iterate)
     ("case9241pegase", 128, 0.05, 0, 3, False),
     ("case2869pegase", 512, 0.05, 0, 300, True),
-    ("case9241pegase", 128, 0.05, 0, 10, False),  # ~3.5 h on 8 threads
+    ("case9241pegase", 128, 0.05, 0, 10, False),  # ~75 min on 8 threads
+    ("case9241pegase", 128, 0.05, 0, 30, False),  # ~3.8 h on 8 threads
 ]
 
 

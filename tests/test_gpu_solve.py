@@ -163,10 +163,10 @@ def test_case2869_N512_first_iterations_match_reference():
             assert abs(g[key] - c[key]) <= 1e-6 * max(1.0, abs(c[key])), (k, key, g[key], c[key])
 
 
-@pytest.mark.parametrize("its", [3, 10])
+@pytest.mark.parametrize("its", [3, 10, 30])
 def test_case9241_N128_first_iterations_match_reference(its):
     """BASELINE configs[4] (the large-n_u stress config, one GPU): the first
-    3 (and 10) interior-point iterations against the reference's log (the
+    3 (10, 30) interior-point iterations against the reference's log (the
     reference CPU needs ~20 min per iteration on 8 threads here, so the golden
     is capped; tests/golden/make_golden.py --long)."""
     big = json.load(open(os.path.join(GOLDEN, "solves_large.json")))
