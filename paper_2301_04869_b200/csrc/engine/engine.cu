@@ -371,8 +371,8 @@ void Engine::setup_stream() {
     if (defer_tail) {
       ZT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
       ZT.zero(st);
-      // about three waves of 64 x 64 tiles of K_hat over the SMs
-      const long long t = (long long)((n_u + 63) / 64) * ((n_u + 63) / 64);
+      // about three waves of the lower 64 x 64 tiles of K_hat over the SMs
+      const long long tt = (n_u + 63) / 64, t = tt * (tt + 1) / 2;
       tail_splits = int(std::max(1LL, std::min<long long>(M, (3LL * sm_count + t / 2) / t)));
     }
   }
@@ -555,7 +555,7 @@ void Engine::reduce_local(double dw) {
                            sprog.stride[kArrDense], YT.get(), rplan.ldy, rp_yt_ptr.get(),
                            rp_yt_row.get(), n_u, tl, int(M), XT.get(), st);
         } else {
-          GemmTN g{tl, n_u, tl, int(M), 0, 1.0, Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
+          GemmTN g{tl, n_u, tl, int(M), 0, 1.0, 0, Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
                    YT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
                    XT.get(), rplan.ldy, (long long)n_u * rplan.ldy};
           launch_gemm_tn(g, st);
@@ -596,7 +596,7 @@ void Engine::reduce_local(double dw) {
       timed("reduce_post", [&] {
         const int tl = int(pb.LU.tl);
         const long long nn = (long long)n_u * n_u;
-        GemmTN g{n_u, n_u, tl, int(M), tail_splits, -1.0,
+        GemmTN g{n_u, n_u, tl, int(M), tail_splits, -1.0, /*lower=*/1,
                  XT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
                  ZT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
                  red_partial.get() + size_t(sl.nchunks + 1) * nn, n_u, nn};
@@ -713,15 +713,18 @@ void Engine::resolve_timers() {
 void Engine::finish_reduce(double dw) {
   const int n_u = pb.M.n_u;
   const long long nn = (long long)n_u * n_u;
+  // the lower triangles of the slabs, mirrored (the tail GEMM computes the
+  // lower tiles only; the Cholesky and Bunch-Kaufman read the lower triangle)
   if (!multi()) {
     launch_sum_parts(red_partial.get(), red_parts, nn, khat.get(), sigma_u.get(), dw, n_u,
-                     nullptr, st);
+                     nullptr, st, n_u);
     return;
   }
   // local sum -> all-reduce over the scenario groups -> diagonal terms once
-  launch_sum_parts(red_partial.get(), red_parts, nn, khat.get(), nullptr, 0.0, 0, nullptr, st);
+  launch_sum_parts(red_partial.get(), red_parts, nn, khat.get(), nullptr, 0.0, 0, nullptr, st,
+                   n_u);
   comm->allreduce(khat.get(), size_t(nn), RedOpKind::kSum, st);
-  launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st);
+  launch_sum_parts(khat.get(), 1, nn, khat.get(), sigma_u.get(), dw, n_u, nullptr, st, n_u);
 }
 
 bool Engine::factor_khat(double dw, const std::function<void()>& regenerate) {

@@ -823,11 +823,16 @@ __global__ void __launch_bounds__(BLOCK, 1) reduce_tiles_kernel(ReduceLaunch a) 
   }
 }
 
-__global__ void sum_parts_kernel(const double* __restrict__ parts, int nparts, long long len,
+// sym_n > 0: the parts are n x n column-major and only their lower triangles
+// are read (the reduction's tail GEMM writes no upper tiles); the result is
+// mirrored, so K_hat is exactly symmetric
+__global__ void sum_parts_kernel(const double* parts, int nparts, long long len,
                                  double* out, const double* diag_add, double dw, int n_mat,
-                                 const double* sub_vec) {
+                                 const double* sub_vec, int sym_n) {
   const long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (j >= len) return;
+  const long long col = sym_n > 0 ? j / sym_n : 0, row = sym_n > 0 ? j % sym_n : 0;
+  if (sym_n > 0 && row < col) return;
   // fixed order: four interleaved running sums combined pairwise
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   int c = 0;
@@ -842,6 +847,7 @@ __global__ void sum_parts_kernel(const double* __restrict__ parts, int nparts, l
   if (n_mat > 0 && diag_add && (j % (n_mat + 1)) == 0) v += diag_add[j / (n_mat + 1)] + dw;
   if (sub_vec) v -= sub_vec[j];
   out[j] = v;
+  if (sym_n > 0 && row != col) out[row * sym_n + col] = v;
 }
 
 __global__ void affine_mix_kernel(const double* __restrict__ a, const double* __restrict__ b,
@@ -1275,11 +1281,11 @@ void launch_reduce_tiles(const ReduceLaunch& a, cudaStream_t st) {
 
 void launch_sum_parts(const double* parts, int nparts, long long len, double* out,
                       const double* diag_add, double dw, int n_mat, const double* sub_vec,
-                      cudaStream_t st) {
+                      cudaStream_t st, int sym_n) {
   if (len <= 0) return;
   const int B = 256;
   sum_parts_kernel<<<int((len + B - 1) / B), B, 0, st>>>(parts, nparts, len, out, diag_add, dw,
-                                                          n_mat, sub_vec);
+                                                          n_mat, sub_vec, sym_n);
   note_launch();
   check_launch("sum_parts");
 }

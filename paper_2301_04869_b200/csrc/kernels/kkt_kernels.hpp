@@ -53,7 +53,7 @@ void launch_affine_mix(const double* a, const double* b, double t, long long len
                        cudaStream_t st);
 void launch_sum_parts(const double* parts, int nparts, long long len, double* out,
                       const double* diag_add, double dw, int n_mat, const double* sub_vec,
-                      cudaStream_t st);
+                      cudaStream_t st, int sym_n = 0);
 
 struct RhsLaunch {
   DevLu lu;

@@ -184,6 +184,7 @@ __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gm = lane >> 2, gk = lane & 3;
   const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN, z = blockIdx.z;
+  if (g.lower && m0 + kGM - 1 < n0) return;  // tile entirely above the diagonal
   int b0 = z, nb = 1;
   if (g.splits > 0) {
     const int per = (g.batch + g.splits - 1) / g.splits;

@@ -35,9 +35,11 @@ void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* yt,
 // FP64 on the tensor pipe (DMMA m8n8k4).  lda, ldb even; A, B 16-byte aligned.
 // splits > 0: batch sum instead -- C[z] = alpha sum over the z-th of `splits`
 // contiguous batch ranges of A[b]' B[b] (C[z] at C + z sc; fixed order).
+// lower: C tiles entirely above the diagonal (all i < j) are skipped (m == n)
 struct GemmTN {
   int m, n, kd, batch, splits;
   double alpha;
+  int lower;
   const double* A;
   long long lda, sa;
   const double* B;
