@@ -517,16 +517,18 @@ _Pragma("unroll")
 // consumer owning (u, c) is (u K + c) mod 512
 template <int K, int C>
 __device__ __forceinline__ void step_acc(const Hdr& h, unsigned items, unsigned col, unsigned v,
-                                         unsigned xb, double (&acc)[kMaxQ], int tid) {
+                                         unsigned xb, double (&acc)[kMaxQ], int tid, int j0) {
   // the step's controls [u0, u0 + n_items) may span several accumulator
-  // registers q (control u of column c lives in register q = u / (C / K))
+  // registers q (control u of column c lives in register q = u / (C / K)).
+  // Only the lower triangle of K_hat is assembled (finish_reduce mirrors it):
+  // entries u < j0 + c are skipped
   const int u0 = h.aux1, n = h.n_items, c = tid % K;
   const int cx = K == 1 ? 0 : (((c >> 1) << 4));
   const int co = K == 1 ? 0 : ((c & 1) << 3);
   for (int q = u0 / (C / K); q * (C / K) < u0 + n; ++q) {
     const int u = q * (C / K) + tid / K;
     const int it = u - u0;
-    if (it >= 0 && it < n) {
+    if (it >= 0 && it < n && u >= j0 + c) {
       const int4 m = ldsi4(items + 16 * it);
       double a0 = 0.0, a1 = 0.0;
       int t = m.y;
@@ -783,7 +785,7 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
         break;
       }
       case kAcc:
-        step_acc<K, C>(h, items, col, v, xb, acc, tid);
+        step_acc<K, C>(h, items, col, v, xb, acc, tid, j0);
         break;
       case kStoreTail: {
         // Z_T of the tile's columns for the batch-sum GEMM (acc -= X_T' Z_T)
