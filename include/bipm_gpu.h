@@ -327,6 +327,11 @@ int bipm_ctx_info(bipm_ctx* c, int64_t out[12]);
    dense steps, acc steps, spmv steps, accumulator registers, t0, tl} */
 int bipm_problem_stream_check(const bipm_problem* p, int32_t K, int32_t consumers,
                               int32_t ring_bytes, int64_t out[10]);
+/* the same for the round-2 program variants: mode bit 1 presolved forward
+   half (no L sweep), bit 2 adjoint identity (no L' sweep, y_N accumulation),
+   bit 4 deferred tail (Z_T stored for the batch-sum GEMM) */
+int bipm_problem_stream_check_ex(const bipm_problem* p, int32_t K, int32_t consumers,
+                                 int32_t ring_bytes, int32_t mode, int64_t out[10]);
 /* debug: raw copy of the reduction's stamp/trace buffer */
 int bipm_ctx_debug_buffer(bipm_ctx* c, int64_t* out, int64_t cap, int64_t* n_out);
 int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap, int32_t* n_out);

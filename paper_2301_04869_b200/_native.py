@@ -99,6 +99,9 @@ SIGNATURES = {
     "bipm_ctx_phase_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
     "bipm_problem_stream_check": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
                                                  ctypes.c_int32, ctypes.POINTER(ctypes.c_int64)]),
+    "bipm_problem_stream_check_ex": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.c_int32,
+                                                    ctypes.c_int32, ctypes.c_int32,
+                                                    ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_debug_buffer": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
                                              ctypes.POINTER(ctypes.c_int64)]),
     "bipm_ctx_step_stamps": (ctypes.c_int, [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int64),
@@ -344,10 +347,12 @@ class Problem:
         buf = (ct * n.value).from_address(data.value)
         return np.array(buf, copy=True)
 
-    def stream_check(self, K: int, consumers: int = 512, ring_bytes: int = 48 * 1024) -> dict:
-        """Host-only build + validation of the streamed reduction's step program."""
+    def stream_check(self, K: int, consumers: int = 512, ring_bytes: int = 48 * 1024,
+                     mode: int = 0) -> dict:
+        """Host-only build + validation of the streamed reduction's step program
+        (mode: 1 presolved, 2 adjoint identity, 4 deferred tail; include/bipm_gpu.h)."""
         out = (ctypes.c_int64 * 10)()
-        check(lib().bipm_problem_stream_check(self._h, K, consumers, ring_bytes, out))
+        check(lib().bipm_problem_stream_check_ex(self._h, K, consumers, ring_bytes, mode, out))
         keys = ("violations", "steps", "nnz_vs", "sweep_steps", "dense_steps", "acc_steps",
                 "spmv_steps", "nq", "t0", "tl")
         return dict(zip(keys, list(out)))

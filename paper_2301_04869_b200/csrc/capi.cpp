@@ -677,25 +677,35 @@ int bipm_ctx_step_stamps(bipm_ctx* c, int32_t enable, int64_t* out, int32_t cap,
 
 int bipm_problem_stream_check(const bipm_problem* bp, int32_t K, int32_t consumers,
                               int32_t ring_bytes, int64_t out[10]) {
+  return bipm_problem_stream_check_ex(bp, K, consumers, ring_bytes, 0, out);
+}
+
+int bipm_problem_stream_check_ex(const bipm_problem* bp, int32_t K, int32_t consumers,
+                                 int32_t ring_bytes, int32_t mode, int64_t out[10]) {
   return guarded([&] {
     const Problem& P = *bp->p;
     const LuPlan& L = P.LU;
-    const StreamProgram S = build_stream_program(L, P.D.g.u, P.D.kxx.out, P.D.kxu.out,
-                                                 P.M.n_u, K, consumers, ring_bytes,
-                                                 kStreamLookahead);
+    const bool presolved = (mode & 1) != 0, identity = presolved && (mode & 2) != 0;
+    const ReachPlan R = build_reach_plan(L, P.D.g.u, P.M.n_u);
+    const StreamProgram S = build_stream_program(
+        L, P.D.g.u, P.D.kxx.out, P.D.kxu.out, P.M.n_u, K, consumers, ring_bytes,
+        kStreamLookahead, presolved ? &R : nullptr, identity, (mode & 4) != 0);
     int64_t bad = 0;
     // (1) every factor entry a sweep reads appears in VS, once per sweep: each
     // L slot twice (L, L'), each U slot twice (U, U'), less the entries the
-    // dense tail covers (both row and column in the tail)
+    // dense tail covers (both row and column in the tail).  The presolved
+    // program has no L sweep (the reach solve reads L), the adjoint identity
+    // no L' sweep
     std::vector<int> seen(size_t(L.nnz_f), 0);
     for (idx v : S.vs_src) {
       if (v < -1 || v >= L.nnz_f) ++bad;
       if (v >= 0) ++seen[size_t(v)];
     }
+    const int l_sweeps = 2 - (presolved ? 1 : 0) - (identity ? 1 : 0);
     auto row_of_l = [&](idx t) { return idx(std::upper_bound(L.l_ptr.begin(), L.l_ptr.end(), t) - L.l_ptr.begin()) - 1; };
     for (idx t = 0; t < L.nnz_l; ++t) {
       const bool in_tail = row_of_l(t) >= L.t0 && L.l_col[size_t(t)] >= L.t0;
-      if (seen[size_t(t)] != (in_tail ? 0 : 2)) ++bad;
+      if (seen[size_t(t)] != (in_tail ? 0 : l_sweeps)) ++bad;
     }
     for (idx i = 0; i < L.n; ++i) {
       const int want = i >= L.t0 ? 0 : 2;  // U rows of the tail live in W

@@ -101,6 +101,14 @@ def test_stream_program_is_valid(case, K):
         assert st["violations"] == 0, st
         assert st["dense_steps"] == (2 if st["tl"] else 0)
         assert st["t0"] + st["tl"] == p.n_x
+        # round-2 variants: presolved forward half (no L sweep, no first dense
+        # step), + adjoint identity (no L' sweep, no second dense step), +
+        # deferred tail; the factor coverage check adapts to the sweeps left
+        for mode, dense in ((1, 1), (3, 0), (7, 0)):
+            sv = p.stream_check(K, 512, ring, mode)
+            assert sv["violations"] == 0, (mode, sv)
+            assert sv["dense_steps"] == (dense if st["tl"] else 0), (mode, sv)
+            assert sv["steps"] < st["steps"] or not st["tl"], (mode, sv, st)
 
 
 def test_dense_tail_keeps_the_fill(monkeypatch):
