@@ -19,6 +19,7 @@
 #include <stdexcept>
 
 #include "kkt_kernels.hpp"
+#include "reach_gemm.hpp"
 #include "sweeps.cuh"
 
 #include "stats.hpp"
@@ -269,7 +270,8 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
                                                                  const double* __restrict__ scale_in,
                                                                  int* status, double piv_tol,
                                                                  const int* vs_src, int nnz_vs,
-                                                                 double* VS) {
+                                                                 double* VS, int blk0, int blkn,
+                                                                 int gather, int guard) {
   constexpr int kB = kGjB, kLb = kGjLdb;
   extern __shared__ double gj[];
   cg::cluster_group cluster = cg::this_cluster();
@@ -283,8 +285,10 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   };
   const int s = blockIdx.x / ncl;
   double* Fs = F + size_t(s) * P.nnz_f;
-  const int tl = P.tl, tt = tl * tl, t0 = P.t0;
-  const int tp = gj_tp(tl), ldr = gj_ldr(tl), ntp = tp / 8;
+  // the diagonal block [blk0, blk0 + blkn) of the tail is inverted in place
+  // (the whole tail: blk0 = 0, blkn = tl); rows keep the tail's stride tl
+  const int tl = P.tl, tt = tl * tl, t0 = P.t0, n = blkn;
+  const int tp = gj_tp(n), ldr = gj_ldr(n), ntp = tp / 8;
   double* Cb = gj;                          // [tp][kLb]  C' = W[:, P], pivot rows -e_p
   double* Rb = Cb + size_t(tp) * kLb;       // [kB][ldr]  W[P, :]
   double* R2 = Rb + size_t(kB) * ldr;       // [kB][ldr]  A11^{-1} W[P, :], pivot cols A11^{-1}
@@ -294,7 +298,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
   const int gm = lane >> 2, gk = lane & 3;
   constexpr int kWarps = BLOCK / 32;
   constexpr int kJ = kGjMaxTail / 32;  // a row's columns over the lanes
-  {
+  if (gather) {
     // S from the factor: every load of a row in flight at once
     double* W = Wbase;
     for (int i = crank * kWarps + warp; i < tl; i += kWarps * ncl) {
@@ -313,14 +317,15 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     }
   }
   sync_all();
-  for (int k0 = 0, pass = 0; k0 < tl; k0 += kB, ++pass) {
+  double* const Wblk = Wbase + size_t(blk0) * tl + blk0;
+  for (int k0 = 0, pass = 0; k0 < n; k0 += kB, ++pass) {
     // in place: every element's update reads only itself and the staged
     // C' / R2, so slot 0 serves every pass (the working set of the CTAs in
     // flight, 148 x tl^2 doubles, then stays in L2 instead of ping-ponging
     // two slots through HBM)
-    const int bb = min(kB, tl - k0);
-    const double* W = Wbase;
-    double* Wn = Wbase;
+    const int bb = min(kB, n - k0);
+    const double* W = Wblk;
+    double* Wn = Wblk;
     {
       // C' and W[P, :]: all of a thread's loads in flight, then the stores
       constexpr int kQ = (kGjMaxTail * kB + BLOCK - 1) / BLOCK;
@@ -332,7 +337,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
         v[u] = 0.0;
         if (i >= k0 && i < k0 + bb)
           v[u] = p == i - k0 ? -1.0 : 0.0;
-        else if (i < tl && p < bb)
+        else if (i < n && p < bb)
           v[u] = W[size_t(i) * tl + k0 + p];
       }
 #pragma unroll
@@ -344,7 +349,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
       for (int u = 0; u < kQ; ++u) {
         const int q = threadIdx.x + u * BLOCK;
         const int pr = q / tp, j = q % tp;
-        v[u] = (pr < bb && j < tl) ? W[size_t(k0 + pr) * tl + j] : 0.0;
+        v[u] = (pr < bb && j < n) ? W[size_t(k0 + pr) * tl + j] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kQ; ++u) {
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
 #pragma unroll
       for (int k = 0; k < kB; ++k) {
         const double piv = __shfl_sync(0xffffffffu, col[k], k);
-        if (crank == 0 && lane == 0 && k < bb) Fs[P.diag[t0 + k0 + k]] = piv;
+        if (crank == 0 && lane == 0 && k < bb) Fs[P.diag[t0 + blk0 + k0 + k]] = piv;
         const double rp = 1.0 / piv;
         col[k] *= rp;
         inv[k] *= rp;
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     const int nch = (ntp + kSJ - 1) / kSJ, nit = ntp * nch;
     auto clean = [&](int it) {
       const int r0 = (it / nch) * 8, c0s = (it % nch) * 8 * kSJ;
-      return it < nit && r0 + 8 <= tl && c0s + 8 * kSJ <= tl &&
+      return it < nit && r0 + 8 <= n && c0s + 8 * kSJ <= n &&
              (r0 + 8 <= k0 || r0 >= k0 + bb) && (c0s + 8 * kSJ <= k0 || c0s >= k0 + bb);
     };
     auto load_strip = [&](int it, double (&o)[kSJ][2]) {
@@ -428,7 +433,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
         for (int v = 0; v < 2; ++v) {
           const int c = (ch * kSJ + jj) * 8 + 2 * gk + v;
           const bool cp = c >= k0 && c < k0 + bb;
-          o[jj][v] = (it < nit && r < tl && c < tl && !rp && !cp) ? W[size_t(r) * tl + c] : 0.0;
+          o[jj][v] = (it < nit && r < n && c < n && !rp && !cp) ? W[size_t(r) * tl + c] : 0.0;
         }
     };
     const int it0 = crank * kWarps + warp, its = kWarps * ncl;
@@ -459,12 +464,12 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
           wn[8 * jj] = old[jj][0] - d[jj][0];
           wn[8 * jj + 1] = old[jj][1] - d[jj][1];
         }
-      } else if (r < tl) {
+      } else if (r < n) {
 #pragma unroll
         for (int jj = 0; jj < kSJ; ++jj) {
           const int c = (ch * kSJ + jj) * 8 + 2 * gk;
-          if (c < tl) Wn[size_t(r) * tl + c] = old[jj][0] - d[jj][0];
-          if (c + 1 < tl) Wn[size_t(r) * tl + c + 1] = old[jj][1] - d[jj][1];
+          if (c < n) Wn[size_t(r) * tl + c] = old[jj][0] - d[jj][0];
+          if (c + 1 < n) Wn[size_t(r) * tl + c + 1] = old[jj][1] - d[jj][1];
         }
       }
 #pragma unroll
@@ -477,7 +482,7 @@ __global__ void __launch_bounds__(BLOCK) refactor_tail_gj_kernel(DevLu P, double
     }
     sync_all();  // every CTA's strips of Wn written before the next pass reads them
   }
-  if (crank != 0) return;
+  if (crank != 0 || !guard) return;
   // pivot guard (linalg.cpp:69-73): every diagonal of U against max |G_x|;
   // growth guard: every factor entry against growth * max |G_x|
   double bad = 0.0, big = 0.0;
@@ -1202,10 +1207,49 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     attr.val.clusterDim.y = attr.val.clusterDim.z = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, refactor_tail_gj_kernel<512>, P, F, FT, D,
-                       static_cast<const double*>(scale), status, piv_tol, vs_src, nnz_vs, VS);
-    note_launch();
-    check_launch("refactor_tail_gj");
+    auto gj = [&](int blk0, int blkn, int gather, int guard) {
+      cudaLaunchKernelEx(&cfg, refactor_tail_gj_kernel<512>, P, F, FT, D,
+                         static_cast<const double*>(scale), status, piv_tol, vs_src, nnz_vs, VS,
+                         blk0, blkn, gather, guard);
+      note_launch();
+      check_launch("refactor_tail_gj");
+    };
+    // 2 x 2 block inversion (BIPM_GJ_BLOCK=0: one Gauss-Jordan over the whole
+    // tail): S = [A B; C E], Ai = A^{-1} and Zi = (E - C Ai B)^{-1} by the
+    // Gauss-Jordan kernel on the diagonal blocks in place (their pivots are
+    // U_TT's diagonal in order), the rest by six DMMA GEMMs:
+    //   T1 = Ai B, T2 = C Ai, E -= C T1 (= Z), W12 = -T1 Zi, W21 = -Zi T2,
+    //   W11 = Ai - T1 W21;  T1, T2 live in the W' slot until the layouts
+    static const int block_env = [] {
+      const char* e = std::getenv("BIPM_GJ_BLOCK");
+      return e ? std::atoi(e) : 1;
+    }();
+    const int tl = P.tl, h = (tl / 2) & ~15, r = tl - h;
+    // (large M only: with a cluster per scenario the whole-tail Gauss-Jordan
+    // already spreads over the GPU; measured 1354/256 2.66 -> 2.29 ms,
+    // 2869/512 31.1 -> 18.6 ms per refactor, 1354/32 0.86 -> 0.88)
+    if (block_env && h >= 64 && cl == 1) {
+      const long long tt = (long long)tl * tl, sw = 2 * tt;
+      double* Wb = D;                      // W, row-major, stride tl
+      double* T1 = D + tt;                 // h x r
+      double* T2 = D + tt + (long long)h * r;  // r x h
+      auto nn = [&](int m, int n, int k, double alpha, double beta, const double* A, long long lda,
+                    const double* B, long long ldb, double* C, long long ldc) {
+        launch_gemm_nn(GemmNN{m, n, k, M, alpha, beta, A, lda, sw, B, ldb, sw, C, ldc, sw}, st);
+      };
+      gj(0, h, 1, 0);                                                       // A -> Ai
+      nn(h, r, h, 1.0, 0.0, Wb, tl, Wb + h, tl, T1, r);                     // T1 = Ai B
+      nn(r, h, h, 1.0, 0.0, Wb + (long long)h * tl, tl, Wb, tl, T2, h);     // T2 = C Ai
+      nn(r, r, h, -1.0, 1.0, Wb + (long long)h * tl, tl, T1, r,
+         Wb + (long long)h * tl + h, tl);                                   // E -= C T1
+      gj(h, r, 0, 1);                                                       // Z -> Zi (+ guard)
+      nn(h, r, r, -1.0, 0.0, T1, r, Wb + (long long)h * tl + h, tl, Wb + h, tl);  // W12
+      nn(r, h, r, -1.0, 0.0, Wb + (long long)h * tl + h, tl, T2, h,
+         Wb + (long long)h * tl, tl);                                       // W21
+      nn(h, h, r, -1.0, 1.0, T1, r, Wb + (long long)h * tl, tl, Wb, tl);    // W11
+    } else {
+      gj(0, tl, 1, 1);
+    }
     refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
                                                      M);
   }

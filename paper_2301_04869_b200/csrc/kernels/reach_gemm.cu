@@ -260,6 +260,92 @@ __global__ void __launch_bounds__(128) gemm_tn_kernel(GemmTN g) {
   }
 }
 
+// Row-major batched C = alpha A B + beta C (the tail's 2 x 2 block inversion,
+// kkt_kernels.cu): 64 x 64 C tiles, four warps of 32 x 32, k chunks of 16,
+// 8-byte cp.async staging (the tail's rows need not be 16-byte aligned).
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+constexpr int kNnPadB = 4;  // Bs row stride 64 + 4 doubles: conflict-free fragments
+
+__global__ void __launch_bounds__(128) gemm_nn_kernel(GemmNN g) {
+  __shared__ __align__(16) double As[2][kGM][kGPad];
+  __shared__ __align__(16) double Bs[2][kGK][kGN + kNnPadB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gm = lane >> 2, gk = lane & 3;
+  const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN, b = blockIdx.z;
+  const double* A = g.A + size_t(b) * g.sa;
+  const double* B = g.B + size_t(b) * g.sb;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  auto load = [&](int k0, int buf) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + q * 128;  // 1024 elements of each tile
+      {
+        const int row = e >> 4, k = k0 + (e & 15), i = m0 + row;
+        const bool ok = i < g.m && k < g.kd;
+        cp_async8(&As[buf][row][e & 15], ok ? A + size_t(i) * g.lda + k : A, ok ? 8 : 0);
+      }
+      {
+        const int kr = e >> 6, j = n0 + (e & 63), k = k0 + kr;
+        const bool ok = j < g.n && k < g.kd;
+        cp_async8(&Bs[buf][kr][e & 63], ok ? B + size_t(k) * g.ldb + j : B, ok ? 8 : 0);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int nk = (g.kd + kGK - 1) / kGK;
+  if (nk > 0) load(0, 0);
+  for (int c = 0; c < nk; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nk) {
+      load((c + 1) * kGK, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kGK / 4; ++ks) {
+      const int kk = ks * 4 + gk;
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[buf][wm + i * 8 + gm][kk];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[buf][kk][wn + j * 8 + gm];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+    __syncthreads();
+  }
+  double* C = g.C + size_t(b) * g.sc;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = m0 + wm + i * 8 + gm;
+    if (r >= g.m) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int col = n0 + wn + j * 8 + 2 * gk + v;
+        if (col < g.n) {
+          double* cp = C + size_t(r) * g.ldc + col;
+          *cp = g.alpha * acc[i][j][v] + (g.beta != 0.0 ? g.beta * *cp : 0.0);
+        }
+      }
+  }
+}
+
 }  // namespace
 
 template <int G>
@@ -301,6 +387,13 @@ void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* yt,
       WT, ldw, sw, yt, ldy, yt_ptr, yt_row, n_u, tl, xt);
   note_launch();
   check_launch("xt_sparse");
+}
+
+void launch_gemm_nn(const GemmNN& g, cudaStream_t st) {
+  if (g.m <= 0 || g.n <= 0 || g.batch <= 0) return;
+  gemm_nn_kernel<<<dim3((g.m + kGM - 1) / kGM, (g.n + kGN - 1) / kGN, g.batch), 128, 0, st>>>(g);
+  note_launch();
+  check_launch("gemm_nn");
 }
 
 void launch_gemm_tn(const GemmTN& g, cudaStream_t st) {

@@ -49,4 +49,18 @@ struct GemmTN {
 };
 void launch_gemm_tn(const GemmTN& g, cudaStream_t st);
 
+// row-major batched C[b] = alpha A[b] B[b] + beta C[b]: A m x kd (lda), B kd x n
+// (ldb), C m x n (ldc), batch strides sa, sb, sc; any alignment (FP64 DMMA)
+struct GemmNN {
+  int m, n, kd, batch;
+  double alpha, beta;
+  const double* A;
+  long long lda, sa;
+  const double* B;
+  long long ldb, sb;
+  double* C;
+  long long ldc, sc;
+};
+void launch_gemm_nn(const GemmNN& g, cudaStream_t st);
+
 }  // namespace bipm
