@@ -360,12 +360,15 @@ void Engine::setup_stream() {
     // (1354, 4.5 entries per op: 8 lanes 1.31 against 4 lanes 1.36 ms per reduce_pre)
     int grp = per_op <= 3 ? 4 : per_op <= 14 ? 8 : per_op <= 28 ? 16 : 32;
     if (const char* e = std::getenv("BIPM_REACH_GROUP")) grp = std::atoi(e);  // experiments
+    const idx nnz_yt = idx(rplan.yt_row.size());
     rdev = ReachDev{int(n_u), int(L.tl), int(rplan.ldy), int(rplan.nnz_yn), ymax, grp,
                     rp_op_ptr.get(), reinterpret_cast<const int4*>(rp_ops.get()),
-                    reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get()};
+                    reinterpret_cast<const int2*>(rp_ent.get()), rp_yn_ptr.get(),
+                    xt_sparse ? 1 : 0, int(nnz_yt), rp_yt_ptr.get()};
     const size_t Ms = size_t(M);
     YN.resize(Ms * size_t(std::max<idx>(1, rplan.nnz_yn)) + 2);  // + the bulk copies' 16-byte rounding
-    YT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
+    // the sparse product reads y_T packed (its pattern only); the GEMM dense
+    YT.resize(Ms * (xt_sparse ? size_t(std::max<idx>(1, nnz_yt)) : size_t(n_u) * size_t(rplan.ldy)));
     XT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
     XT.zero(st);
     if (defer_tail) {
@@ -552,8 +555,8 @@ void Engine::reduce_local(double dw) {
         if (xt_sparse) {
           // W' = W transposed is Dp's second slot (rows padded to dense_ld)
           launch_xt_sparse(Dp.get() + size_t(tl) * dense_ld(tl), dense_ld(tl),
-                           sprog.stride[kArrDense], YT.get(), rplan.ldy, rp_yt_ptr.get(),
-                           rp_yt_row.get(), n_u, tl, int(M), XT.get(), st);
+                           sprog.stride[kArrDense], YT.get(), rdev.nnz_yt, rp_yt_ptr.get(),
+                           rp_yt_row.get(), n_u, tl, int(M), XT.get(), rplan.ldy, st);
         } else {
           GemmTN g{tl, n_u, tl, int(M), 0, 1.0, 0, Dp.get(), dense_ld(tl), sprog.stride[kArrDense],
                    YT.get(), rplan.ldy, (long long)n_u * rplan.ldy,
@@ -642,6 +645,8 @@ void Engine::reduce_rhs_local(double dw, double* d_out, const double* d_rhat1,
   a.dw = dw;
   a.part = rhs_part.get();
   a.scratch = rhs_scratch.size() ? rhs_scratch.get() : nullptr;
+  // step-stamp debug mode: the last 64 entries of the buffer
+  a.phase = phase.size() > 1000 ? phase.get() + phase.size() - 64 : nullptr;
   timed("reduce_rhs", [&] { launch_reduce_rhs(a, st); });
   launch_sum_parts(rhs_part.get(), M, pb.M.n_u, d_out, nullptr, 0.0, 0, nullptr, st);
   if (multi()) comm->allreduce(d_out, size_t(pb.M.n_u), RedOpKind::kSum, st);
@@ -672,6 +677,7 @@ void Engine::reduce_rhs_fork(double dw, double* d_out) {
   a.dw = dw;
   a.part = rhs_part.get();
   a.scratch = rhs_scratch.size() ? rhs_scratch.get() : nullptr;
+  a.phase = phase.size() > 1000 ? phase.get() + phase.size() - 64 : nullptr;
   cuda_check(cudaEventRecord(ev_fork, st), "fork");
   cuda_check(cudaStreamWaitEvent(st_rhs, ev_fork, 0), "fork");
   timed("reduce_rhs", [&] { launch_reduce_rhs(a, st_rhs); }, st_rhs);

@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 #include <stdexcept>
 
 #include "kkt_kernels.hpp"
@@ -879,9 +880,23 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
   const double* __restrict__ r1 = a.rhat1 + size_t(s) * n_x;
   const double* __restrict__ r3 = a.rhat3 + size_t(s) * n_x;
 
+  // debug: clock64 after each phase, CTA 0 (RhsLaunch::phase)
+  int np = 0;
+  auto mark = [&] {
+    if (a.phase && s == 0 && threadIdx.x == 0) a.phase[np++] = clock64();
+  };
+  mark();
   for (int p = threadIdx.x; p < n_x; p += BLOCK) X[p] = r3[P.perm[p]];
   __syncthreads();
-  solve_LU<BLOCK, 1>(P, F, X);  // X = P a
+  mark();
+  // X = P a
+  level_sweep<BLOCK, 1, false>(P.sL, F.F, X);
+  mark();
+  tail_gather<BLOCK, 1, false>(P.sL, F.F, X);
+  dense_tail_gemm<BLOCK, 1>(P, dense_block(P, F, 0), X);
+  mark();
+  level_sweep<BLOCK, 1, true>(P.sU, F.F + P.nnz_l, X);
+  mark();
   // Z = P (rhat1 - K~ a)
   for (int p = threadIdx.x; p < n_x; p += BLOCK) {
     const int i = P.perm[p];
@@ -892,7 +907,14 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
     Z[p] = v;
   }
   __syncthreads();
-  solve_LUt<BLOCK, 1>(P, F, Z);
+  mark();
+  level_sweep<BLOCK, 1, true>(P.sUt, F.FT, Z);
+  mark();
+  tail_gather<BLOCK, 1, true>(P.sUt, F.FT, Z);
+  dense_tail_gemm<BLOCK, 1>(P, dense_block(P, F, 1), Z);
+  mark();
+  level_sweep<BLOCK, 1, false>(P.sLt, F.FT + (P.nnz_f - P.nnz_l), Z);
+  mark();
   double* out = a.part + size_t(s) * a.n_u;
   for (int u = threadIdx.x; u < a.n_u; u += BLOCK) {
     double v = 0.0;
@@ -901,6 +923,10 @@ __global__ void __launch_bounds__(BLOCK) reduce_rhs_kernel(RhsLaunch a, double* 
     for (int q = a.kxu.t_ptr[u]; q < a.kxu.t_ptr[u + 1]; ++q)
       v += kxu[a.kxu.t_slot[q]] * X[P.iperm[a.kxu.t_row[q]]];
     out[u] = v;
+  }
+  if (a.phase) {
+    __syncthreads();
+    mark();
   }
 }
 
@@ -1098,9 +1124,11 @@ void check_launch(const char* what) {
 
 }  // namespace
 
+// (the level sweeps add their static level-pointer buffers, sweeps.cuh)
+constexpr int kSingleRhsSmemCap = 200 * 1024;
 size_t single_rhs_smem(int n_x) {
   const size_t b = size_t(2) * n_x * sizeof(double);
-  return b <= 200 * 1024 ? b : 0;
+  return b <= size_t(kSingleRhsSmemCap) ? b : 0;
 }
 
 // the cluster-resident Gauss-Jordan (opt-in) when a cluster of <= 16 CTAs
@@ -1220,36 +1248,41 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     // U_TT's diagonal in order), the rest by six DMMA GEMMs:
     //   T1 = Ai B, T2 = C Ai, E -= C T1 (= Z), W12 = -T1 Zi, W21 = -Zi T2,
     //   W11 = Ai - T1 W21;  T1, T2 live in the W' slot until the layouts
-    static const int block_env = [] {
+    static const int block_env = [] {  // recursion depth of the block inversion
       const char* e = std::getenv("BIPM_GJ_BLOCK");
-      return e ? std::atoi(e) : 1;
+      return e ? std::atoi(e) : 2;
     }();
-    const int tl = P.tl, h = (tl / 2) & ~15, r = tl - h;
-    // (large M only: with a cluster per scenario the whole-tail Gauss-Jordan
-    // already spreads over the GPU; measured 1354/256 2.66 -> 2.29 ms,
-    // 2869/512 31.1 -> 18.6 ms per refactor, 1354/32 0.86 -> 0.88)
-    if (block_env && h >= 64 && cl == 1) {
-      const long long tt = (long long)tl * tl, sw = 2 * tt;
-      double* Wb = D;                      // W, row-major, stride tl
-      double* T1 = D + tt;                 // h x r
-      double* T2 = D + tt + (long long)h * r;  // r x h
-      auto nn = [&](int m, int n, int k, double alpha, double beta, const double* A, long long lda,
-                    const double* B, long long ldb, double* C, long long ldc) {
-        launch_gemm_nn(GemmNN{m, n, k, M, alpha, beta, A, lda, sw, B, ldb, sw, C, ldc, sw}, st);
-      };
-      gj(0, h, 1, 0);                                                       // A -> Ai
-      nn(h, r, h, 1.0, 0.0, Wb, tl, Wb + h, tl, T1, r);                     // T1 = Ai B
-      nn(r, h, h, 1.0, 0.0, Wb + (long long)h * tl, tl, Wb, tl, T2, h);     // T2 = C Ai
-      nn(r, r, h, -1.0, 1.0, Wb + (long long)h * tl, tl, T1, r,
-         Wb + (long long)h * tl + h, tl);                                   // E -= C T1
-      gj(h, r, 0, 1);                                                       // Z -> Zi (+ guard)
-      nn(h, r, r, -1.0, 0.0, T1, r, Wb + (long long)h * tl + h, tl, Wb + h, tl);  // W12
-      nn(r, h, r, -1.0, 0.0, Wb + (long long)h * tl + h, tl, T2, h,
-         Wb + (long long)h * tl, tl);                                       // W21
-      nn(h, h, r, -1.0, 1.0, T1, r, Wb + (long long)h * tl, tl, Wb, tl);    // W11
-    } else {
-      gj(0, tl, 1, 1);
-    }
+    const int tl = P.tl;
+    const long long tt = (long long)tl * tl, sw = 2 * tt;
+    auto nn = [&](int m, int n, int k, double alpha, double beta, const double* A, long long lda,
+                  const double* B, long long ldb, double* C, long long ldc) {
+      launch_gemm_nn(GemmNN{m, n, k, M, alpha, beta, A, lda, sw, B, ldb, sw, C, ldc, sw}, st);
+    };
+    // invert the diagonal block [b0, b0 + n) of W in place; temporaries in the
+    // W' slot from `off` on (the outer level's T1, T2 stay live while its
+    // second half recurses)
+    std::function<void(int, int, int, int, int, long long)> inv =
+        [&](int b0, int n, int gather, int guard, int depth, long long off) {
+          const int h = (n / 2) & ~15, r = n - h;
+          if (depth <= 0 || h < 64 || cl != 1) {
+            gj(b0, n, gather, guard);
+            return;
+          }
+          double* Wb = D + (long long)b0 * tl + b0;  // block origin, stride tl
+          double* T1 = D + tt + off;                  // h x r
+          double* T2 = T1 + (long long)h * r;          // r x h
+          double* Cb = Wb + (long long)h * tl;         // C, then W21
+          double* Eb = Cb + h;                         // E, then Z, then Zi
+          inv(b0, h, gather, 0, depth - 1, off);                    // A -> Ai
+          nn(h, r, h, 1.0, 0.0, Wb, tl, Wb + h, tl, T1, r);          // T1 = Ai B
+          nn(r, h, h, 1.0, 0.0, Cb, tl, Wb, tl, T2, h);              // T2 = C Ai
+          nn(r, r, h, -1.0, 1.0, Cb, tl, T1, r, Eb, tl);             // E -= C T1
+          inv(b0 + h, r, 0, guard, depth - 1, off + 2LL * h * r);   // Z -> Zi
+          nn(h, r, r, -1.0, 0.0, T1, r, Eb, tl, Wb + h, tl);         // W12 = -T1 Zi
+          nn(r, h, r, -1.0, 0.0, Eb, tl, T2, h, Cb, tl);             // W21 = -Zi T2
+          nn(h, h, r, -1.0, 1.0, T1, r, Cb, tl, Wb, tl);             // W11 = Ai - T1 W21
+        };
+    inv(0, tl, 1, 1, block_env, 0);
     refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
                                                      M);
   }
@@ -1350,9 +1383,9 @@ void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(reduce_rhs_kernel<kSolveBlock>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSingleRhsSmemCap);
     cudaFuncSetAttribute(reduce_rhs_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
+                         kSingleRhsSmemCap);
     attr_set = true;
   }
   // latency-bound level sweeps: more threads per scenario while the scenarios
@@ -1374,9 +1407,9 @@ void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(recover_state_kernel<kSolveBlock>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, kSingleRhsSmemCap);
     cudaFuncSetAttribute(recover_state_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
+                         kSingleRhsSmemCap);
     attr_set = true;
   }
   // latency-bound level sweeps: more threads per scenario while the scenarios

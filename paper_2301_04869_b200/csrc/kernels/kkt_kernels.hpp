@@ -64,6 +64,7 @@ struct RhsLaunch {
   double dw;
   double* part;  // [M][n_u] per-scenario contributions
   double* scratch;  // [M][2 n_x] when single_rhs_smem(n_x) == 0, else unused
+  long long* phase = nullptr;  // debug: clock64 per phase of scenario 0
 };
 // shared memory of the single-RHS kernels' two n_x vectors, 0 when they do
 // not fit (the caller then provides RhsLaunch/RecoverLaunch::scratch)

@@ -56,9 +56,13 @@ __global__ void __launch_bounds__(32 * kReachWarps)
   int* src = reinterpret_cast<int*>(fv + SEG);
   const double* Fs = F + size_t(s) * nnz_f;
   const double* gs = gu + size_t(s) * gu_nnz;
-  double* ts = yt + (size_t(s) * p.n_u + u) * p.ldy;
-  for (int i = gl; i < p.ldy; i += G) ts[i] = 0.0;
   const int ob = p.op_ptr[u], oe = p.op_ptr[u + 1];
+  const int ny = p.yn_ptr[u + 1] - p.yn_ptr[u];
+  // packed y_T: the column's tail ops follow its ny y_N ops in yt_row order
+  double* ts = p.packed ? yt + size_t(s) * p.nnz_yt + p.yt_ptr[u] - (ob + ny)
+                        : yt + (size_t(s) * p.n_u + u) * p.ldy;
+  if (!p.packed)
+    for (int i = gl; i < p.ldy; i += G) ts[i] = 0.0;
   for (int o = ob; o < oe;) {
     // segment: up to G ops whose entries fit the staging buffer (an op with
     // more entries than that runs alone, straight from global memory)
@@ -99,29 +103,33 @@ __global__ void __launch_bounds__(32 * kReachWarps)
         if (dest >= 0)
           y[dest] = b - a;
         else
-          ts[-1 - dest] = b - a;
+          ts[p.packed ? o + i : -1 - dest] = b - a;
       }
       __syncwarp(gmask);
     }
     o += nseg;
   }
   double* ys = yn + size_t(s) * p.nnz_yn + p.yn_ptr[u];
-  const int ny = p.yn_ptr[u + 1] - p.yn_ptr[u];
   for (int i = gl; i < ny; i += G) ys[i] = y[i];
 }
 
-// X_T = W y_T with y_T sparse (column u nonzero on yt_row[yt_ptr[u] ..]):
+// X_T = W y_T with y_T sparse (column u nonzero on yt_row[yt_ptr[u] ..], its
+// values packed in the same order, [M][nnz_yt]):
 // X_T[:, u] = sum_k y_T[t_k, u] W[:, t_k] = sum_k y_T[t_k, u] W'[t_k, :].
 // CTA = (scenario, 32 output rows i): W'[:, i-block] (tl x 32) is staged in
 // shared memory once, then each warp forms whole columns u, lane = row i,
 // broadcasting the column's (t_k, y) pairs: 27 of 307 rows per column at 1354
-// instead of the dense product's 307.
+// instead of the dense product's 307.  The pairs are read coalesced (packed
+// y_T) and the next column's first 32 are in flight while the current one is
+// summed, so a warp's columns do not each wait a full memory latency.
 constexpr int kXtRows = 32, kXtWarps = 16;
 __global__ void __launch_bounds__(32 * kXtWarps)
     xt_sparse_kernel(const double* __restrict__ WT, int ldw, long long sw,
-                     const double* __restrict__ yt, int ldy, const int* __restrict__ yt_ptr,
-                     const int* __restrict__ yt_row, int n_u, int tl, double* __restrict__ xt) {
-  extern __shared__ double wts[];  // [tl][kXtRows]
+                     const double* __restrict__ ytc, int nnz_yt, const int* __restrict__ yt_ptr,
+                     const int* __restrict__ yt_row, int n_u, int tl, double* __restrict__ xt,
+                     int ldy) {
+  extern __shared__ double wts[];  // [tl][kXtRows], then yt_ptr
+  int* ptr = reinterpret_cast<int*>(wts + size_t(tl) * kXtRows);
   const int s = blockIdx.y, i0 = blockIdx.x * kXtRows;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* W = WT + size_t(s) * sw;
@@ -129,19 +137,37 @@ __global__ void __launch_bounds__(32 * kXtWarps)
     const int t = q / kXtRows, i = i0 + q % kXtRows;
     wts[q] = i < tl ? W[size_t(t) * ldw + i] : 0.0;
   }
+  for (int q = tid; q <= n_u; q += 32 * kXtWarps) ptr[q] = yt_ptr[q];
   __syncthreads();
-  const double* ys = yt + size_t(s) * n_u * ldy;
+  const double* ys = ytc + size_t(s) * nnz_yt;
   double* xs = xt + size_t(s) * n_u * ldy;
   const int i = i0 + lane;
+  auto fetch = [&](int u, int& tv, double& yv) {
+    tv = 0;
+    yv = 0.0;
+    if (u < n_u) {
+      const int k = ptr[u] + lane;
+      if (k < ptr[u + 1]) {
+        tv = yt_row[k];
+        yv = ys[k];
+      }
+    }
+  };
+  int tn;
+  double yn;
+  fetch(warp, tn, yn);
   for (int u = warp; u < n_u; u += kXtWarps) {
-    const int kb = yt_ptr[u], ke = yt_ptr[u + 1];
-    const double* yc = ys + size_t(u) * ldy;
+    int tv = tn;
+    double yv = yn;
+    fetch(u + kXtWarps, tn, yn);  // next column's first chunk, in flight
+    const int kb = ptr[u], ke = ptr[u + 1];
     double a0 = 0.0, a1 = 0.0;
-    // 32 (t, y) pairs loaded at once by the lanes, then broadcast
     for (int k0 = kb; k0 < ke; k0 += 32) {
+      if (k0 > kb) {  // columns longer than 32 entries: later chunks inline
+        tv = k0 + lane < ke ? yt_row[k0 + lane] : 0;
+        yv = k0 + lane < ke ? ys[k0 + lane] : 0.0;
+      }
       const int n = min(32, ke - k0);
-      const int tv = lane < n ? yt_row[k0 + lane] : 0;
-      const double yv = lane < n ? yc[tv] : 0.0;
       int k = 0;
       for (; k + 1 < n; k += 2) {
         const int t0 = __shfl_sync(0xffffffffu, tv, k), t1 = __shfl_sync(0xffffffffu, tv, k + 1);
@@ -376,15 +402,15 @@ void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz
   check_launch("reach_solve");
 }
 
-void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* yt, int ldy,
+void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* ytc, int nnz_yt,
                       const int* yt_ptr, const int* yt_row, int n_u, int tl, int M, double* xt,
-                      cudaStream_t st) {
+                      int ldy, cudaStream_t st) {
   if (M <= 0 || n_u <= 0 || tl <= 0) return;
-  const size_t smem = size_t(tl) * kXtRows * sizeof(double);
+  const size_t smem = size_t(tl) * kXtRows * sizeof(double) + size_t(n_u + 1) * sizeof(int);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(xt_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   xt_sparse_kernel<<<dim3((tl + kXtRows - 1) / kXtRows, M), 32 * kXtWarps, smem, st>>>(
-      WT, ldw, sw, yt, ldy, yt_ptr, yt_row, n_u, tl, xt);
+      WT, ldw, sw, ytc, nnz_yt, yt_ptr, yt_row, n_u, tl, xt, ldy);
   note_launch();
   check_launch("xt_sparse");
 }

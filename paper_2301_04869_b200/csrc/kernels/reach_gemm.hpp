@@ -15,20 +15,24 @@ struct ReachDev {
   const int4* ops;    // {dest, G_u slot or -1, entry begin, entry end}
   const int2* ent;    // {source y_N entry (column-local), L factor slot}
   const int* yn_ptr;  // [n_u + 1]
+  // packed: y_T holds only y_T's pattern (yt_ptr / yt_row order), [M][nnz_yt]
+  int packed, nnz_yt;
+  const int* yt_ptr;  // [n_u + 1]
 };
 
-// y_N [M][nnz_yn] and y_T [M][n_u][ldy] (rows >= tl zero) from the factors
+// y_N [M][nnz_yn] and y_T -- [M][n_u][ldy] (rows >= tl zero), or packed
+// [M][nnz_yt] -- from the factors
 // F [M][nnz_f] and the G_u values [M][gu_nnz]
 void launch_reach_solve(const ReachDev& p, int M, const double* F, long long nnz_f,
                         const double* gu, long long gu_nnz, double* yn, double* yt,
                         cudaStream_t st);
 
 // X_T = W y_T for every scenario with y_T's column pattern (yt_ptr, yt_row,
-// tail-local rows): WT = W' = W transposed, rows of ldw doubles, scenario
-// stride sw; yt, xt [M][n_u][ldy]
-void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* yt, int ldy,
+// tail-local rows) and packed values ytc [M][nnz_yt]: WT = W' = W transposed,
+// rows of ldw doubles, scenario stride sw; xt [M][n_u][ldy]
+void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* ytc, int nnz_yt,
                       const int* yt_ptr, const int* yt_row, int n_u, int tl, int M, double* xt,
-                      cudaStream_t st);
+                      int ldy, cudaStream_t st);
 
 // C[b](i, j) = alpha sum_k A[b][i lda + k] B[b][j ldb + k]  (both operands
 // k-contiguous, C column-major: C[b][j ldc + i]), i < m, j < n, k < kd;

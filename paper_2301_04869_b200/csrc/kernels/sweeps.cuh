@@ -34,11 +34,12 @@ template <int BLOCK, typename Range, typename Term, typename Finish>
 __device__ __forceinline__ void group_dot(int items, Range range, Term term, Finish finish) {
   constexpr int kWarps = BLOCK / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int g = 1;
-  while (g < 32 && items * (g * 2) <= BLOCK) g *= 2;
-  const int per_warp = 32 / g;
+  int lg = 0;  // g = 2^lg lanes per item (shifts: g is not a compile-time constant)
+  while (lg < 5 && items * (2 << lg) <= BLOCK) ++lg;
+  const int g = 1 << lg;
+  const int per_warp = 32 >> lg;
   const int sub = lane & (g - 1);
-  const int gid = lane / g;
+  const int gid = lane >> lg;
   for (int base = warp * per_warp; base < items; base += kWarps * per_warp) {
     const int item = base + gid;
     double acc = 0.0;
@@ -64,11 +65,12 @@ __device__ __forceinline__ void level_items(const int4* __restrict__ items, int 
   constexpr int kWarps = BLOCK / 32;
   const int n = nrows * K;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int g = 1;
-  while (g < 32 && n * (g * 2) <= BLOCK) g *= 2;
-  const int per_warp = 32 / g;
+  int lg = 0;
+  while (lg < 5 && n * (2 << lg) <= BLOCK) ++lg;
+  const int g = 1 << lg;
+  const int per_warp = 32 >> lg;
   const int sub = lane & (g - 1);
-  const int gid = lane / g;
+  const int gid = lane >> lg;
   for (int base = warp * per_warp; base < n; base += kWarps * per_warp) {
     const int item = base + gid;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
@@ -101,8 +103,165 @@ __device__ __forceinline__ void level_items(const int4* __restrict__ items, int 
   }
 }
 
+// Single right-hand side (one CTA per scenario: no other CTA hides the
+// per-level memory round trips, items -> col / V -> X).  Everything but the
+// X gathers is independent of the previous levels, so it is software
+// pipelined: the item records of level l + 2 and the first two entries
+// (columns, values, diagonal) of level l + 1 are loaded while level l runs.
+// Same summation order as level_items (bitwise identical results).
+#ifndef BIPM_SWEEP1_PF
+#define BIPM_SWEEP1_PF 2  // prefetched entries per item (0: plain level_items sweeps)
+#endif
+template <int BLOCK, bool kDiag>
+__device__ void level_sweep1(const DevSweep& S, const double* __restrict__ V, double* X) {
+  constexpr int kWarps = BLOCK / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4* __restrict__ items = reinterpret_cast<const int4*>(S.items);
+  const int* __restrict__ col = S.col;
+  const int nl = S.n_lvl;
+  struct Geo {
+    int i0, n, lg;  // g = 2^lg lanes per item
+  };
+  // the level pointers in shared memory: the item records two levels ahead
+  // are then one memory round trip away, not two
+  constexpr int kLvlCap = 1024;
+  __shared__ int s_lvl[kLvlCap + 1];
+  const bool lvl_smem = nl <= kLvlCap;
+  if (lvl_smem) {
+    for (int i = threadIdx.x; i <= nl; i += BLOCK) s_lvl[i] = S.lvl_ptr[i];
+    __syncthreads();
+  }
+  auto geo = [&](int lv) {
+    Geo q{0, 0, 0};
+    if (lv < nl) {
+      q.i0 = lvl_smem ? s_lvl[lv] : __ldg(S.lvl_ptr + lv);
+      q.n = (lvl_smem ? s_lvl[lv + 1] : __ldg(S.lvl_ptr + lv + 1)) - q.i0;
+      while (q.lg < 5 && q.n * (2 << q.lg) <= BLOCK) ++q.lg;
+    }
+    return q;
+  };
+  // this thread's first item of a level (the first pass over its items)
+  auto first_item = [&](const Geo& q) { return ((warp << 5) + lane) >> q.lg; };
+  auto load_meta = [&](const Geo& q) {
+    const int item = first_item(q);
+    return item < q.n ? items[q.i0 + item] : make_int4(0, 0, 0, 0);
+  };
+  constexpr int kPf = BIPM_SWEEP1_PF > 0 ? BIPM_SWEEP1_PF : 1;
+  struct Ent {
+    int c[kPf];
+    double v[kPf], d;
+  };
+  auto load_ent = [&](const Geo& q, const int4& m) {
+    Ent e;
+    const int g = 1 << q.lg;
+    const int t = m.y + (kDiag ? 1 : 0) + (lane & (g - 1));
+#pragma unroll
+    for (int k = 0; k < kPf; ++k) {
+      const bool ok = t + k * g < m.z;
+      e.c[k] = ok ? col[t + k * g] : 0;
+      e.v[k] = ok ? V[t + k * g] : 0.0;
+    }
+    e.d = kDiag && m.z > m.y ? V[m.y] : 1.0;
+    return e;
+  };
+  Geo g_cur = geo(0), g_nxt = geo(1);
+  int4 m_cur = load_meta(g_cur), m_nxt = load_meta(g_nxt);
+  Ent e_cur = load_ent(g_cur, m_cur);
+  for (int lv = 0; lv < nl; ++lv) {
+    const Geo g_nn = geo(lv + 2);
+    const int4 m_nn = load_meta(g_nn);    // two levels ahead
+    const Ent e_nxt = load_ent(g_nxt, m_nxt);  // one level ahead
+    {
+      const Geo& q = g_cur;
+      const int g = 1 << q.lg, per_warp = 32 >> q.lg, sub = lane & (g - 1);
+      // first pass: the prefetched item
+      {
+        const int item = first_item(q);
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        if (item < q.n) {
+          const int4 m = m_cur;
+          int t = m.y + (kDiag ? 1 : 0) + sub;
+          auto ev = [&](int k) { return k < kPf ? e_cur.v[k] : V[t + k * g]; };
+          auto ec = [&](int k) { return k < kPf ? e_cur.c[k] : col[t + k * g]; };
+          if (t + 3 * g < m.z) {
+            a0 += ev(0) * X[ec(0)];
+            a1 += ev(1) * X[ec(1)];
+            a2 += ev(2) * X[ec(2)];
+            a3 += ev(3) * X[ec(3)];
+            t += 4 * g;
+            for (; t + 3 * g < m.z; t += 4 * g) {
+              const int c0 = col[t], c1 = col[t + g], c2 = col[t + 2 * g], c3 = col[t + 3 * g];
+              const double v0 = V[t], v1 = V[t + g], v2 = V[t + 2 * g], v3 = V[t + 3 * g];
+              a0 += v0 * X[c0];
+              a1 += v1 * X[c1];
+              a2 += v2 * X[c2];
+              a3 += v3 * X[c3];
+            }
+            for (; t < m.z; t += g) a0 += V[t] * X[col[t]];
+          } else {
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              if (t + k * g < m.z) a0 += ev(k) * X[ec(k)];
+          }
+        }
+        double acc = (a0 + a1) + (a2 + a3);
+        for (int off = g >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (item < q.n && sub == 0) {
+          double* x = X + m_cur.x;
+          if (kDiag)
+            *x = (*x - acc) / e_cur.d;
+          else
+            *x -= acc;
+        }
+      }
+      // further passes (levels with more items than threads): as level_items
+      if (q.n > kWarps * per_warp) {
+        const int4* it = items + q.i0;
+        const int gid = lane >> q.lg;
+        for (int base = (warp + kWarps) * per_warp; base < q.n; base += kWarps * per_warp) {
+          const int item = base + gid;
+          double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+          int4 m = make_int4(0, 0, 0, 0);
+          if (item < q.n) {
+            m = it[item];
+            int t = m.y + (kDiag ? 1 : 0) + sub;
+            for (; t + 3 * g < m.z; t += 4 * g) {
+              const int c0 = col[t], c1 = col[t + g], c2 = col[t + 2 * g], c3 = col[t + 3 * g];
+              const double v0 = V[t], v1 = V[t + g], v2 = V[t + 2 * g], v3 = V[t + 3 * g];
+              a0 += v0 * X[c0];
+              a1 += v1 * X[c1];
+              a2 += v2 * X[c2];
+              a3 += v3 * X[c3];
+            }
+            for (; t < m.z; t += g) a0 += V[t] * X[col[t]];
+          }
+          double acc = (a0 + a1) + (a2 + a3);
+          for (int off = g >> 1; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+          if (item < q.n && sub == 0) {
+            double* x = X + m.x;
+            if (kDiag)
+              *x = (*x - acc) / V[m.y];
+            else
+              *x -= acc;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    g_cur = g_nxt;
+    m_cur = m_nxt;
+    e_cur = e_nxt;
+    g_nxt = g_nn;
+    m_nxt = m_nn;
+  }
+}
+
 template <int BLOCK, int K, bool kDiag>
 __device__ void level_sweep(const DevSweep& S, const double* __restrict__ V, double* X) {
+  if constexpr (K == 1 && BIPM_SWEEP1_PF > 0) {
+    level_sweep1<BLOCK, kDiag>(S, V, X);
+    return;
+  }
   const int4* items = reinterpret_cast<const int4*>(S.items);
   for (int lv = 0; lv < S.n_lvl; ++lv) {
     const int i0 = S.lvl_ptr[lv];

@@ -51,6 +51,9 @@ CONFIGS = [
     {"BIPM_PRE_TAIL": "0"},
     {"BIPM_STREAM_CHUNK": "1"},
     {"BIPM_GJ_CLUSTER_RESIDENT": "1"},
+    {"BIPM_GJ_BLOCK": "0"},
+    {"BIPM_GJ_BLOCK": "1"},
+    {"BIPM_GJ_BLOCK": "3"},
 ]
 
 
