@@ -13,6 +13,7 @@
 // or, when y_T is sparse enough, by xt_sparse_kernel -- so W is read once per
 // scenario instead of once per column tile of the reduction.  gemm_tn_kernel
 // also forms the batch-sum tail product -sum_s X_T' Z_T after the tiles.
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -116,71 +117,112 @@ __global__ void __launch_bounds__(32 * kReachWarps)
 // X_T = W y_T with y_T sparse (column u nonzero on yt_row[yt_ptr[u] ..], its
 // values packed in the same order, [M][nnz_yt]):
 // X_T[:, u] = sum_k y_T[t_k, u] W[:, t_k] = sum_k y_T[t_k, u] W'[t_k, :].
-// CTA = (scenario, 32 output rows i): W'[:, i-block] (tl x 32) is staged in
-// shared memory once, then each warp forms whole columns u, lane = row i,
-// broadcasting the column's (t_k, y) pairs: 27 of 307 rows per column at 1354
-// instead of the dense product's 307.  The pairs are read coalesced (packed
-// y_T) and the next column's first 32 are in flight while the current one is
-// summed, so a warp's columns do not each wait a full memory latency.
+// CTA = (scenario, 32 RPL output rows): W'[:, i-block] (tl x 32 RPL) is staged
+// in shared memory once, then each warp forms whole columns u, lane = RPL
+// consecutive rows i.  A column's (t_k, y) pairs are read coalesced (packed
+// y_T; the next chunk's loads in flight while the current one is summed) and
+// written as 16-byte records to the warp's slot in shared memory, so each
+// entry costs one broadcast record load plus one W' load of RPL doubles per
+// lane (shuffling t and y to the lanes cost three SHFLs per entry and
+// bound the kernel on the MIO queue).  RPL = 2 halves the record loads per
+// FMA where the 64-row W' block fits in shared memory.
 constexpr int kXtRows = 32, kXtWarps = 16;
+template <int RPL>
 __global__ void __launch_bounds__(32 * kXtWarps)
     xt_sparse_kernel(const double* __restrict__ WT, int ldw, long long sw,
                      const double* __restrict__ ytc, int nnz_yt, const int* __restrict__ yt_ptr,
                      const int* __restrict__ yt_row, int n_u, int tl, double* __restrict__ xt,
                      int ldy) {
-  extern __shared__ double wts[];  // [tl][kXtRows], then yt_ptr
-  int* ptr = reinterpret_cast<int*>(wts + size_t(tl) * kXtRows);
-  const int s = blockIdx.y, i0 = blockIdx.x * kXtRows;
+  constexpr int R = kXtRows * RPL;  // rows per CTA
+  extern __shared__ __align__(16) double wts[];  // [tl][R], records, then yt_ptr
+  double2* rec_all = reinterpret_cast<double2*>(wts + size_t(tl) * R);
+  int* ptr = reinterpret_cast<int*>(rec_all + 32 * kXtWarps);
+  const int s = blockIdx.y, i0 = blockIdx.x * R;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* W = WT + size_t(s) * sw;
-  for (int q = tid; q < tl * kXtRows; q += 32 * kXtWarps) {
-    const int t = q / kXtRows, i = i0 + q % kXtRows;
+  for (int q = tid; q < tl * R; q += 32 * kXtWarps) {
+    const int t = q / R, i = i0 + q % R;
     wts[q] = i < tl ? W[size_t(t) * ldw + i] : 0.0;
   }
   for (int q = tid; q <= n_u; q += 32 * kXtWarps) ptr[q] = yt_ptr[q];
   __syncthreads();
+  double2* rec = rec_all + 32 * warp;
+  const unsigned rec_b = static_cast<unsigned>(__cvta_generic_to_shared(rec));
+  const unsigned w_b = static_cast<unsigned>(__cvta_generic_to_shared(wts)) + 8 * RPL * lane;
   const double* ys = ytc + size_t(s) * nnz_yt;
   double* xs = xt + size_t(s) * n_u * ldy;
-  const int i = i0 + lane;
-  auto fetch = [&](int u, int& tv, double& yv) {
-    tv = 0;
-    yv = 0.0;
-    if (u < n_u) {
-      const int k = ptr[u] + lane;
-      if (k < ptr[u + 1]) {
-        tv = yt_row[k];
-        yv = ys[k];
-      }
-    }
+  // chunk of up to 32 entries starting at k0 of column u (rows pre-scaled to
+  // byte offsets of W' rows)
+  auto fetch = [&](int k0, int ke, int& tv, double& yv) {
+    const int k = k0 + lane;
+    tv = k < ke ? yt_row[k] * (R * 8) : 0;
+    yv = k < ke ? ys[k] : 0.0;
   };
+  int u = warp;
+  if (u >= n_u) return;
   int tn;
   double yn;
-  fetch(warp, tn, yn);
-  for (int u = warp; u < n_u; u += kXtWarps) {
-    int tv = tn;
-    double yv = yn;
-    fetch(u + kXtWarps, tn, yn);  // next column's first chunk, in flight
+  fetch(ptr[u], ptr[u + 1], tn, yn);
+  for (; u < n_u; u += kXtWarps) {
     const int kb = ptr[u], ke = ptr[u + 1];
-    double a0 = 0.0, a1 = 0.0;
+    double a0[RPL], a1[RPL];
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) a0[r] = a1[r] = 0.0;
     for (int k0 = kb; k0 < ke; k0 += 32) {
-      if (k0 > kb) {  // columns longer than 32 entries: later chunks inline
-        tv = k0 + lane < ke ? yt_row[k0 + lane] : 0;
-        yv = k0 + lane < ke ? ys[k0 + lane] : 0.0;
+      __syncwarp();
+      rec[lane] = make_double2(yn, __hiloint2double(0, tn));
+      __syncwarp();
+      // the following chunk (this column's or the next column's first) in flight
+      if (k0 + 32 < ke) {
+        fetch(k0 + 32, ke, tn, yn);
+      } else if (u + kXtWarps < n_u) {
+        fetch(ptr[u + kXtWarps], ptr[u + kXtWarps + 1], tn, yn);
       }
       const int n = min(32, ke - k0);
       int k = 0;
-      for (; k + 1 < n; k += 2) {
-        const int t0 = __shfl_sync(0xffffffffu, tv, k), t1 = __shfl_sync(0xffffffffu, tv, k + 1);
-        const double y0 = __shfl_sync(0xffffffffu, yv, k), y1 = __shfl_sync(0xffffffffu, yv, k + 1);
-        a0 += y0 * wts[t0 * kXtRows + lane];
-        a1 += y1 * wts[t1 * kXtRows + lane];
+      for (; k + 3 < n; k += 4) {
+        double2 e[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                       : "=d"(e[q].x), "=d"(e[q].y)
+                       : "r"(rec_b + 16 * (k + q)));
+        double w[4][RPL];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const unsigned a = w_b + unsigned(__double2loint(e[q].y));
+          if constexpr (RPL == 2)
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[q][0]), "=d"(w[q][1]) : "r"(a));
+          else
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(w[q][0]) : "r"(a));
+        }
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          a0[r] += e[0].x * w[0][r];
+          a1[r] += e[1].x * w[1][r];
+          a0[r] += e[2].x * w[2][r];
+          a1[r] += e[3].x * w[3][r];
+        }
       }
-      if (k < n) {
-        const int t0 = __shfl_sync(0xffffffffu, tv, k);
-        a0 += __shfl_sync(0xffffffffu, yv, k) * wts[t0 * kXtRows + lane];
+      for (; k < n; ++k) {
+        double2 e;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(e.x), "=d"(e.y) : "r"(rec_b + 16 * k));
+        const unsigned a = w_b + unsigned(__double2loint(e.y));
+#pragma unroll
+        for (int r = 0; r < RPL; ++r) {
+          double w;
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(w) : "r"(a + 8 * r));
+          a0[r] += e.x * w;
+        }
       }
     }
-    if (i < tl) xs[size_t(u) * ldy + i] = a0 + a1;
+    if (kb == ke && u + kXtWarps < n_u)  // empty column: its successor's chunk
+      fetch(ptr[u + kXtWarps], ptr[u + kXtWarps + 1], tn, yn);
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = i0 + RPL * lane + r;
+      if (i < tl) xs[size_t(u) * ldy + i] = a0[r] + a1[r];
+    }
   }
 }
 
@@ -406,11 +448,26 @@ void launch_xt_sparse(const double* WT, int ldw, long long sw, const double* ytc
                       const int* yt_ptr, const int* yt_row, int n_u, int tl, int M, double* xt,
                       int ldy, cudaStream_t st) {
   if (M <= 0 || n_u <= 0 || tl <= 0) return;
-  const size_t smem = size_t(tl) * kXtRows * sizeof(double) + size_t(n_u + 1) * sizeof(int);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(xt_sparse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  xt_sparse_kernel<<<dim3((tl + kXtRows - 1) / kXtRows, M), 32 * kXtWarps, smem, st>>>(
-      WT, ldw, sw, ytc, nnz_yt, yt_ptr, yt_row, n_u, tl, xt, ldy);
+  auto smem_of = [&](int rpl) {
+    return size_t(tl) * kXtRows * rpl * sizeof(double) + 32 * kXtWarps * sizeof(double2) +
+           size_t(n_u + 1) * sizeof(int);
+  };
+  // two rows per lane where the 64-row W' block fits (1354/256, tl 272:
+  // reduce_pre 1.01 -> 0.95 ms against one row per lane; BIPM_XT_RPL=1|2)
+  int rpl = 2;
+  if (const char* e = std::getenv("BIPM_XT_RPL")) rpl = std::atoi(e) == 2 ? 2 : 1;
+  if (smem_of(rpl) > 227 * 1024) rpl = 1;
+  const size_t smem = smem_of(rpl);
+  const int R = kXtRows * rpl;
+  if (rpl == 2) {
+    cudaFuncSetAttribute(xt_sparse_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    xt_sparse_kernel<2><<<dim3((tl + R - 1) / R, M), 32 * kXtWarps, smem, st>>>(
+        WT, ldw, sw, ytc, nnz_yt, yt_ptr, yt_row, n_u, tl, xt, ldy);
+  } else {
+    cudaFuncSetAttribute(xt_sparse_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    xt_sparse_kernel<1><<<dim3((tl + R - 1) / R, M), 32 * kXtWarps, smem, st>>>(
+        WT, ldw, sw, ytc, nnz_yt, yt_ptr, yt_row, n_u, tl, xt, ldy);
+  }
   note_launch();
   check_launch("xt_sparse");
 }

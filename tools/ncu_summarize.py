@@ -46,8 +46,9 @@ def launches(path, out):
 
 
 def report(path, out, workload=None, group=None):
-    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    # base units: every row in ns / bytes (auto units change per row)
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--print-units", "base"],
+                         capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr = rows[0]
     res = {"source": os.path.basename(path), "launches": []}
@@ -64,12 +65,11 @@ def report(path, out, workload=None, group=None):
                   not k.endswith("not_issued") and f(k)}
         st = sum(stalls.values()) or 1.0
         rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
-        unit_r = hdr and rows[1][hdr.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in hdr else ""
-        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit_r, 1)
+        mult = 1
         launch = {
             "kernel": short(d.get("Kernel Name", "")), "grid": d.get("Grid Size"),
             "block": d.get("Block Size"),
-            "duration_ms": f("gpu__time_duration.sum") / 1e6 if rows[1][hdr.index("gpu__time_duration.sum")] == "nsecond" else f("gpu__time_duration.sum"),
+            "duration_ms": f("gpu__time_duration.sum") / 1e6,
             "dram_bytes": (rd + wr) * mult if rd is not None and wr is not None else None,
             "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
             "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),

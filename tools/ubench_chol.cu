@@ -5,6 +5,8 @@
 //   -o tools/ubench_chol_bin tools/ubench_chol.cu
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
+#include <algorithm>
 #include <vector>
 
 #include "kernels/dense_chol.cu"
@@ -63,6 +65,20 @@ int main(int argc, char** argv) {
       for (int k = 0; k < 7; ++k) printf(" %s %lld", nm[k], tot[k] / (np ? np : 1));
       printf("\n");
     }
+  }
+  {
+    // residual of L L' against A (lower triangle; the shift is <= 1e-13 |A|)
+    std::vector<double> L(A.size());
+    cudaMemcpy(L.data(), dK, A.size() * 8, cudaMemcpyDeviceToHost);
+    double err = 0.0, amax = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int i = j; i < n; ++i) {
+        double s = 0.0;
+        for (int k = 0; k <= j; ++k) s += L[size_t(k) * n + i] * L[size_t(k) * n + j];
+        err = std::max(err, std::fabs(s - A[size_t(j) * n + i]));
+        amax = std::max(amax, std::fabs(A[size_t(j) * n + i]));
+      }
+    printf("residual max|LL'-A|/max|A| = %.3e\n", err / amax);
   }
   printf("status %s\n", cudaGetErrorString(cudaDeviceSynchronize()));
 }
