@@ -377,6 +377,8 @@ void Engine::setup_stream() {
       // about three waves of the lower 64 x 64 tiles of K_hat over the SMs
       const long long tt = (n_u + 63) / 64, t = tt * (tt + 1) / 2;
       tail_splits = int(std::max(1LL, std::min<long long>(M, (3LL * sm_count + t / 2) / t)));
+      if (const char* e = std::getenv("BIPM_TAIL_SPLITS"))
+        tail_splits = std::max(1, std::min(int(M), std::atoi(e)));
     }
   }
   sp_pat.upload(sprog.pat);
@@ -391,7 +393,22 @@ void Engine::setup_stream() {
     }
     sp_issue.upload(iss);
   }
-  sp_ring.upload(sprog.ring_off);
+  {
+    // ring words: offset | accumulation-step skip control (reduce_stream.cu kRw*)
+    // (BIPM_ACC_SKIP=0: no step skipped, for A/B runs)
+    const char* ev = std::getenv("BIPM_ACC_SKIP");
+    const bool acc_skip = !ev || std::atoi(ev) != 0;
+    std::vector<int> rw(sprog.ring_off.size());
+    for (size_t j = 0; j < rw.size(); ++j) {
+      const unsigned off = unsigned(sprog.ring_off[j]);
+      if (off > 0x3ffffu) throw Error(kInvalidArgument, "stream program: ring offset exceeds 18 bits");
+      const int sk = sprog.skip[j];
+      const unsigned hi = acc_skip ? unsigned(std::min(sk >> 4, 4095)) : 4095u;
+      const unsigned fl = ((sk & kFlagBarrier) ? 1u << 18 : 0u) | ((sk & kFlagPre) ? 1u << 19 : 0u);
+      rw[j] = int(off | fl | (hi << 20));
+    }
+    sp_ring.upload(rw);
+  }
   sp_vs_src.upload(sprog.vs_src);
   sp_kxu_slot.upload(sprog.kxu_t_slot.empty() ? std::vector<idx>{0} : sprog.kxu_t_slot);
   sp_gu_slot.upload(sprog.gu_t_slot.empty() ? std::vector<idx>{0} : sprog.gu_t_slot);

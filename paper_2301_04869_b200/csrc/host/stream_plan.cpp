@@ -111,6 +111,9 @@ struct Builder {
     is.x_off = p.x_off;
     is.x_count = p.x_count;
     S.issue.push_back(is);
+    S.skip.push_back(p.kind == kStepAcc && n_items > 0
+                         ? ((p.aux1 + n_items - 1) << 4) | (p.flags & (kFlagPre | kFlagBarrier))
+                         : (0x7ffffff << 4));
   }
 
   // One triangular sweep (its levels, then optionally the tail gather as one

@@ -90,6 +90,12 @@ struct StreamProgram {
   std::vector<int> pat;          // pattern blocks (16-byte aligned)
   std::vector<StepIssue> issue;  // per step
   std::vector<int> ring_off;     // per step (consumer lookup)
+  // per step: (last control << 4) | pre/post barrier flags of an accumulation
+  // step, 0x7ffffff << 4 otherwise.  A column tile starting at j0 assembles
+  // only K_hat's lower triangle (u >= j0 + c), so it skips -- neither loads
+  // nor runs -- every accumulation step whose controls all lie below j0,
+  // keeping the step's barriers
+  std::vector<int> skip;
   std::vector<idx> vs_src;       // VS position -> factor slot (F), -1: padding
   idx nnz_vs = 0;
   std::vector<idx> kxu_t_slot, gu_t_slot;  // column-order gathers of K_xu, G_u values

@@ -81,6 +81,15 @@ __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(C) : "memory");
 }
 
+// ring word of a step (engine.cu: ring_word): byte offset in the ring (bits
+// 0-17), the barrier flags of an accumulation step (bit 18 after, bit 19
+// before), and its last control (bits 20-31; 4095: never skipped)
+constexpr unsigned kRwOffMask = 0x3ffffu, kRwPost = 1u << 18, kRwPre = 1u << 19;
+__device__ __forceinline__ bool acc_skipped(unsigned rw, int j0) {
+  const int hi = int(rw >> 20);
+  return hi != 4095 && hi < j0;
+}
+
 // ---------------------------------------------------------------- panel
 // Row r of the K-column panel is K*8 bytes of 16-byte chunks, chunk c at
 // position c ^ sw(r) (host/stream_plan.hpp panel_word); rows are addressed by
@@ -680,10 +689,14 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
             xb2 = unsigned(((e & 1) + f[8]) * 8 + 15) & ~15u;
           }
           unsigned long long* fb = &full[j % kNB];
-          mbar_arrive_tx(fb, unsigned(f[1]) + vb + xb2);
-          bulk_g2s(ring + f[2], a.pat + f[0], unsigned(f[1]), fb);
-          if (vb) bulk_g2s(ring + f[9], vsrc, vb, fb);
-          if (xb2) bulk_g2s(ring + f[10], xsrc, xb2, fb);
+          if (acc_skipped(ring_off[j % P], j0)) {
+            mbar_arrive(fb);  // accumulation step below the tile's triangle: nothing to load
+          } else {
+            mbar_arrive_tx(fb, unsigned(f[1]) + vb + xb2);
+            bulk_g2s(ring + f[2], a.pat + f[0], unsigned(f[1]), fb);
+            if (vb) bulk_g2s(ring + f[9], vsrc, vb, fb);
+            if (xb2) bulk_g2s(ring + f[10], xsrc, xb2, fb);
+          }
         }
         __syncwarp();
       }
@@ -711,7 +724,20 @@ __global__ void __launch_bounds__(C + 32, 512 / C) reduce_stream_kernel(StreamLa
     mbar_wait(&full[j & (kNB - 1)], (j / kNB) & 1);
     tr(2);
     if (stamp && s == s_lo) a.phase[2 * jj + 1] = clock64();
-    const unsigned base = rb + ring_off[jj];
+    const unsigned rw = unsigned(ring_off[jj]);
+    if (acc_skipped(rw, j0)) {
+      // skipped accumulation step (StreamProgram::skip): its barriers only
+      if (rw & kRwPre) consumer_sync<C>();
+      if (rw & kRwPost) consumer_sync<C>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[j & (kNB - 1)]);
+      if (++jj == P) {
+        jj = 0;
+        ++s;
+      }
+      continue;
+    }
+    const unsigned base = rb + (rw & kRwOffMask);
     Hdr h;
     {
       const int4 h0 = ldsi4(base), h1 = ldsi4(base + 16), h2 = ldsi4(base + 32);

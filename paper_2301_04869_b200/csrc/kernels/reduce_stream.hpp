@@ -21,7 +21,7 @@ struct StreamLaunch {
   int list_cap;         // tile list entries (G_u + K_xu columns, each rounded to even)
   const int* pat;       // pattern blocks
   const int* issue;     // StepIssue records (12 ints each)
-  const int* ring_off;  // per step
+  const int* ring_off;  // per step: ring word (reduce_stream.cu kRw*: offset, skip control)
   const double* arr[kStreamArrays];
   long long stride[kStreamArrays];
   DevCsr gu, kxu, kuu;  // transposed views give a tile's columns
