@@ -374,9 +374,12 @@ void Engine::setup_stream() {
     if (defer_tail) {
       ZT.resize(Ms * size_t(n_u) * size_t(rplan.ldy));
       ZT.zero(st);
-      // about three waves of the lower 64 x 64 tiles of K_hat over the SMs
+      // about sixteen CTAs per SM over the lower 64 x 64 tiles of K_hat (up
+      // to five are co-resident; measured reduce_post, same box: 1354/256
+      // 10 -> 32 splits 1.13 -> 0.85 ms, 2869/512 3 -> 16-64 splits 13.8 ->
+      // 9.0-9.3 ms -- three CTAs per SM left the FP64 pipe idle)
       const long long tt = (n_u + 63) / 64, t = tt * (tt + 1) / 2;
-      tail_splits = int(std::max(1LL, std::min<long long>(M, (3LL * sm_count + t / 2) / t)));
+      tail_splits = int(std::max(1LL, std::min<long long>(M, (16LL * sm_count + t / 2) / t)));
       if (const char* e = std::getenv("BIPM_TAIL_SPLITS"))
         tail_splits = std::max(1, std::min(int(M), std::atoi(e)));
     }
