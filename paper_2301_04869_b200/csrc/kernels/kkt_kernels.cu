@@ -674,7 +674,7 @@ __global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, d
                                         double* VS, int M) {
   const long long n1 = (long long)M * P.nnz_f, n2 = (long long)M * nnz_vs;
   const int tl = P.tl, tt = tl * tl;
-  const long long n3 = (long long)M * tt;
+  const long long n3 = 0;  // W' by transpose_w_kernel
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n1 + n2 + n3;
        q += stride) {
@@ -693,6 +693,37 @@ __global__ void refactor_layouts_kernel(DevLu P, const double* __restrict__ F, d
       double* W = D + size_t(s) * 2 * tt;
       W[tt + e] = W[j * tl + i];
     }
+  }
+}
+
+// W' = transpose(W) per scenario through 32 x 32 shared-memory tiles (both
+// sides coalesced; the element-wise form in refactor_layouts_kernel read W
+// with a stride of tl doubles), and the reduction's row-padded copy (Dp, rows
+// of ldw doubles, zero beyond tl) of W, W' or both (slot 0, 1, -1) from the
+// same tiles, which replaces pad_dense_kernel's second pass over D
+__global__ void transpose_w_kernel(double* D, int tl, double* Dp, int ldw, int slot) {
+  __shared__ double t[32][33];
+  const int tt = tl * tl, s = blockIdx.z;
+  double* W = D + size_t(s) * 2 * tt;
+  const int i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;  // W rows i0.., columns j0..
+  const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+  // padded row r of slot k of this scenario (Dp keeps the [M][2][tl][ldw]
+  // layout when only one slot is written, as pad_dense_kernel does)
+  auto prow = [&](int k, int r) -> double* {
+    return Dp + ((size_t(s) * 2 + k) * tl + r) * ldw;
+  };
+  for (int r = y; r < 32; r += 8) {
+    const int i = i0 + r, j = j0 + x;
+    const double v = i < tl && j < tl ? W[size_t(i) * tl + j] : 0.0;
+    t[r][x] = v;
+    if (Dp && slot != 1 && i < tl && j < ldw) prow(0, i)[j] = v;
+  }
+  __syncthreads();
+  for (int r = y; r < 32; r += 8) {  // W'(j0 + r, i0 + x) = W(i0 + x, j0 + r)
+    const int i = j0 + r, j = i0 + x;
+    if (i >= tl) continue;
+    if (j < tl) W[tt + size_t(i) * tl + j] = t[x][r];
+    if (Dp && slot != 0 && j < ldw) prow(1, i)[j] = j < tl ? t[x][r] : 0.0;
   }
 }
 
@@ -1180,6 +1211,7 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                         int nnz_vs, double* VS, double* Dp, double* scale, cudaStream_t st,
                         int dp_slot, cudaEvent_t after_levels) {
   if (M <= 0) return;
+  bool padded = false;  // Dp written by transpose_w_kernel
   refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
   check_launch("refactor_levels");
@@ -1191,6 +1223,13 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
     refactor_tail_kernel<kLuBlock><<<M, kLuBlock, smem, st>>>(P, F, FT, D, scale, status,
                                                               piv_tol, vs_src, nnz_vs, VS);
   } else if (cgj_launch(P, M, F, D, scale, status, piv_tol, st)) {
+    if (P.tl > 0) {
+      const int nb = (P.tl + 31) / 32;
+      transpose_w_kernel<<<dim3(nb, nb, M), 256, 0, st>>>(D, P.tl, Dp, (P.tl + 15) & ~15,
+                                                         dp_slot);
+      note_launch();
+      padded = true;
+    }
     refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
                                                      M);
   } else {
@@ -1283,12 +1322,19 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
           nn(h, h, r, -1.0, 1.0, T1, r, Cb, tl, Wb, tl);             // W11 = Ai - T1 W21
         };
     inv(0, tl, 1, 1, block_env, 0);
+    if (P.tl > 0) {
+      const int nb = (P.tl + 31) / 32;
+      transpose_w_kernel<<<dim3(nb, nb, M), 256, 0, st>>>(D, P.tl, Dp, (P.tl + 15) & ~15,
+                                                         dp_slot);
+      note_launch();
+      padded = true;
+    }
     refactor_layouts_kernel<<<4 * 148, 512, 0, st>>>(P, F, FT, D, vs_src, VS ? nnz_vs : 0, VS,
                                                      M);
   }
   note_launch();
   check_launch("refactor_tail");
-  if (Dp && P.tl > 0) {
+  if (Dp && P.tl > 0 && !padded) {
     const int ldw = (P.tl + 15) & ~15;
     const long long n = (long long)M * (dp_slot >= 0 ? 1 : 2) * P.tl * ldw;
     pad_dense_kernel<<<int(std::min<long long>((n + 255) / 256, 8 * 148)), 256, 0, st>>>(
