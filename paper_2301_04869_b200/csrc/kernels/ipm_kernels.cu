@@ -342,25 +342,45 @@ __global__ void condensed_rhs_kernel(IpmDims d, DevCsr hx, DevCsr hu, const doub
   if (id >= (long long)d.M * per) return;
   const int s = int(id / per), c = int(id % per);
   const size_t so = size_t(s) * d.m;
-  if (c < d.n_x) {
-    const double* v = hxv + size_t(s) * hx.nnz;
-    double y = r1x[size_t(s) * d.n_x + c];
-    for (int q = hx.t_ptr[c]; q < hx.t_ptr[c + 1]; ++q) {
-      const int r = hx.t_row[q];
-      const double t = sigma_s[so + r] * r4[so + r] - r2[so + r];
-      y += v[hx.t_slot[q]] * (1.0 * t);
+  // y += H'(sigma_s r4 - r2) over the column's entries in order; four
+  // entries' index and value loads in flight before their (unchanged) sums
+  auto column = [&](const DevCsr& H, const double* v, int col, double y) {
+    int q = H.t_ptr[col];
+    const int q1 = H.t_ptr[col + 1];
+    for (; q + 4 <= q1; q += 4) {
+      int rr[4], sl[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        rr[u] = H.t_row[q + u];
+        sl[u] = H.t_slot[q + u];
+      }
+      double sg[4], a4[4], b2[4], hv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        sg[u] = sigma_s[so + rr[u]];
+        a4[u] = r4[so + rr[u]];
+        b2[u] = r2[so + rr[u]];
+        hv[u] = v[sl[u]];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double t = sg[u] * a4[u] - b2[u];
+        y += hv[u] * (1.0 * t);
+      }
     }
-    rhat1[size_t(s) * d.n_x + c] = y;
+    for (; q < q1; ++q) {
+      const int r = H.t_row[q];
+      const double t = sigma_s[so + r] * r4[so + r] - r2[so + r];
+      y += v[H.t_slot[q]] * (1.0 * t);
+    }
+    return y;
+  };
+  if (c < d.n_x) {
+    rhat1[size_t(s) * d.n_x + c] =
+        column(hx, hxv + size_t(s) * hx.nnz, c, r1x[size_t(s) * d.n_x + c]);
   } else {
     const int cu = c - d.n_x;
-    const double* v = huv + size_t(s) * hu.nnz;
-    double y = 0.0;
-    for (int q = hu.t_ptr[cu]; q < hu.t_ptr[cu + 1]; ++q) {
-      const int r = hu.t_row[q];
-      const double t = sigma_s[so + r] * r4[so + r] - r2[so + r];
-      y += v[hu.t_slot[q]] * (1.0 * t);
-    }
-    part_u[size_t(s) * d.n_u + cu] = y;
+    part_u[size_t(s) * d.n_u + cu] = column(hu, huv + size_t(s) * hu.nnz, cu, 0.0);
   }
 }
 

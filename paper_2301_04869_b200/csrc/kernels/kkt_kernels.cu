@@ -1022,8 +1022,24 @@ __global__ void recover_slack_kernel(DevCsr hx, DevCsr hu, int m, int n_x, int M
   const double* hxs = hxv + size_t(s) * hx.nnz;
   const double* hus = huv + size_t(s) * hu.nnz;
   const double* pxs = px + size_t(s) * n_x;
+  // row i of H_x p_x in order, four entries' loads in flight
   double a = 0.0;
-  for (int t = hx.ptr[i]; t < hx.ptr[i + 1]; ++t) a += hxs[t] * pxs[hx.ind[t]];
+  int t = hx.ptr[i];
+  const int t1 = hx.ptr[i + 1];
+  for (; t + 4 <= t1; t += 4) {
+    int ci[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ci[u] = hx.ind[t + u];
+    double hv[4], xv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      hv[u] = hxs[t + u];
+      xv[u] = pxs[ci[u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) a += hv[u] * xv[u];
+  }
+  for (; t < t1; ++t) a += hxs[t] * pxs[hx.ind[t]];
   double hp = 0.0 + 1.0 * a;
   double b = 0.0;
   for (int t = hu.ptr[i]; t < hu.ptr[i + 1]; ++t) b += hus[t] * pu[hu.ind[t]];
