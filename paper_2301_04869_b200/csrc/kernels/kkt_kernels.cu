@@ -1228,7 +1228,19 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                         int dp_slot, cudaEvent_t after_levels) {
   if (M <= 0) return;
   bool padded = false;  // Dp written by transpose_w_kernel
-  refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
+  // few scenarios (one CTA each, most SMs idle): 1024 threads per scenario
+  // shorten each level's pass (BIPM_LEVELS_BLOCK=512|1024 for experiments)
+  static const int levels_env = [] {
+    const char* e = std::getenv("BIPM_LEVELS_BLOCK");
+    return e ? std::atoi(e) : 0;
+  }();
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const bool wide = levels_env ? levels_env == 1024 : 2 * M <= sms;
+  if (wide)
+    refactor_levels_kernel<1024><<<M, 1024, 0, st>>>(P, gx, nnz_gx, F, scale);
+  else
+    refactor_levels_kernel<512><<<M, 512, 0, st>>>(P, gx, nnz_gx, F, scale);
   note_launch();
   check_launch("refactor_levels");
   if (after_levels) cudaEventRecord(after_levels, st);
