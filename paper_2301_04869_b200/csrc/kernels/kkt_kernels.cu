@@ -1228,15 +1228,16 @@ void launch_lu_refactor(const DevLu& P, int M, const double* gx, int nnz_gx, dou
                         int dp_slot, cudaEvent_t after_levels) {
   if (M <= 0) return;
   bool padded = false;  // Dp written by transpose_w_kernel
-  // few scenarios (one CTA each, most SMs idle): 1024 threads per scenario
-  // shorten each level's pass (BIPM_LEVELS_BLOCK=512|1024 for experiments)
+  // up to one scenario per SM: 1024 threads per scenario shorten each
+  // level's pass (measured refactor: 1354/32 0.84 -> 0.74 ms, 1354/148 1.46
+  // -> 1.36, 9241/128 33.9 -> 27.5; BIPM_LEVELS_BLOCK=512|1024 for experiments)
   static const int levels_env = [] {
     const char* e = std::getenv("BIPM_LEVELS_BLOCK");
     return e ? std::atoi(e) : 0;
   }();
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const bool wide = levels_env ? levels_env == 1024 : 2 * M <= sms;
+  const bool wide = levels_env ? levels_env == 1024 : M <= sms;
   if (wide)
     refactor_levels_kernel<1024><<<M, 1024, 0, st>>>(P, gx, nnz_gx, F, scale);
   else
