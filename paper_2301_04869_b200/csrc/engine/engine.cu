@@ -332,8 +332,12 @@ void Engine::setup_stream() {
   adj_identity = adj;
   if (const char* e = std::getenv("BIPM_TAIL_DEFER")) defer_tail = std::atoi(e) != 0;
   defer_tail = defer_tail && adj && L.tl > 0;
+  // producer lookahead in steps (< the kernel's 32 mbarrier slots;
+  // BIPM_LOOKAHEAD for experiments)
+  int lookahead = kStreamLookahead;
+  if (const char* e = std::getenv("BIPM_LOOKAHEAD")) lookahead = std::max(1, std::min(31, std::atoi(e)));
   sprog = build_stream_program(L, D.g.u, D.kxx.out, D.kxu.out, n_u, K, best.C, ring,
-                               kStreamLookahead, presolve ? &rplan : nullptr, adj, defer_tail);
+                               lookahead, presolve ? &rplan : nullptr, adj, defer_tail);
   if (presolve) {
     rp_op_ptr.upload(rplan.op_ptr);
     rp_ops.upload(rplan.ops.empty() ? std::vector<idx>(4, 0) : rplan.ops);
