@@ -1450,6 +1450,21 @@ void launch_affine_mix(const double* a, const double* b, double t, long long len
   check_launch("affine_mix");
 }
 
+// 1024 threads per scenario while there is at most one scenario per SM
+// (measured: 9241/128 rhs 3.85 -> 2.57 ms, recovery 3.70 -> 2.50 ms against
+// 512 threads; 1354/128 0.25 -> 0.22 ms; BIPM_RHS_WIDE_M overrides the limit)
+static bool wide_single_rhs(int M) {
+  static const int lim = [] {
+    const char* e = std::getenv("BIPM_RHS_WIDE_M");
+    if (e) return std::atoi(e);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return M <= lim;
+}
+
 void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
   if (a.M <= 0) return;
   const size_t smem = single_rhs_smem(a.n_x);
@@ -1465,8 +1480,8 @@ void launch_reduce_rhs(const RhsLaunch& a, cudaStream_t st) {
   }
   // latency-bound level sweeps: more threads per scenario while the scenarios
   // leave SMs free (measured at 1354: 256 -> 512 threads 0.44 -> 0.35 ms;
-  // 1024 threads 0.29 ms at 32 scenarios, 0.56 ms at 256)
-  if (a.M <= 96)
+  // 1024 threads 0.29 ms at 32 scenarios, 0.56 ms at 256; wide_single_rhs)
+  if (wide_single_rhs(a.M))
     reduce_rhs_kernel<1024><<<a.M, 1024, smem, st>>>(a, scratch, smem ? 1 : 0);
   else
     reduce_rhs_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
@@ -1489,8 +1504,8 @@ void launch_recover_state(const RecoverLaunch& a, cudaStream_t st) {
   }
   // latency-bound level sweeps: more threads per scenario while the scenarios
   // leave SMs free (measured at 1354: 256 -> 512 threads 0.44 -> 0.35 ms;
-  // 1024 threads 0.29 ms at 32 scenarios, 0.56 ms at 256)
-  if (a.M <= 96)
+  // 1024 threads 0.29 ms at 32 scenarios, 0.56 ms at 256; wide_single_rhs)
+  if (wide_single_rhs(a.M))
     recover_state_kernel<1024><<<a.M, 1024, smem, st>>>(a, scratch, smem ? 1 : 0);
   else
     recover_state_kernel<kSolveBlock><<<a.M, kSolveBlock, smem, st>>>(a, scratch, smem ? 1 : 0);
