@@ -244,8 +244,14 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
   for (int c0 = 0; c0 < n; c0 += kNb) {
     const int w = min(kNb, n - c0);
     stamp();
-    // (1) diagonal block on CTA 0, warp 0
-    if (blockIdx.x == 0 && warp == 0) {
+    // (1) every CTA factors the diagonal block itself (warp 0; identical
+    // inputs give an identical factor) into its shared-memory copy for the
+    // panel solve, CTA 0 writes it back: no grid barrier between the factor
+    // and the panel solve, and no reload of L11
+    double(*L)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
+    double* rdiag = buf + kNb * (kNb + 1);  // reciprocals of the diagonal
+    __shared__ int fail_s;
+    if (warp == 0) {
       const int r = lane;
       double a[kNb];
 #pragma unroll
@@ -253,46 +259,30 @@ __global__ void __launch_bounds__(128) cholesky_coop_kernel(double* K, int n, in
         a[c] = (c < w && r < w && c <= r) ? K[size_t(c0 + c) * n + c0 + r] : 0.0;
       stamp();
       double piv = 0.0;
-      const int f = warp_chol32(a, w, r, buf, &piv);
+      const int f = warp_chol32(a, w, r, rdiag + kNb, &piv);
+      if (r == 0) fail_s = f;
       if (f) {
-        if (r == 0) {
+        if (blockIdx.x == 0 && r == 0) {
           info[0] = c0 + f;
           reinterpret_cast<double*>(info)[2] = piv;
         }
       } else {
 #pragma unroll
-        for (int c = 0; c < kNb; ++c)
-          if (c < w && r < w && c <= r) K[size_t(c0 + c) * n + c0 + r] = a[c];
+        for (int c = 0; c < kNb; ++c) {
+          const bool in = c < w && r < w && c <= r;
+          L[r][c] = in ? a[c] : 0.0;
+          if (in && blockIdx.x == 0) K[size_t(c0 + c) * n + c0 + r] = a[c];
+        }
       }
     }
     stamp();
-    grid.sync();
+    __syncthreads();
     stamp();
-    if (*(volatile int*)info) return;
+    if (fail_s) return;  // every CTA reached the same verdict
     const int rows = n - c0 - w;
     if (rows <= 0) break;
     // (2) L21 = A21 L11^{-T}, one thread per row
     {
-      double(*L)[kNb + 1] = reinterpret_cast<double(*)[kNb + 1]>(buf);
-      double* rdiag = buf + kNb * (kNb + 1);  // reciprocals of the diagonal
-      {
-        // the diagonal block, zero-padded beyond w: all eight loads of a
-        // thread in flight, then the stores (a serial load/store loop cost
-        // ~5k cycles per panel)
-        constexpr int kPer = kNb * kNb / 128;
-        double v[kPer];
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int q = tid + u * 128, rr = q % kNb, cc = q / kNb;
-          v[u] = (rr < w && cc < w && cc <= rr) ? K[size_t(c0 + cc) * n + c0 + rr] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-          const int q = tid + u * 128;
-          L[q % kNb][q / kNb] = v[u];
-        }
-      }
-      __syncthreads();
       if (tid < kNb) rdiag[tid] = tid < w ? 1.0 / L[tid][tid] : 1.0;
       __syncthreads();
       for (int rb = blockIdx.x * 128; rb < rows; rb += gridDim.x * 128) {
